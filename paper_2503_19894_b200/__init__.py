@@ -1,0 +1,565 @@
+"""tilesim-b200: the B200 (sm_100a) gate-application path of CAST/tilesim.
+
+Python mirror of the reference's operator surface, bound through the C ABI of
+``libtilesim_b200.so`` (include/tilesim_cuda.h).  Names follow the reference:
+
+  gatecore / circuit  make_named_gate, gen_benchmark, parse_circuit,
+                      serialize_circuit, Circuit               (proj/src/circuit.cpp,
+                                                                SPEC.md:136-198)
+  fusion              run_fusion, FusionConfig, CostModel, estimate_cost
+                                                               
+  kernel              plan_kernel -> KernelPlan, apply_kernel
+  sim                 Statevector, init_zero_state, run_circuit, norm,
+                      compare_states
+
+There is no CPU fallback: device calls raise SimError on a host without a
+CUDA device, and importing this package raises ImportError when the shared
+library has not been built (``python -c "import __graft_entry__ as g; g.build()"``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtilesim_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make -C {_HERE}/csrc` (no CPU fallback exists)")
+
+_lib = C.CDLL(LIB_PATH)
+
+_u64 = C.c_uint64
+_i64 = C.c_int64
+_vp = C.c_void_p
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+
+class TilesimError(RuntimeError):
+    code = 3
+
+
+class ParseError(TilesimError):
+    code = 1
+
+
+class ConfigError(TilesimError):
+    code = 2
+
+
+class SimError(TilesimError):
+    code = 3
+
+
+_ERRORS = {1: ParseError, 2: ConfigError, 3: SimError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise _ERRORS.get(rc, TilesimError)(_lib.tsg_last_error().decode())
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("k", C.c_int), ("kernel_class", C.c_int), ("sub_k", C.c_int), ("n_controls", C.c_int),
+                ("sparse", C.c_int), ("op_count", _u64), ("entry_ops", _u64), ("loop_count", _u64),
+                ("touched_fraction", C.c_double)]
+
+
+class RunReport(C.Structure):
+    _fields_ = [("planning_s", C.c_double), ("execution_s", C.c_double), ("gates", _u64), ("launches", _u64),
+                ("bytes", _u64), ("touched_bytes", _u64), ("total_op_count", _u64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class _FusionConfigC(C.Structure):
+    _fields_ = [("mode", C.c_int), ("k_max", C.c_int), ("max_op_count", _i64), ("agglomerative", C.c_int),
+                ("multi_traversal", C.c_int), ("zero_tol", C.c_double), ("one_tol", C.c_double),
+                ("max_traversals", C.c_int), ("threads", C.c_int)]
+
+
+class _FusionStatsC(C.Structure):
+    _fields_ = [("original_gate_count", _u64), ("fused_block_count", _u64), ("total_op_count", _u64),
+                ("compression_ratio", C.c_double), ("fusion_wall_time", C.c_double)]
+
+
+def _sig(name, args, res=C.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+
+
+_sig("tsg_last_error", [], C.c_char_p)
+_sig("tsg_version", [], C.c_char_p)
+_sig("tsg_device_count", [_ip])
+_sig("tsg_ctx_create", [C.c_int, C.POINTER(_vp)])
+_sig("tsg_ctx_destroy", [_vp])
+_sig("tsg_state_create", [_vp, C.c_int, C.c_int, C.POINTER(_vp)])
+_sig("tsg_state_destroy", [_vp])
+_sig("tsg_state_info", [_vp, _ip, _ip])
+_sig("tsg_state_init_zero", [_vp])
+_sig("tsg_state_init_basis", [_vp, _u64])
+_sig("tsg_state_init_random", [_vp, _u64])
+_sig("tsg_state_upload", [_vp, _dp, _dp])
+_sig("tsg_state_download", [_vp, _dp, _dp])
+_sig("tsg_state_download_range", [_vp, _u64, _u64, _dp, _dp])
+_sig("tsg_state_copy", [_vp, _vp])
+_sig("tsg_synchronize", [_vp])
+_sig("tsg_timer_begin", [_vp])
+_sig("tsg_timer_end", [_vp, _dp])
+_sig("tsg_plan_create", [_vp, C.c_int, C.c_int, _ip, _dp, C.c_double, C.c_double, C.c_int, C.POINTER(_vp)])
+_sig("tsg_plan_destroy", [_vp])
+_sig("tsg_plan_info_get", [_vp, C.POINTER(PlanInfo)])
+_sig("tsg_apply", [_vp, _vp, _dp, _u64, _u64])
+_sig("tsg_norm", [_vp, _dp])
+_sig("tsg_compare", [_vp, _dp, _dp, _dp])
+_sig("tsg_compare_states", [_vp, _vp, _dp])
+_sig("tsg_overlap", [_vp, _vp, _dp, _dp])
+_sig("tsg_program_create", [_vp, _vp, C.c_double, C.c_double, C.c_int, C.POINTER(_vp)])
+_sig("tsg_program_destroy", [_vp])
+_sig("tsg_program_run", [_vp, _vp, C.c_int, C.POINTER(RunReport)])
+_sig("tsg_program_enqueue", [_vp, _vp, C.c_int])
+_sig("tsg_program_run_profiled", [_vp, _vp, _dp, C.POINTER(RunReport)])
+_sig("tsg_program_gate_info", [_vp, _u64, C.POINTER(PlanInfo)])
+_sig("tsg_bench_cost_model", [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _u64, C.POINTER(_vp)])
+_sig("tsc_circuit_create", [C.c_int, C.POINTER(_vp)])
+_sig("tsc_circuit_destroy", [_vp])
+_sig("tsc_circuit_copy", [_vp, C.POINTER(_vp)])
+_sig("tsc_circuit_add_named", [_vp, C.c_char_p, _dp, C.c_int, _ip, C.c_int])
+_sig("tsc_circuit_add_matrix", [_vp, C.c_int, _ip, _dp])
+_sig("tsc_circuit_n_qubits", [_vp, _ip])
+_sig("tsc_circuit_n_gates", [_vp, C.POINTER(_u64)])
+_sig("tsc_circuit_gate", [_vp, _u64, _ip, _ip, _dp])
+_sig("tsc_circuit_gate_name", [_vp, _u64], C.c_char_p)
+_sig("tsc_gen_benchmark", [C.c_char_p, C.c_int, C.c_int, _u64, C.POINTER(_vp)])
+_sig("tsc_parse_circuit", [C.c_char_p, C.POINTER(_vp)])
+_sig("tsc_serialize_circuit", [_vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)])
+_sig("tsc_run_fusion", [_vp, C.POINTER(_FusionConfigC), _vp, C.POINTER(_vp), C.POINTER(_FusionStatsC)])
+_sig("tsc_cost_model_parse", [C.c_char_p, C.POINTER(_vp)])
+_sig("tsc_cost_model_destroy", [_vp])
+_sig("tsc_cost_model_serialize", [_vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)])
+_sig("tsc_estimate_cost", [_vp, C.c_int, _u64, C.c_int, C.c_int, _dp])
+
+KERNEL_CLASSES = ("identity", "diagonal", "direct", "tile")
+
+
+def version() -> str:
+    return _lib.tsg_version().decode()
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _lib.tsg_device_count(C.byref(n))
+    return n.value
+
+
+def _ints(xs):
+    xs = list(xs)
+    return (C.c_int * max(1, len(xs)))(*xs)
+
+
+def _matrix_arg(m) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(m, dtype=np.complex128))
+    if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] & (a.shape[0] - 1):
+        raise ConfigError("matrix must be square with a power-of-two dimension")
+    return a.view(np.float64).reshape(-1)
+
+
+def _read_text(fn, handle) -> str:
+    need = C.c_size_t()
+    _check(fn(handle, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    _check(fn(handle, buf, need.value, C.byref(need)))
+    return buf.value.decode()
+
+
+# ============================================================ circuit IR ===
+@dataclass
+class Gate:
+    """A k-qubit operator on strictly increasing targets (gate.hpp:17-24)."""
+    targets: list
+    matrix: np.ndarray
+    name: str = ""
+
+    @property
+    def k(self) -> int:
+        return len(self.targets)
+
+
+class Circuit:
+    """Program-ordered gate list (circuit.hpp:12-15), owned by the C++ side."""
+
+    def __init__(self, n_qubits: int = 0, _handle=None):
+        if _handle is None:
+            h = _vp()
+            _check(_lib.tsc_circuit_create(n_qubits, C.byref(h)))
+            _handle = h.value
+        self._h = _handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.tsc_circuit_destroy(self._h)
+            self._h = None
+
+    @property
+    def n_qubits(self) -> int:
+        n = C.c_int()
+        _check(_lib.tsc_circuit_n_qubits(self._h, C.byref(n)))
+        return n.value
+
+    def __len__(self) -> int:
+        n = _u64()
+        _check(_lib.tsc_circuit_n_gates(self._h, C.byref(n)))
+        return n.value
+
+    def add(self, name: str, qubits, params=()):
+        """make_named_gate(name, params, qubits) appended; qubits in argument order."""
+        p = (C.c_double * max(1, len(params)))(*params)
+        _check(_lib.tsc_circuit_add_named(self._h, name.encode(), p, len(params), _ints(qubits), len(qubits)))
+        return self
+
+    def add_matrix(self, qubits, matrix):
+        """Raw unitary in the argument order of `qubits` (make_gate_arg_order)."""
+        m = _matrix_arg(matrix)
+        _check(_lib.tsc_circuit_add_matrix(self._h, len(qubits), _ints(qubits), m.ctypes.data_as(_dp)))
+        return self
+
+    def gate(self, i: int) -> Gate:
+        k = C.c_int()
+        _check(_lib.tsc_circuit_gate(self._h, i, C.byref(k), None, None))
+        t = (C.c_int * k.value)()
+        m = np.zeros(2 * (1 << (2 * k.value)))
+        _check(_lib.tsc_circuit_gate(self._h, i, None, t, m.ctypes.data_as(_dp)))
+        d = 1 << k.value
+        return Gate(list(t), m.view(np.complex128).reshape(d, d).copy(),
+                    _lib.tsc_circuit_gate_name(self._h, i).decode())
+
+    def gates(self):
+        return [self.gate(i) for i in range(len(self))]
+
+    def copy(self) -> "Circuit":
+        h = _vp()
+        _check(_lib.tsc_circuit_copy(self._h, C.byref(h)))
+        return Circuit(_handle=h.value)
+
+    def serialize(self) -> str:
+        return _read_text(_lib.tsc_serialize_circuit, self._h)
+
+
+def gen_benchmark(kind: str, n: int, depth: int = 1, seed: int = 0) -> Circuit:
+    """QFT ALA RQC QVC IQP HES and QAOA; recipes in DESIGN.md §3."""
+    h = _vp()
+    _check(_lib.tsc_gen_benchmark(kind.lower().encode(), n, depth, seed, C.byref(h)))
+    return Circuit(_handle=h.value)
+
+
+def parse_circuit(text: str) -> Circuit:
+    h = _vp()
+    _check(_lib.tsc_parse_circuit(text.encode(), C.byref(h)))
+    return Circuit(_handle=h.value)
+
+
+def serialize_circuit(c: Circuit) -> str:
+    return c.serialize()
+
+
+def make_named_gate(name: str, params, qubits) -> Gate:
+    c = Circuit(max(qubits) + 1)
+    c.add(name, qubits, params)
+    return c.gate(0)
+
+
+# ================================================================ fusion ===
+@dataclass
+class FusionConfig:
+    """SPEC.md:311-315.  mode: 'none' | 'size-only' | 'adaptive'."""
+    k_max: int = 5
+    max_op_count: int | None = None
+    mode: str = "size-only"
+    agglomerative: bool = True
+    multi_traversal: bool = True
+    zero_tol: float = 1e-8
+    one_tol: float = 1e-8
+    max_traversals: int = 64
+    threads: int = 1
+
+    @staticmethod
+    def paper_cpu() -> "FusionConfig":
+        return FusionConfig(k_max=7, max_op_count=4096, mode="adaptive")
+
+    def _c(self) -> _FusionConfigC:
+        modes = {"none": 0, "size-only": 1, "size": 1, "adaptive": 2}
+        if self.mode not in modes:
+            raise ConfigError(f"unknown fusion mode {self.mode!r}")
+        return _FusionConfigC(modes[self.mode], self.k_max, -1 if self.max_op_count is None else self.max_op_count,
+                              int(self.agglomerative), int(self.multi_traversal), self.zero_tol, self.one_tol,
+                              self.max_traversals, self.threads)
+
+
+class CostModel:
+    """Measured (k, op_count, threads) -> seconds-per-group table."""
+
+    def __init__(self, text: str | None = None, _handle=None):
+        if _handle is None:
+            h = _vp()
+            _check(_lib.tsc_cost_model_parse((text or "").encode(), C.byref(h)))
+            _handle = h.value
+        self._h = _handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.tsc_cost_model_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def load(path: str) -> "CostModel":
+        if not os.path.exists(path):
+            raise ParseError(f"cost model file not found: {path}")
+        with open(path) as f:
+            return CostModel(f.read())
+
+    def save(self, path: str) -> None:
+        with open(path, "w") as f:
+            f.write(self.serialize())
+
+    def serialize(self) -> str:
+        return _read_text(_lib.tsc_cost_model_serialize, self._h)
+
+    def estimate(self, k: int, op_count: int, threads: int, n: int) -> float:
+        out = C.c_double()
+        _check(_lib.tsc_estimate_cost(self._h, k, op_count, threads, n, C.byref(out)))
+        return out.value
+
+
+def run_fusion(c: Circuit, cfg: FusionConfig | None = None, cost_model: CostModel | None = None):
+    """run_fusion(c, cfg, cm) -> (fused Circuit, FusionStats dict)."""
+    cfg = cfg or FusionConfig()
+    h = _vp()
+    st = _FusionStatsC()
+    cc = cfg._c()
+    _check(_lib.tsc_run_fusion(c._h, C.byref(cc), cost_model._h if cost_model else None, C.byref(h), C.byref(st)))
+    stats = {f: getattr(st, f) for f, _ in _FusionStatsC._fields_}
+    return Circuit(_handle=h.value), stats
+
+
+# ================================================================ device ===
+class Context:
+    """One B200 (tsg_ctx).  Raises SimError when no CUDA device is present."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        _check(_lib.tsg_ctx_create(device, C.byref(h)))
+        self._h = h.value
+        self.device = device
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.tsg_ctx_destroy(self._h)
+            self._h = None
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class Statevector:
+    """Device-resident SoA statevector; precision 'f64' | 'f32'."""
+
+    def __init__(self, n: int, precision: str = "f64", ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        bits = {"f64": 64, "f32": 32, "c128": 64, "c64": 32}[precision]
+        h = _vp()
+        _check(_lib.tsg_state_create(self.ctx._h, n, bits, C.byref(h)))
+        self._h = h.value
+        self.n = n
+        self.precision_bits = bits
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.tsg_state_destroy(self._h)
+            self._h = None
+
+    def init_zero(self):
+        _check(_lib.tsg_state_init_zero(self._h))
+        return self
+
+    def init_basis(self, index: int):
+        _check(_lib.tsg_state_init_basis(self._h, index))
+        return self
+
+    def init_random(self, seed: int):
+        _check(_lib.tsg_state_init_random(self._h, seed))
+        return self
+
+    def upload(self, re: np.ndarray, im: np.ndarray):
+        re = np.ascontiguousarray(re, dtype=np.float64)
+        im = np.ascontiguousarray(im, dtype=np.float64)
+        if re.size != 1 << self.n or im.size != 1 << self.n:
+            raise ConfigError("host arrays must have 2^n entries")
+        _check(_lib.tsg_state_upload(self._h, re.ctypes.data_as(_dp), im.ctypes.data_as(_dp)))
+        return self
+
+    def download(self, begin: int = 0, count: int | None = None):
+        count = (1 << self.n) - begin if count is None else count
+        re = np.empty(count)
+        im = np.empty(count)
+        _check(_lib.tsg_state_download_range(self._h, begin, count, re.ctypes.data_as(_dp), im.ctypes.data_as(_dp)))
+        return re, im
+
+    def amplitudes(self) -> np.ndarray:
+        re, im = self.download()
+        return re + 1j * im
+
+    def synchronize(self):
+        _check(_lib.tsg_synchronize(self._h))
+
+    def timer_begin(self):
+        _check(_lib.tsg_timer_begin(self._h))
+
+    def timer_end(self) -> float:
+        out = C.c_double()
+        _check(_lib.tsg_timer_end(self._h, C.byref(out)))
+        return out.value
+
+    def norm(self) -> float:
+        out = C.c_double()
+        _check(_lib.tsg_norm(self._h, C.byref(out)))
+        return out.value
+
+    def copy_from(self, other: "Statevector"):
+        _check(_lib.tsg_state_copy(self._h, other._h))
+        return self
+
+
+def init_zero_state(n: int, precision: str = "f64") -> Statevector:
+    return Statevector(n, precision).init_zero()
+
+
+def norm(sv: Statevector) -> float:
+    return sv.norm()
+
+
+def compare_states(a: Statevector, b) -> float:
+    """max_i |a_i - b_i| against another Statevector or host (re, im) arrays."""
+    out = C.c_double()
+    if isinstance(b, Statevector):
+        _check(_lib.tsg_compare_states(a._h, b._h, C.byref(out)))
+    else:
+        re = np.ascontiguousarray(b[0], dtype=np.float64)
+        im = np.ascontiguousarray(b[1], dtype=np.float64)
+        _check(_lib.tsg_compare(a._h, re.ctypes.data_as(_dp), im.ctypes.data_as(_dp), C.byref(out)))
+    return out.value
+
+
+def overlap(a: Statevector, b: Statevector) -> complex:
+    re, im = C.c_double(), C.c_double()
+    _check(_lib.tsg_overlap(a._h, b._h, C.byref(re), C.byref(im)))
+    return complex(re.value, im.value)
+
+
+class KernelPlan:
+    """plan_kernel(g, n, s=0, zero_tol, one_tol, runtime_matrix)."""
+
+    def __init__(self, gate: Gate, n: int, zero_tol=1e-8, one_tol=1e-8, runtime_matrix=False, ctx=None):
+        self.ctx = ctx or _default_ctx
+        m = _matrix_arg(gate.matrix)
+        h = _vp()
+        _check(_lib.tsg_plan_create(self.ctx._h if self.ctx else None, n, gate.k, _ints(gate.targets),
+                                    m.ctypes.data_as(_dp), zero_tol, one_tol, int(runtime_matrix), C.byref(h)))
+        self._h = h.value
+        self.gate = gate
+        self.n = n
+        self.runtime_matrix = runtime_matrix
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.tsg_plan_destroy(self._h)
+            self._h = None
+
+    def info(self) -> dict:
+        pi = PlanInfo()
+        _check(_lib.tsg_plan_info_get(self._h, C.byref(pi)))
+        d = {f: getattr(pi, f) for f, _ in PlanInfo._fields_}
+        d["kernel"] = KERNEL_CLASSES[pi.kernel_class]
+        return d
+
+
+def plan_kernel(gate: Gate, n: int, s: int = 0, zero_tol=1e-8, one_tol=1e-8, runtime_matrix=False) -> KernelPlan:
+    if s != 0:
+        raise ConfigError("the B200 kernels use the GPU ABI's s = 0 loop (PAPER.md:380)")
+    return KernelPlan(gate, n, zero_tol, one_tol, runtime_matrix)
+
+
+def apply_kernel(plan: KernelPlan, sv: Statevector, matrix_override=None, t_begin: int = 0, t_end: int | None = None):
+    """apply_kernel(plan, state, override, t_begin, t_end) over s = 0 groups."""
+    ov = None
+    if matrix_override is not None:
+        arr = _matrix_arg(matrix_override)
+        ov = arr.ctypes.data_as(_dp)
+    _check(_lib.tsg_apply(sv._h, plan._h, ov, t_begin, (1 << 64) - 1 if t_end is None else t_end))
+
+
+class Program:
+    """A fused circuit planned once and replayed (CUDA graph) -- run_circuit's engine."""
+
+    def __init__(self, fused: Circuit, precision: str = "f64", zero_tol=1e-8, one_tol=1e-8, ctx=None):
+        self.ctx = ctx or default_context()
+        bits = {"f64": 64, "f32": 32, "c128": 64, "c64": 32}[precision]
+        h = _vp()
+        _check(_lib.tsg_program_create(self.ctx._h, fused._h, zero_tol, one_tol, bits, C.byref(h)))
+        self._h = h.value
+        self.n_gates = len(fused)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.tsg_program_destroy(self._h)
+            self._h = None
+
+    def run(self, sv: Statevector, use_graph: bool = True) -> dict:
+        r = RunReport()
+        _check(_lib.tsg_program_run(sv._h, self._h, int(use_graph), C.byref(r)))
+        return r.as_dict()
+
+    def enqueue(self, sv: Statevector, use_graph: bool = True) -> None:
+        """Asynchronous run on the state's stream (time it with sv.timer_begin/end)."""
+        _check(_lib.tsg_program_enqueue(sv._h, self._h, int(use_graph)))
+
+    def run_profiled(self, sv: Statevector):
+        secs = np.zeros(max(1, self.n_gates))
+        r = RunReport()
+        _check(_lib.tsg_program_run_profiled(sv._h, self._h, secs.ctypes.data_as(_dp), C.byref(r)))
+        return secs[: self.n_gates], r.as_dict()
+
+    def gate_info(self, i: int) -> dict:
+        pi = PlanInfo()
+        _check(_lib.tsg_program_gate_info(self._h, i, C.byref(pi)))
+        d = {f: getattr(pi, f) for f, _ in PlanInfo._fields_}
+        d["kernel"] = KERNEL_CLASSES[pi.kernel_class]
+        return d
+
+
+def run_circuit(c: Circuit, sv: Statevector, zero_tol=1e-8, one_tol=1e-8, use_graph=True) -> dict:
+    """run_circuit: plan every gate, apply in order on the device."""
+    prec = "f64" if sv.precision_bits == 64 else "f32"
+    prog = Program(c, prec, zero_tol, one_tol, sv.ctx)
+    return prog.run(sv, use_graph)
+
+
+def bench_cost_model(bench_n: int = 28, k_max: int = 6, precision: str = "f64", repetitions: int = 5,
+                     seed: int = 1, ctx: Context | None = None) -> CostModel:
+    ctx = ctx or default_context()
+    h = _vp()
+    _check(_lib.tsg_bench_cost_model(ctx._h, bench_n, k_max, 64 if precision in ("f64", "c128") else 32,
+                                     repetitions, seed, C.byref(h)))
+    return CostModel(_handle=h.value)

@@ -1,0 +1,870 @@
+// Device runtime of the B200 path and its C ABI (tsg_*): contexts, device
+// statevectors, transfers, measurement reductions, kernel plans and
+// programs (a planned fused circuit replayed as a CUDA graph).
+//
+// Reference operations replaced: Statevector / init_zero_state
+// :505-524, plan_kernel :450, apply_kernel :459, run_circuit :525-533,
+// compare_states :534, norm :543.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../host/handles.hpp"
+#include "gate_launch.hpp"
+#include "tilesim/plan.hpp"
+
+using namespace tilesim;
+using tsg_detail::require;
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw SimError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+std::atomic<uint64_t> g_state_serial{1};
+
+// ------------------------------------------------------------ reductions
+constexpr int kRedThreads = 256;
+
+template <typename Real>
+__global__ void __launch_bounds__(kRedThreads) k_sumsq(const Real* __restrict__ re, const Real* __restrict__ im,
+                                                         uint64_t n, double* __restrict__ partial) {
+  double acc = 0.0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double x = re[i], y = im[i];
+    acc = fma(x, x, fma(y, y, acc));
+  }
+  __shared__ double red[kRedThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < kRedThreads / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+  }
+}
+
+// max_i |a_i - b_i| with b either a device state of type RealB or fp64 host data
+template <typename RealA, typename RealB>
+__global__ void __launch_bounds__(kRedThreads) k_maxdiff(const RealA* __restrict__ ar, const RealA* __restrict__ ai,
+                                                           const RealB* __restrict__ br, const RealB* __restrict__ bi,
+                                                           uint64_t n, double* __restrict__ partial) {
+  double m = 0.0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double dr = static_cast<double>(ar[i]) - static_cast<double>(br[i]);
+    const double di = static_cast<double>(ai[i]) - static_cast<double>(bi[i]);
+    m = fmax(m, sqrt(dr * dr + di * di));
+  }
+  __shared__ double red[kRedThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < kRedThreads / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) partial[blockIdx.x] = fmax(partial[blockIdx.x], m);
+  }
+}
+
+// sum conj(a_i) b_i
+template <typename Real>
+__global__ void __launch_bounds__(kRedThreads) k_overlap(const Real* __restrict__ ar, const Real* __restrict__ ai,
+                                                           const Real* __restrict__ br, const Real* __restrict__ bi,
+                                                           uint64_t n, double* __restrict__ partial) {
+  double sr = 0.0, si = 0.0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double xr = ar[i], xi = ai[i], yr = br[i], yi = bi[i];
+    sr = fma(xr, yr, fma(xi, yi, sr));
+    si = fma(xr, yi, fma(-xi, yr, si));
+  }
+  __shared__ double red[2][kRedThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+    si += __shfl_xor_sync(0xffffffffu, si, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = sr;
+    red[1][threadIdx.x >> 5] = si;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    sr = threadIdx.x < kRedThreads / 32 ? red[0][threadIdx.x] : 0.0;
+    si = threadIdx.x < kRedThreads / 32 ? red[1][threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      sr += __shfl_xor_sync(0xffffffffu, sr, o);
+      si += __shfl_xor_sync(0xffffffffu, si, o);
+    }
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = sr;
+      partial[2 * blockIdx.x + 1] = si;
+    }
+  }
+}
+
+// ------------------------------------------------------- init / convert
+template <typename Real>
+__global__ void k_set_amp(Real* re, Real* im, uint64_t idx, double vr, double vi) {
+  re[idx] = static_cast<Real>(vr);
+  im[idx] = static_cast<Real>(vi);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// x_c(i) = u53(mix64(seed ^ ((2i + c) * golden))) - 0.5
+template <typename Real>
+__global__ void k_init_random(Real* re, Real* im, uint64_t n, uint64_t seed) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t a = mix64(seed ^ ((2 * i) * 0x9e3779b97f4a7c15ULL));
+    const uint64_t b = mix64(seed ^ ((2 * i + 1) * 0x9e3779b97f4a7c15ULL));
+    re[i] = static_cast<Real>(static_cast<double>(a >> 11) * 0x1.0p-53 - 0.5);
+    im[i] = static_cast<Real>(static_cast<double>(b >> 11) * 0x1.0p-53 - 0.5);
+  }
+}
+
+template <typename Real>
+__global__ void k_scale(Real* re, Real* im, uint64_t n, double s) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    re[i] = static_cast<Real>(re[i] * s);
+    im[i] = static_cast<Real>(im[i] * s);
+  }
+}
+
+template <typename To, typename From>
+__global__ void k_convert(To* __restrict__ dst, const From* __restrict__ src, uint64_t n) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = static_cast<To>(src[i]);
+}
+
+}  // namespace
+
+// ============================================================== handles ===
+struct tsg_ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string name;
+};
+
+struct tsg_state {
+  tsg_ctx* ctx = nullptr;
+  int n = 0;
+  int prec = 64;
+  uint64_t serial = 0;
+  void* re = nullptr;
+  void* im = nullptr;
+  cudaStream_t stream = nullptr;
+  double* partial = nullptr;  // reduction scratch (2 * kMaxBlocks doubles)
+  double* stage = nullptr;    // 2 x kStage doubles of transfer / compare staging
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // tsg_timer_*
+  uint64_t size() const { return uint64_t{1} << n; }
+  size_t amp_bytes() const { return prec == 64 ? 8 : 4; }
+};
+
+struct tsg_plan {
+  tsg_ctx* ctx = nullptr;
+  KernelPlan plan;
+  void* dev_mat = nullptr;  // tile matrix scratch (state precision), allocated on demand
+  size_t dev_mat_bytes = 0;
+};
+
+namespace {
+
+constexpr int kMaxBlocks = 148 * 8;
+constexpr uint64_t kStage = uint64_t{1} << 22;  // doubles per staging half (32 MiB)
+
+struct ProgramGate {
+  KernelPlan plan;
+  LaunchStructure ls;
+  tsg::GateLaunch launch;  // re/im filled per run
+  size_t mat_offset = 0;   // into the device arena (tile class)
+  bool has_mat = false;
+};
+
+}  // namespace
+
+struct tsg_program {
+  tsg_ctx* ctx = nullptr;
+  int n = 0;
+  int prec = 64;
+  std::vector<ProgramGate> gates;
+  void* arena = nullptr;
+  double planning_s = 0.0;
+  uint64_t launches = 0, bytes = 0, touched_bytes = 0, total_ops = 0;
+  struct Graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::map<std::pair<tsg_state*, uint64_t>, Graph> graphs;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+void use_device(tsg_ctx* ctx) { ck(cudaSetDevice(ctx->device), "cudaSetDevice"); }
+
+unsigned red_grid(uint64_t n) {
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(kMaxBlocks, (n + kRedThreads - 1) / kRedThreads)));
+}
+
+unsigned ew_grid(const tsg_ctx* ctx, uint64_t n) {
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(ctx->num_sms) * 16, (n + 255) / 256)));
+}
+
+double fetch_sum(tsg_state* st, unsigned blocks) {
+  std::vector<double> h(blocks);
+  ck(cudaMemcpyAsync(h.data(), st->partial, blocks * sizeof(double), cudaMemcpyDeviceToHost, st->stream), "partials");
+  ck(cudaStreamSynchronize(st->stream), "reduction sync");
+  double sum = 0.0, comp = 0.0;  // Kahan over block partials
+  for (double v : h) {
+    const double y = v - comp, t = sum + y;
+    comp = (t - sum) - y;
+    sum = t;
+  }
+  return sum;
+}
+
+double state_norm(tsg_state* st) {
+  const unsigned g = red_grid(st->size());
+  if (st->prec == 64)
+    k_sumsq<double><<<g, kRedThreads, 0, st->stream>>>((double*)st->re, (double*)st->im, st->size(), st->partial);
+  else
+    k_sumsq<float><<<g, kRedThreads, 0, st->stream>>>((float*)st->re, (float*)st->im, st->size(), st->partial);
+  ck(cudaGetLastError(), "k_sumsq");
+  return std::sqrt(fetch_sum(st, g));
+}
+
+// fill a GateLaunch from a plan's launch structure
+tsg::GateLaunch make_launch(const KernelPlan& p, const LaunchStructure& ls) {
+  tsg::GateLaunch g;
+  g.klass = static_cast<int>(ls.klass);
+  g.k = p.gate.k();
+  g.ks = ls.ks;
+  g.sparse = ls.sparse ? 1 : 0;
+  g.n = p.n;
+  g.n_masks = static_cast<int>(p.group_masks.masks.size());
+  for (int i = 0; i < g.n_masks; ++i) g.masks[i] = p.group_masks.masks[i];
+  g.fixed_or = ls.control_values;
+  g.n_ctrl = static_cast<int>(ls.controls.size());
+  for (int i = 0; i < g.n_ctrl; ++i) g.ctrl[i] = ls.controls[i];
+  for (int i = 0; i < ls.ks; ++i) g.sub_targets[i] = ls.sub_targets[i];
+  for (size_t j = 0; j < ls.offsets.size() && j < (1u << tsg::kMaxSub); ++j) g.off[j] = ls.offsets[j];
+  g.m_re = ls.sub_re.data();
+  g.m_im = ls.sub_im.data();
+  g.g_begin = 0;
+  g.g_end = uint64_t{1} << (p.n - p.gate.k());
+  g.full_range = true;
+  return g;
+}
+
+// the tile kernels stage the sub-matrix from global memory: [D*D re][D*D im]
+std::vector<unsigned char> tile_matrix_bytes(const LaunchStructure& ls, int prec) {
+  const size_t dd = ls.sub_re.size();
+  std::vector<unsigned char> out(2 * dd * (prec == 64 ? 8 : 4));
+  if (prec == 64) {
+    double* d = reinterpret_cast<double*>(out.data());
+    std::copy(ls.sub_re.begin(), ls.sub_re.end(), d);
+    std::copy(ls.sub_im.begin(), ls.sub_im.end(), d + dd);
+  } else {
+    float* f = reinterpret_cast<float*>(out.data());
+    for (size_t i = 0; i < dd; ++i) {
+      f[i] = static_cast<float>(ls.sub_re[i]);
+      f[dd + i] = static_cast<float>(ls.sub_im[i]);
+    }
+  }
+  return out;
+}
+
+bool needs_tile_matrix(const tsg::GateLaunch& g, int prec) {
+  const int dm = prec == 64 ? 4 : 5;
+  if (g.klass == 3) return true;
+  if (g.klass == 2 && g.ks > dm) return true;
+  if (g.klass == 1 && g.ks > dm) return true;  // sub-range diagonal falls back to tile
+  return false;
+}
+
+int launch(tsg_state* st, const tsg::GateLaunch& g) {
+  return st->prec == 64 ? tsg::launch_gate_f64(g, st->stream, st->ctx->num_sms)
+                        : tsg::launch_gate_f32(g, st->stream, st->ctx->num_sms);
+}
+
+double touched_fraction(const LaunchStructure& ls) {
+  if (ls.klass == KernelClass::Identity) return 0.0;
+  return std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
+}
+
+void fill_info(const KernelPlan& p, const LaunchStructure& ls, tsg_plan_info* out) {
+  out->k = p.gate.k();
+  out->kernel_class = static_cast<int>(ls.klass);
+  out->sub_k = ls.ks;
+  out->n_controls = static_cast<int>(ls.controls.size());
+  out->sparse = ls.sparse ? 1 : 0;
+  out->op_count = p.profile.op_count;
+  out->entry_ops = p.entry_ops.size();
+  out->loop_count = uint64_t{1} << (p.n - p.gate.k());
+  out->touched_fraction = touched_fraction(ls);
+}
+
+void run_program(tsg_state* st, tsg_program* prog, std::vector<cudaEvent_t>* marks) {
+  for (size_t i = 0; i < prog->gates.size(); ++i) {
+    tsg::GateLaunch g = prog->gates[i].launch;
+    g.re = st->re;
+    g.im = st->im;
+    if (prog->gates[i].has_mat) g.dev_mat = static_cast<unsigned char*>(prog->arena) + prog->gates[i].mat_offset;
+    if (marks) ck(cudaEventRecord((*marks)[i], st->stream), "event");
+    launch(st, g);
+  }
+  if (marks) ck(cudaEventRecord(marks->back(), st->stream), "event");
+}
+
+}  // namespace
+
+// ================================================================ C ABI ===
+extern "C" {
+
+int tsg_device_count(int* out) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (out) *out = n;
+  return TSG_OK;
+}
+
+int tsg_ctx_create(int device, tsg_ctx** out) {
+  TSG_TRY({
+    require(out != nullptr, "null output handle");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+      cudaGetLastError();
+      throw SimError("no CUDA device available: the tilesim-b200 path has no CPU fallback");
+    }
+    require(device >= 0 && device < count, "device index out of range");
+    auto ctx = std::make_unique<tsg_ctx>();
+    ctx->device = device;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10) throw SimError(std::string("device ") + prop.name + " is not sm_100 class (B200 required)");
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->name = prop.name;
+    *out = ctx.release();
+  })
+}
+
+int tsg_ctx_destroy(tsg_ctx* ctx) {
+  delete ctx;
+  return TSG_OK;
+}
+
+int tsg_state_create(tsg_ctx* ctx, int n_qubits, int precision_bits, tsg_state** out) {
+  TSG_TRY({
+    require(ctx && out, "null argument");
+    require(n_qubits >= 1 && n_qubits <= 40, "qubit count must be in [1, 40] for one device");
+    require(precision_bits == 64 || precision_bits == 32, "precision_bits must be 64 or 32");
+    use_device(ctx);
+    auto st = std::make_unique<tsg_state>();
+    st->ctx = ctx;
+    st->n = n_qubits;
+    st->prec = precision_bits;
+    st->serial = g_state_serial++;
+    const size_t bytes = st->size() * st->amp_bytes();
+    size_t free_b = 0, total_b = 0;
+    ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const size_t need = 2 * bytes + 2 * kStage * sizeof(double) + 2 * kMaxBlocks * sizeof(double);
+    if (need > free_b)
+      throw SimError("statevector allocation failed: need " + std::to_string(2 * bytes) + " bytes (2^" +
+                     std::to_string(n_qubits + (precision_bits == 64 ? 4 : 3)) + ") plus staging, " +
+                     std::to_string(free_b) + " free");
+    ck(cudaMalloc(&st->re, bytes), "cudaMalloc re");
+    ck(cudaMalloc(&st->im, bytes), "cudaMalloc im");
+    ck(cudaMalloc(&st->partial, 2 * kMaxBlocks * sizeof(double)), "cudaMalloc partial");
+    ck(cudaMalloc(&st->stage, 2 * kStage * sizeof(double)), "cudaMalloc stage");
+    ck(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    *out = st.release();
+  })
+}
+
+int tsg_state_destroy(tsg_state* st) {
+  if (!st) return TSG_OK;
+  cudaSetDevice(st->ctx->device);
+  if (st->stream) cudaStreamSynchronize(st->stream);
+  cudaFree(st->re);
+  cudaFree(st->im);
+  cudaFree(st->partial);
+  cudaFree(st->stage);
+  if (st->stream) cudaStreamDestroy(st->stream);
+  if (st->t0) cudaEventDestroy(st->t0);
+  if (st->t1) cudaEventDestroy(st->t1);
+  delete st;
+  return TSG_OK;
+}
+
+int tsg_state_info(const tsg_state* st, int* n_qubits, int* precision_bits) {
+  TSG_TRY({
+    require(st != nullptr, "null handle");
+    if (n_qubits) *n_qubits = st->n;
+    if (precision_bits) *precision_bits = st->prec;
+  })
+}
+
+int tsg_state_init_basis(tsg_state* st, uint64_t index) {
+  TSG_TRY({
+    require(st != nullptr, "null handle");
+    require(index < st->size(), "basis index out of range");
+    use_device(st->ctx);
+    const size_t bytes = st->size() * st->amp_bytes();
+    ck(cudaMemsetAsync(st->re, 0, bytes, st->stream), "memset re");
+    ck(cudaMemsetAsync(st->im, 0, bytes, st->stream), "memset im");
+    if (st->prec == 64) k_set_amp<double><<<1, 1, 0, st->stream>>>((double*)st->re, (double*)st->im, index, 1.0, 0.0);
+    else k_set_amp<float><<<1, 1, 0, st->stream>>>((float*)st->re, (float*)st->im, index, 1.0, 0.0);
+    ck(cudaGetLastError(), "k_set_amp");
+  })
+}
+
+int tsg_state_init_zero(tsg_state* st) { return tsg_state_init_basis(st, 0); }
+
+int tsg_state_init_random(tsg_state* st, uint64_t seed) {
+  TSG_TRY({
+    require(st != nullptr, "null handle");
+    use_device(st->ctx);
+    const unsigned g = ew_grid(st->ctx, st->size());
+    if (st->prec == 64) k_init_random<double><<<g, 256, 0, st->stream>>>((double*)st->re, (double*)st->im, st->size(), seed);
+    else k_init_random<float><<<g, 256, 0, st->stream>>>((float*)st->re, (float*)st->im, st->size(), seed);
+    ck(cudaGetLastError(), "k_init_random");
+    const double nrm = state_norm(st);
+    if (st->prec == 64) k_scale<double><<<g, 256, 0, st->stream>>>((double*)st->re, (double*)st->im, st->size(), 1.0 / nrm);
+    else k_scale<float><<<g, 256, 0, st->stream>>>((float*)st->re, (float*)st->im, st->size(), 1.0 / nrm);
+    ck(cudaGetLastError(), "k_scale");
+  })
+}
+
+int tsg_state_upload(tsg_state* st, const double* re, const double* im) {
+  TSG_TRY({
+    require(st && re && im, "null argument");
+    use_device(st->ctx);
+    if (st->prec == 64) {
+      ck(cudaMemcpyAsync(st->re, re, st->size() * 8, cudaMemcpyHostToDevice, st->stream), "upload re");
+      ck(cudaMemcpyAsync(st->im, im, st->size() * 8, cudaMemcpyHostToDevice, st->stream), "upload im");
+    } else {
+      for (uint64_t b = 0; b < st->size(); b += kStage) {
+        const uint64_t c = std::min(kStage, st->size() - b);
+        ck(cudaMemcpyAsync(st->stage, re + b, c * 8, cudaMemcpyHostToDevice, st->stream), "upload re");
+        ck(cudaMemcpyAsync(st->stage + kStage, im + b, c * 8, cudaMemcpyHostToDevice, st->stream), "upload im");
+        k_convert<float, double><<<ew_grid(st->ctx, c), 256, 0, st->stream>>>((float*)st->re + b, st->stage, c);
+        k_convert<float, double><<<ew_grid(st->ctx, c), 256, 0, st->stream>>>((float*)st->im + b, st->stage + kStage, c);
+        ck(cudaGetLastError(), "k_convert");
+      }
+    }
+    ck(cudaStreamSynchronize(st->stream), "upload sync");
+  })
+}
+
+int tsg_state_download_range(tsg_state* st, uint64_t begin, uint64_t count, double* re, double* im) {
+  TSG_TRY({
+    require(st && re && im, "null argument");
+    require(begin <= st->size() && count <= st->size() - begin, "download range outside the state");
+    use_device(st->ctx);
+    if (st->prec == 64) {
+      ck(cudaMemcpyAsync(re, (double*)st->re + begin, count * 8, cudaMemcpyDeviceToHost, st->stream), "download re");
+      ck(cudaMemcpyAsync(im, (double*)st->im + begin, count * 8, cudaMemcpyDeviceToHost, st->stream), "download im");
+    } else {
+      for (uint64_t b = 0; b < count; b += kStage) {
+        const uint64_t c = std::min(kStage, count - b);
+        k_convert<double, float><<<ew_grid(st->ctx, c), 256, 0, st->stream>>>(st->stage, (float*)st->re + begin + b, c);
+        k_convert<double, float><<<ew_grid(st->ctx, c), 256, 0, st->stream>>>(st->stage + kStage, (float*)st->im + begin + b, c);
+        ck(cudaGetLastError(), "k_convert");
+        ck(cudaMemcpyAsync(re + b, st->stage, c * 8, cudaMemcpyDeviceToHost, st->stream), "download re");
+        ck(cudaMemcpyAsync(im + b, st->stage + kStage, c * 8, cudaMemcpyDeviceToHost, st->stream), "download im");
+      }
+    }
+    ck(cudaStreamSynchronize(st->stream), "download sync");
+  })
+}
+
+int tsg_state_download(tsg_state* st, double* re, double* im) {
+  if (!st) {
+    tsg_detail::set_error("null handle");
+    return TSG_ERR_CONFIG;
+  }
+  return tsg_state_download_range(st, 0, st->size(), re, im);
+}
+
+int tsg_state_copy(tsg_state* dst, const tsg_state* src) {
+  TSG_TRY({
+    require(dst && src, "null argument");
+    require(dst->n == src->n && dst->prec == src->prec, "state shapes differ");
+    use_device(dst->ctx);
+    ck(cudaStreamSynchronize(src->stream), "source sync");
+    const size_t bytes = dst->size() * dst->amp_bytes();
+    ck(cudaMemcpyAsync(dst->re, src->re, bytes, cudaMemcpyDeviceToDevice, dst->stream), "copy re");
+    ck(cudaMemcpyAsync(dst->im, src->im, bytes, cudaMemcpyDeviceToDevice, dst->stream), "copy im");
+  })
+}
+
+int tsg_synchronize(tsg_state* st) {
+  TSG_TRY({
+    require(st != nullptr, "null handle");
+    ck(cudaStreamSynchronize(st->stream), "stream sync");
+  })
+}
+
+int tsg_timer_begin(tsg_state* st) {
+  TSG_TRY({
+    require(st != nullptr, "null handle");
+    use_device(st->ctx);
+    if (!st->t0) ck(cudaEventCreate(&st->t0), "event");
+    if (!st->t1) ck(cudaEventCreate(&st->t1), "event");
+    ck(cudaEventRecord(st->t0, st->stream), "event record");
+  })
+}
+
+int tsg_timer_end(tsg_state* st, double* seconds) {
+  TSG_TRY({
+    require(st && seconds && st->t0, "timer not started");
+    ck(cudaEventRecord(st->t1, st->stream), "event record");
+    ck(cudaEventSynchronize(st->t1), "event sync");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, st->t0, st->t1), "elapsed");
+    *seconds = ms * 1e-3;
+  })
+}
+
+int tsg_norm(tsg_state* st, double* out) {
+  TSG_TRY({
+    require(st && out, "null argument");
+    use_device(st->ctx);
+    *out = state_norm(st);
+  })
+}
+
+int tsg_compare(tsg_state* st, const double* re, const double* im, double* maxdiff) {
+  TSG_TRY({
+    require(st && re && im && maxdiff, "null argument");
+    use_device(st->ctx);
+    const unsigned g = red_grid(kStage);
+    ck(cudaMemsetAsync(st->partial, 0, g * sizeof(double), st->stream), "memset partial");
+    for (uint64_t b = 0; b < st->size(); b += kStage) {
+      const uint64_t c = std::min(kStage, st->size() - b);
+      ck(cudaMemcpyAsync(st->stage, re + b, c * 8, cudaMemcpyHostToDevice, st->stream), "compare upload");
+      ck(cudaMemcpyAsync(st->stage + kStage, im + b, c * 8, cudaMemcpyHostToDevice, st->stream), "compare upload");
+      if (st->prec == 64)
+        k_maxdiff<double, double><<<g, kRedThreads, 0, st->stream>>>((double*)st->re + b, (double*)st->im + b, st->stage,
+                                                                   st->stage + kStage, c, st->partial);
+      else
+        k_maxdiff<float, double><<<g, kRedThreads, 0, st->stream>>>((float*)st->re + b, (float*)st->im + b, st->stage,
+                                                                  st->stage + kStage, c, st->partial);
+      ck(cudaGetLastError(), "k_maxdiff");
+    }
+    std::vector<double> h(g);
+    ck(cudaMemcpyAsync(h.data(), st->partial, g * sizeof(double), cudaMemcpyDeviceToHost, st->stream), "partials");
+    ck(cudaStreamSynchronize(st->stream), "compare sync");
+    *maxdiff = *std::max_element(h.begin(), h.end());
+  })
+}
+
+int tsg_compare_states(tsg_state* a, tsg_state* b, double* maxdiff) {
+  TSG_TRY({
+    require(a && b && maxdiff, "null argument");
+    require(a->n == b->n, "state sizes differ");
+    use_device(a->ctx);
+    ck(cudaStreamSynchronize(b->stream), "sync b");
+    const unsigned g = red_grid(a->size());
+    ck(cudaMemsetAsync(a->partial, 0, g * sizeof(double), a->stream), "memset partial");
+    if (a->prec == 64 && b->prec == 64)
+      k_maxdiff<double, double><<<g, kRedThreads, 0, a->stream>>>((double*)a->re, (double*)a->im, (double*)b->re,
+                                                                (double*)b->im, a->size(), a->partial);
+    else if (a->prec == 32 && b->prec == 32)
+      k_maxdiff<float, float><<<g, kRedThreads, 0, a->stream>>>((float*)a->re, (float*)a->im, (float*)b->re,
+                                                              (float*)b->im, a->size(), a->partial);
+    else if (a->prec == 32)
+      k_maxdiff<float, double><<<g, kRedThreads, 0, a->stream>>>((float*)a->re, (float*)a->im, (double*)b->re,
+                                                               (double*)b->im, a->size(), a->partial);
+    else
+      k_maxdiff<double, float><<<g, kRedThreads, 0, a->stream>>>((double*)a->re, (double*)a->im, (float*)b->re,
+                                                               (float*)b->im, a->size(), a->partial);
+    ck(cudaGetLastError(), "k_maxdiff");
+    std::vector<double> h(g);
+    ck(cudaMemcpyAsync(h.data(), a->partial, g * sizeof(double), cudaMemcpyDeviceToHost, a->stream), "partials");
+    ck(cudaStreamSynchronize(a->stream), "compare sync");
+    *maxdiff = *std::max_element(h.begin(), h.end());
+  })
+}
+
+int tsg_overlap(tsg_state* a, tsg_state* b, double* re, double* im) {
+  TSG_TRY({
+    require(a && b && re && im, "null argument");
+    require(a->n == b->n && a->prec == b->prec, "state shapes differ");
+    use_device(a->ctx);
+    ck(cudaStreamSynchronize(b->stream), "sync b");
+    const unsigned g = red_grid(a->size());
+    if (a->prec == 64)
+      k_overlap<double><<<g, kRedThreads, 0, a->stream>>>((double*)a->re, (double*)a->im, (double*)b->re,
+                                                          (double*)b->im, a->size(), a->partial);
+    else
+      k_overlap<float><<<g, kRedThreads, 0, a->stream>>>((float*)a->re, (float*)a->im, (float*)b->re, (float*)b->im,
+                                                         a->size(), a->partial);
+    ck(cudaGetLastError(), "k_overlap");
+    std::vector<double> h(2 * g);
+    ck(cudaMemcpyAsync(h.data(), a->partial, 2 * g * sizeof(double), cudaMemcpyDeviceToHost, a->stream), "partials");
+    ck(cudaStreamSynchronize(a->stream), "overlap sync");
+    double sr = 0, si = 0;
+    for (unsigned i = 0; i < g; ++i) {
+      sr += h[2 * i];
+      si += h[2 * i + 1];
+    }
+    *re = sr;
+    *im = si;
+  })
+}
+
+// ------------------------------------------------------------------ plans
+int tsg_plan_create(tsg_ctx* ctx, int n_qubits, int k, const int* targets, const double* matrix, double zero_tol,
+                    double one_tol, int runtime_matrix, tsg_plan** out) {
+  TSG_TRY({
+    require(out && targets && matrix, "null argument");
+    require(k >= 1 && k <= kFusedQubitCap, "gate size must be in [1, 12]");
+    require(zero_tol >= 0 && one_tol >= 0, "tolerances must be >= 0");
+    GateMatrix m(k);
+    for (size_t i = 0; i < m.entries().size(); ++i) m.entries()[i] = cplx(matrix[2 * i], matrix[2 * i + 1]);
+    Gate g = make_gate(std::move(m), std::vector<int>(targets, targets + k));
+    auto p = std::make_unique<tsg_plan>();
+    p->ctx = ctx;
+    p->plan = plan_kernel(g, n_qubits, 0, zero_tol, one_tol, runtime_matrix != 0);
+    *out = p.release();
+  })
+}
+
+int tsg_plan_destroy(tsg_plan* p) {
+  if (!p) return TSG_OK;
+  if (p->dev_mat) cudaFree(p->dev_mat);
+  delete p;
+  return TSG_OK;
+}
+
+int tsg_plan_info_get(const tsg_plan* p, tsg_plan_info* out) {
+  TSG_TRY({
+    require(p && out, "null argument");
+    fill_info(p->plan, p->plan.launch, out);
+  })
+}
+
+int tsg_apply(tsg_state* st, const tsg_plan* pc, const double* matrix_override, uint64_t t_begin, uint64_t t_end) {
+  TSG_TRY({
+    require(st && pc, "null argument");
+    tsg_plan* p = const_cast<tsg_plan*>(pc);
+    const KernelPlan& kp = p->plan;
+    if (kp.n != st->n) throw ConfigError("plan was made for a different qubit count");
+    if (matrix_override && !kp.runtime_matrix) throw SimError("matrix override given for a plan with baked matrix");
+    if (!matrix_override && kp.runtime_matrix) throw SimError("runtime-matrix plan needs a matrix override");
+    const uint64_t groups = uint64_t{1} << (kp.n - kp.gate.k());
+    if (t_end == UINT64_MAX) t_end = groups;
+    if (t_begin > t_end || t_end > groups) throw SimError("loop range outside [0, 2^(n-k))");
+    use_device(st->ctx);
+    GateMatrix over;
+    if (matrix_override) {
+      over = GateMatrix(kp.gate.k());
+      for (size_t i = 0; i < over.entries().size(); ++i)
+        over.entries()[i] = cplx(matrix_override[2 * i], matrix_override[2 * i + 1]);
+    }
+    const LaunchStructure ls = derive_launch(kp, matrix_override ? &over : nullptr, st->prec);
+    tsg::GateLaunch g = make_launch(kp, ls);
+    g.re = st->re;
+    g.im = st->im;
+    g.g_begin = t_begin;
+    g.g_end = t_end;
+    g.full_range = t_begin == 0 && t_end == groups;
+    if (t_begin == t_end) return TSG_OK;
+    if (needs_tile_matrix(g, st->prec)) {
+      const auto bytes = tile_matrix_bytes(ls, st->prec);
+      if (p->dev_mat_bytes < bytes.size()) {
+        if (p->dev_mat) ck(cudaFree(p->dev_mat), "cudaFree");
+        ck(cudaMalloc(&p->dev_mat, bytes.size()), "cudaMalloc plan matrix");
+        p->dev_mat_bytes = bytes.size();
+      }
+      ck(cudaMemcpyAsync(p->dev_mat, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, st->stream), "matrix upload");
+      g.dev_mat = p->dev_mat;
+    }
+    launch(st, g);
+  })
+}
+
+// --------------------------------------------------------------- programs
+int tsg_program_create(tsg_ctx* ctx, const tsc_circuit* fused, double zero_tol, double one_tol, int precision_bits,
+                       tsg_program** out) {
+  TSG_TRY({
+    require(ctx && fused && out, "null argument");
+    require(precision_bits == 64 || precision_bits == 32, "precision_bits must be 64 or 32");
+    use_device(ctx);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto prog = std::make_unique<tsg_program>();
+    prog->ctx = ctx;
+    prog->n = fused->c.n_qubits;
+    prog->prec = precision_bits;
+    std::vector<unsigned char> arena;
+    const uint64_t amp = precision_bits == 64 ? 16 : 8;
+    for (const Gate& g : fused->c.gates) {
+      ProgramGate pg;
+      pg.plan = plan_kernel(g, prog->n, 0, zero_tol, one_tol, false);
+      pg.ls = precision_bits == 64 ? pg.plan.launch : derive_launch(pg.plan, nullptr, precision_bits);
+      pg.launch = make_launch(pg.plan, pg.ls);
+      if (needs_tile_matrix(pg.launch, precision_bits)) {
+        const auto bytes = tile_matrix_bytes(pg.ls, precision_bits);
+        pg.mat_offset = (arena.size() + 255) & ~size_t{255};
+        arena.resize(pg.mat_offset + bytes.size());
+        std::copy(bytes.begin(), bytes.end(), arena.begin() + pg.mat_offset);
+        pg.has_mat = true;
+      }
+      prog->total_ops += pg.plan.profile.op_count;
+      if (pg.ls.klass != KernelClass::Identity) {
+        ++prog->launches;
+        prog->bytes += 2 * (uint64_t{1} << prog->n) * amp;
+        prog->touched_bytes += static_cast<uint64_t>(2.0 * std::ldexp(1.0, prog->n) * amp * touched_fraction(pg.ls));
+      }
+      prog->gates.push_back(std::move(pg));
+    }
+    if (!arena.empty()) {
+      ck(cudaMalloc(&prog->arena, arena.size()), "cudaMalloc program arena");
+      ck(cudaMemcpy(prog->arena, arena.data(), arena.size(), cudaMemcpyHostToDevice), "program arena upload");
+    }
+    // the host snapped matrices referenced by launch.m_re/m_im must follow the moved vectors
+    for (ProgramGate& pg : prog->gates) {
+      pg.launch.m_re = pg.ls.sub_re.data();
+      pg.launch.m_im = pg.ls.sub_im.data();
+    }
+    ck(cudaEventCreate(&prog->ev0), "event");
+    ck(cudaEventCreate(&prog->ev1), "event");
+    prog->planning_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = prog.release();
+  })
+}
+
+int tsg_program_destroy(tsg_program* prog) {
+  if (!prog) return TSG_OK;
+  cudaSetDevice(prog->ctx->device);
+  for (auto& kv : prog->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+  }
+  if (prog->arena) cudaFree(prog->arena);
+  if (prog->ev0) cudaEventDestroy(prog->ev0);
+  if (prog->ev1) cudaEventDestroy(prog->ev1);
+  delete prog;
+  return TSG_OK;
+}
+
+static void fill_report(const tsg_program* prog, double exec_s, tsg_run_report* r) {
+  if (!r) return;
+  r->planning_s = prog->planning_s;
+  r->execution_s = exec_s;
+  r->gates = prog->gates.size();
+  r->launches = prog->launches;
+  r->bytes = prog->bytes;
+  r->touched_bytes = prog->touched_bytes;
+  r->total_op_count = prog->total_ops;
+}
+
+static cudaGraphExec_t program_graph(tsg_state* st, tsg_program* prog) {
+  auto key = std::make_pair(st, st->serial);
+  auto it = prog->graphs.find(key);
+  if (it == prog->graphs.end()) {
+    // relaxed capture: first-use kernel attributes may be set while capturing
+    tsg_program::Graph gr;
+    ck(cudaStreamBeginCapture(st->stream, cudaStreamCaptureModeRelaxed), "begin capture");
+    try {
+      run_program(st, prog, nullptr);
+    } catch (...) {
+      cudaGraph_t dummy = nullptr;
+      cudaStreamEndCapture(st->stream, &dummy);
+      if (dummy) cudaGraphDestroy(dummy);
+      throw;
+    }
+    ck(cudaStreamEndCapture(st->stream, &gr.graph), "end capture");
+    ck(cudaGraphInstantiate(&gr.exec, gr.graph, 0), "graph instantiate");
+    it = prog->graphs.emplace(key, gr).first;
+  }
+  return it->second.exec;
+}
+
+static void enqueue_program(tsg_state* st, tsg_program* prog, int use_graph) {
+  require(st->n == prog->n && st->prec == prog->prec, "program was built for a different state shape");
+  use_device(st->ctx);
+  if (use_graph) ck(cudaGraphLaunch(program_graph(st, prog), st->stream), "graph launch");
+  else run_program(st, prog, nullptr);
+}
+
+int tsg_program_enqueue(tsg_state* st, tsg_program* prog, int use_graph) {
+  TSG_TRY({
+    require(st && prog, "null argument");
+    enqueue_program(st, prog, use_graph);
+  })
+}
+
+int tsg_program_run(tsg_state* st, tsg_program* prog, int use_graph, tsg_run_report* report) {
+  TSG_TRY({
+    require(st && prog, "null argument");
+    if (use_graph) program_graph(st, prog);  // capture before the timed events
+    ck(cudaEventRecord(prog->ev0, st->stream), "event");
+    enqueue_program(st, prog, use_graph);
+    ck(cudaEventRecord(prog->ev1, st->stream), "event");
+    ck(cudaEventSynchronize(prog->ev1), "run sync");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, prog->ev0, prog->ev1), "elapsed");
+    fill_report(prog, ms * 1e-3, report);
+  })
+}
+
+int tsg_program_run_profiled(tsg_state* st, tsg_program* prog, double* seconds, tsg_run_report* report) {
+  TSG_TRY({
+    require(st && prog, "null argument");
+    require(st->n == prog->n && st->prec == prog->prec, "program was built for a different state shape");
+    use_device(st->ctx);
+    std::vector<cudaEvent_t> marks(prog->gates.size() + 1);
+    for (auto& e : marks) ck(cudaEventCreate(&e), "event");
+    run_program(st, prog, &marks);
+    ck(cudaEventSynchronize(marks.back()), "run sync");
+    double total = 0.0;
+    for (size_t i = 0; i < prog->gates.size(); ++i) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, marks[i], marks[i + 1]), "elapsed");
+      if (seconds) seconds[i] = ms * 1e-3;
+      total += ms * 1e-3;
+    }
+    for (auto& e : marks) cudaEventDestroy(e);
+    fill_report(prog, total, report);
+  })
+}
+
+int tsg_program_gate_info(const tsg_program* prog, uint64_t i, tsg_plan_info* out) {
+  TSG_TRY({
+    require(prog && out, "null argument");
+    require(i < prog->gates.size(), "gate index out of range");
+    fill_info(prog->gates[i].plan, prog->gates[i].ls, out);
+  })
+}
+
+int tsg_bench_cost_model(tsg_ctx*, int, int, int, int, uint64_t, tsc_cost_model**) {
+  tsg_detail::set_error("tsg_bench_cost_model: not built yet");
+  return TSG_ERR_SIM;
+}
+
+}  // extern "C"

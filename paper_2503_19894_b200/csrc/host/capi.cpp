@@ -1,0 +1,200 @@
+// C ABI for the host-only part of the surface: circuit IR, generators, text
+// format, fusion pass and cost model (include/tilesim_cuda.h, tsc_*).
+#include <cstring>
+
+#include "handles.hpp"
+
+namespace tsg_detail {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace tsg_detail
+
+using namespace tilesim;
+using tsg_detail::require;
+
+namespace {
+
+GateMatrix matrix_from(int k, const double* m) {
+  GateMatrix g(k);
+  for (size_t i = 0; i < g.entries().size(); ++i) g.entries()[i] = cplx(m[2 * i], m[2 * i + 1]);
+  return g;
+}
+
+int copy_out(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf && cap > 0) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return TSG_OK;
+}
+
+FusionConfig to_config(const tsc_fusion_config* c) {
+  FusionConfig f;
+  require(c->mode >= 0 && c->mode <= 2, "fusion mode must be 0 (none), 1 (size-only) or 2 (adaptive)");
+  f.mode = c->mode == 0 ? FusionMode::None : (c->mode == 1 ? FusionMode::SizeOnly : FusionMode::Adaptive);
+  f.k_max = c->k_max;
+  if (c->max_op_count >= 0) f.max_op_count = static_cast<uint64_t>(c->max_op_count);
+  f.agglomerative = c->agglomerative != 0;
+  f.multi_traversal = c->multi_traversal != 0;
+  f.zero_tol = c->zero_tol;
+  f.one_tol = c->one_tol;
+  f.max_traversals = c->max_traversals;
+  f.threads = c->threads;
+  require(f.zero_tol >= 0 && f.one_tol >= 0, "tolerances must be >= 0");
+  return f;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tsg_last_error(void) { return tsg_detail::g_last_error.c_str(); }
+const char* tsg_version(void) { return "tilesim-b200 0.1 (sm_100a)"; }
+
+int tsc_circuit_create(int n_qubits, tsc_circuit** out) {
+  TSG_TRY({
+    require(out != nullptr, "null output handle");
+    require(n_qubits >= 1 && n_qubits <= 62, "qubit count must be in [1, 62]");
+    *out = new tsc_circuit();
+    (*out)->c.n_qubits = n_qubits;
+  })
+}
+
+int tsc_circuit_destroy(tsc_circuit* c) {
+  delete c;
+  return TSG_OK;
+}
+
+int tsc_circuit_copy(const tsc_circuit* c, tsc_circuit** out) {
+  TSG_TRY({
+    require(c && out, "null handle");
+    *out = new tsc_circuit(*c);
+  })
+}
+
+int tsc_circuit_add_named(tsc_circuit* c, const char* name, const double* params, int n_params, const int* qubits,
+                          int n_qubits) {
+  TSG_TRY({
+    require(c && name, "null handle");
+    std::vector<int> q(qubits, qubits + n_qubits);
+    for (int x : q)
+      if (x < 0 || x >= c->c.n_qubits) throw ConfigError("qubit index out of range");
+    c->c.gates.push_back(make_named_gate(name, std::vector<double>(params, params + n_params), q));
+  })
+}
+
+int tsc_circuit_add_matrix(tsc_circuit* c, int k, const int* qubits, const double* matrix) {
+  TSG_TRY({
+    require(c && qubits && matrix, "null argument");
+    require(k >= 1 && k <= kFusedQubitCap, "matrix gate size must be in [1, 12]");
+    std::vector<int> q(qubits, qubits + k);
+    for (int x : q)
+      if (x < 0 || x >= c->c.n_qubits) throw ConfigError("qubit index out of range");
+    c->c.gates.push_back(make_gate_arg_order(matrix_from(k, matrix), q));
+  })
+}
+
+int tsc_circuit_n_qubits(const tsc_circuit* c, int* out) {
+  TSG_TRY({
+    require(c && out, "null argument");
+    *out = c->c.n_qubits;
+  })
+}
+
+int tsc_circuit_n_gates(const tsc_circuit* c, uint64_t* out) {
+  TSG_TRY({
+    require(c && out, "null argument");
+    *out = c->c.gates.size();
+  })
+}
+
+int tsc_circuit_gate(const tsc_circuit* c, uint64_t i, int* k, int* targets, double* matrix) {
+  TSG_TRY({
+    require(c != nullptr, "null handle");
+    require(i < c->c.gates.size(), "gate index out of range");
+    const Gate& g = c->c.gates[i];
+    if (k) *k = g.k();
+    if (targets)
+      for (int j = 0; j < g.k(); ++j) targets[j] = g.targets[j];
+    if (matrix)
+      for (size_t j = 0; j < g.matrix.entries().size(); ++j) {
+        matrix[2 * j] = g.matrix.entries()[j].real();
+        matrix[2 * j + 1] = g.matrix.entries()[j].imag();
+      }
+  })
+}
+
+const char* tsc_circuit_gate_name(const tsc_circuit* c, uint64_t i) {
+  if (!c || i >= c->c.gates.size()) return "";
+  return c->c.gates[i].name.c_str();
+}
+
+int tsc_gen_benchmark(const char* kind, int n, int depth, uint64_t seed, tsc_circuit** out) {
+  TSG_TRY({
+    require(kind && out, "null argument");
+    *out = new tsc_circuit{gen_benchmark(parse_benchmark_kind(kind), n, depth, seed)};
+  })
+}
+
+int tsc_parse_circuit(const char* text, tsc_circuit** out) {
+  TSG_TRY({
+    require(text && out, "null argument");
+    *out = new tsc_circuit{parse_circuit(text)};
+  })
+}
+
+int tsc_serialize_circuit(const tsc_circuit* c, char* buf, size_t cap, size_t* needed) {
+  TSG_TRY({
+    require(c != nullptr, "null handle");
+    copy_out(serialize_circuit(c->c), buf, cap, needed);
+  })
+}
+
+int tsc_run_fusion(const tsc_circuit* c, const tsc_fusion_config* cfg, const tsc_cost_model* cm, tsc_circuit** out,
+                   tsc_fusion_stats* stats) {
+  TSG_TRY({
+    require(c && cfg && out, "null argument");
+    FusionStats st;
+    Circuit fused = run_fusion(c->c, to_config(cfg), cm ? &cm->cm : nullptr, &st);
+    *out = new tsc_circuit{std::move(fused)};
+    if (stats) {
+      stats->original_gate_count = st.original_gate_count;
+      stats->fused_block_count = st.fused_block_count;
+      stats->total_op_count = st.total_op_count;
+      stats->compression_ratio = st.compression_ratio;
+      stats->fusion_wall_time = st.fusion_wall_time;
+    }
+  })
+}
+
+int tsc_cost_model_parse(const char* text, tsc_cost_model** out) {
+  TSG_TRY({
+    require(text && out, "null argument");
+    *out = new tsc_cost_model{parse_cost_model(text)};
+  })
+}
+
+int tsc_cost_model_destroy(tsc_cost_model* cm) {
+  delete cm;
+  return TSG_OK;
+}
+
+int tsc_cost_model_serialize(const tsc_cost_model* cm, char* buf, size_t cap, size_t* needed) {
+  TSG_TRY({
+    require(cm != nullptr, "null handle");
+    copy_out(serialize_cost_model(cm->cm), buf, cap, needed);
+  })
+}
+
+int tsc_estimate_cost(const tsc_cost_model* cm, int k, uint64_t op_count, int threads, int n, double* seconds) {
+  TSG_TRY({
+    require(cm && seconds, "null argument");
+    const auto c = estimate_cost(cm->cm, k, op_count, threads, n);
+    if (!c) throw ConfigError("no cost records for this gate size / thread count");
+    *seconds = *c;
+  })
+}
+
+}  // extern "C"

@@ -1,0 +1,175 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): complex128 max |dpsi| <= 1e-10, complex64
+<= 1e-5, fidelity >= 1 - 1e-9, on the SAME kernel plan (same tolerances and
+scalar kinds) as the oracle's SPEC apply_kernel.
+"""
+import numpy as np
+import pytest
+
+import paper_2503_19894_b200 as ts
+from oracle import binding as ob
+from tests._util import random_gate_matrix, random_state, to_oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {64: 1e-12, 32: 1e-5}
+PREC = {64: "f64", 32: "f32"}
+
+TARGET_SETS = {
+    1: [[0], [1], [3], [9]],
+    2: [[0, 1], [0, 5], [2, 7], [6, 11]],
+    3: [[0, 1, 2], [0, 3, 8], [4, 9, 12], [1, 2, 10]],
+    4: [[0, 1, 2, 3], [0, 2, 6, 11], [5, 7, 9, 12]],
+    5: [[0, 1, 2, 3, 4], [1, 4, 6, 9, 12], [3, 5, 7, 8, 13]],
+    6: [[0, 1, 2, 3, 4, 5], [0, 2, 5, 7, 10, 13], [6, 7, 8, 9, 10, 11]],
+}
+
+
+def _gpu_apply(n, targets, m, re, im, prec, override=None, t_begin=0, t_end=None, runtime=False):
+    sv = ts.Statevector(n, PREC[prec]).upload(re, im)
+    plan = ts.KernelPlan(ts.Gate(list(targets), m), n, runtime_matrix=runtime)
+    ts.apply_kernel(plan, sv, override, t_begin, t_end)
+    return sv, plan
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("kind", ["dense", "perm", "diag", "controlled"])
+def test_apply_matches_oracle(prec, k, kind):
+    n = 14
+    ts.default_context()
+    for i, targets in enumerate(TARGET_SETS[k]):
+        m = random_gate_matrix(k, 100 * k + i, kind)
+        dt = np.float64 if prec == 64 else np.float32
+        re, im = random_state(n, 7 + i, dt)
+        sv, plan = _gpu_apply(n, targets, m, re.astype(np.float64), im.astype(np.float64), prec)
+        ore, oim = re.copy(), im.copy()
+        ob.apply_kernel(n, targets, m, ore, oim)  # SPEC apply_kernel, same precision
+        d = ts.compare_states(sv, (ore.astype(np.float64), oim.astype(np.float64)))
+        assert d <= TOL[prec], (k, kind, targets, plan.info(), d)
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_named_gate_classes(prec):
+    """Control peeling and kernel-class selection on the named gates."""
+    n = 12
+    cases = [("cx", [2, 7], "direct", 1, 1), ("cx", [7, 2], "direct", 1, 1), ("cz", [0, 5], "diagonal", 0, 2),
+             ("cp", [3, 4], "diagonal", 0, 2), ("rz", [5], "diagonal", 1, 0), ("t", [0], "diagonal", 0, 1),
+             ("h", [0], "direct", 1, 0), ("ccx", [1, 4, 9], "direct", 1, 2), ("swap", [2, 10], "direct", 2, 0),
+             ("x", [11], "direct", 1, 0), ("y", [0], "direct", 1, 0)]
+    for name, qubits, klass, sub_k, ctrl in cases:
+        params = [0.7] if name in ("cp", "rz") else []
+        g = ts.make_named_gate(name, params, qubits)
+        re, im = random_state(n, 3)
+        sv, plan = _gpu_apply(n, g.targets, g.matrix, re, im, prec)
+        info = plan.info()
+        assert (info["kernel"], info["sub_k"], info["n_controls"]) == (klass, sub_k, ctrl), (name, info)
+        ore = re.astype(np.float64 if prec == 64 else np.float32)
+        oim = im.astype(ore.dtype)
+        ob.apply_kernel(n, g.targets, g.matrix, ore, oim)
+        assert ts.compare_states(sv, (ore.astype(np.float64), oim.astype(np.float64))) <= TOL[prec], name
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("k,targets", [(1, [0]), (2, [1, 6]), (3, [0, 4, 9]), (5, [0, 1, 3, 8, 10]),
+                                       (6, [2, 3, 4, 5, 6, 7])])
+def test_subrange_partition(prec, k, targets):
+    """Disjoint [t_begin, t_end) calls compose to the full application."""
+    n = 13
+    m = random_gate_matrix(k, 5, "dense")
+    re, im = random_state(n, 11)
+    full, _ = _gpu_apply(n, targets, m, re, im, prec)
+    sv = ts.Statevector(n, PREC[prec]).upload(re, im)
+    plan = ts.KernelPlan(ts.Gate(targets, m), n)
+    T = 1 << (n - k)
+    cuts = sorted({0, T, T // 3, T // 2 + 1, (7 * T) // 8})
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        ts.apply_kernel(plan, sv, None, a, b)
+    assert ts.compare_states(sv, full) <= TOL[prec] / 10
+
+
+def test_runtime_matrix_override():
+    n = 12
+    targets = [1, 5]
+    m = random_gate_matrix(2, 1, "dense")
+    m2 = random_gate_matrix(2, 2, "dense")
+    re, im = random_state(n, 4)
+    sv, plan = _gpu_apply(n, targets, m, re, im, 64, override=m2, runtime=True)
+    ore, oim = re.copy(), im.copy()
+    ob.apply_kernel(n, targets, m, ore, oim, override=m2)
+    assert ts.compare_states(sv, (ore, oim)) <= 1e-12
+    # an override whose sparsity differs from the plan is a SimError
+    with pytest.raises(ts.SimError):
+        ts.apply_kernel(plan, sv, np.eye(4))
+    # a baked plan refuses overrides
+    baked = ts.KernelPlan(ts.Gate(targets, m), n)
+    with pytest.raises(ts.SimError):
+        ts.apply_kernel(baked, sv, m2)
+
+
+@pytest.mark.parametrize("kind,n,depth,prec,kmax", [
+    ("qft", 16, 1, 64, 5), ("rqc", 16, 12, 64, 5), ("ala", 14, 6, 64, 4), ("qvc", 14, 4, 64, 5),
+    ("iqp", 16, 4, 64, 5), ("hes", 16, 4, 64, 5), ("qaoa", 16, 4, 32, 6), ("qaoa", 16, 4, 32, 3),
+    ("rqc", 14, 10, 32, 6), ("qft", 12, 1, 64, 6),
+])
+def test_fused_circuit_matches_oracle(kind, n, depth, prec, kmax):
+    c = ts.gen_benchmark(kind, n, depth, 42)
+    fused, _ = ts.run_fusion(c, ts.FusionConfig(k_max=kmax))
+    sv = ts.Statevector(n, PREC[prec]).init_random(1)
+    re0, im0 = sv.download()
+    rep = ts.run_circuit(fused, sv)
+    assert rep["gates"] == len(fused)
+    dt = np.float64 if prec == 64 else np.float32
+    ore, oim = re0.astype(dt), im0.astype(dt)
+    ob.run_circuit(to_oracle(fused), ore, oim, threads=4)
+    d = ts.compare_states(sv, (ore.astype(np.float64), oim.astype(np.float64)))
+    bar = 1e-10 if prec == 64 else 1e-5
+    assert d <= bar, d
+    # against the unfused dense oracle in fp64 as well (fidelity bar)
+    rre, rim = re0.copy(), im0.copy()
+    ob.reference_run(to_oracle(c), rre, rim)
+    psi = sv.amplitudes()
+    fid = abs(np.vdot(rre + 1j * rim, psi)) ** 2
+    assert fid >= 1 - 1e-9 if prec == 64 else fid >= 1 - 1e-5
+
+
+def test_qft_analytic_basis_state():
+    """QFT|x> = sum_y e^{2 pi i x y / 2^n} |y> / 2^{n/2} (SURVEY.md §8c extra oracle 1)."""
+    n, x = 20, 0x5A5A5
+    c = ts.gen_benchmark("qft", n)
+    fused, _ = ts.run_fusion(c, ts.FusionConfig(k_max=5))
+    sv = ts.Statevector(n, "f64").init_basis(x)
+    ts.run_circuit(fused, sv)
+    y = np.arange(1 << n)
+    want = np.exp(2j * np.pi * ((x * y) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
+    assert np.abs(sv.amplitudes() - want).max() <= 1e-10
+
+
+def test_norm_compare_init():
+    sv = ts.Statevector(16, "f64").init_random(9)
+    re, im = sv.download()
+    assert abs(sv.norm() - 1.0) < 1e-12
+    assert abs(sv.norm() - np.sqrt((re * re + im * im).sum())) < 1e-13
+    other = ts.Statevector(16, "f64").init_random(9)
+    assert ts.compare_states(sv, other) == 0.0
+    z = ts.Statevector(16, "f32").init_zero()
+    zr, zi = z.download()
+    assert zr[0] == 1.0 and zr[1:].sum() == 0 and zi.sum() == 0
+    assert abs(ts.compare_states(z, (re, im)) - np.sqrt(((zr - re) ** 2 + (zi - im) ** 2).max())) < 1e-6
+    assert abs(ts.overlap(sv, other) - 1.0) < 1e-12
+
+
+def test_program_graph_and_profile():
+    c = ts.gen_benchmark("rqc", 18, 8, 3)
+    fused, _ = ts.run_fusion(c, ts.FusionConfig(k_max=4))
+    prog = ts.Program(fused, "f64")
+    a = ts.Statevector(18, "f64").init_random(2)
+    b = ts.Statevector(18, "f64").copy_from(a)
+    r1 = prog.run(a, use_graph=True)
+    secs, r2 = prog.run_profiled(b)
+    assert ts.compare_states(a, b) == 0.0
+    assert r1["launches"] == r2["launches"] and len(secs) == len(fused) and (secs >= 0).all()
+    prog.run(a, use_graph=True)  # cached graph replay
+    prog.run(b, use_graph=False)
+    assert ts.compare_states(a, b) == 0.0
