@@ -266,7 +266,8 @@ def run_ours(args):
                 sv.download(int(i0), 1)
             e2e_times.append(time.perf_counter() - t0)
             del p1, p2
-            assert abs(nrm - 1.0) < 1e-9
+            # one_tol=1e-8 lowering of cos(phi)~1 in tiny CP phases perturbs the norm by ~1e-8 (SPEC semantics)
+            assert abs(nrm - 1.0) < 1e-6, nrm
         e2e = {"value": dist.max(statistics.median(e2e_times)), "unit": "s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "includes": "generate+fuse+plan+upload+init+run+readback"}
 

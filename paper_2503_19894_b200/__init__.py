@@ -202,7 +202,7 @@ class Circuit:
         self._h = _handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.tsc_circuit_destroy(self._h)
             self._h = None
 
@@ -312,7 +312,7 @@ class CostModel:
         self._h = _handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.tsc_cost_model_destroy(self._h)
             self._h = None
 
@@ -358,7 +358,7 @@ class Context:
         self.device = device
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.tsg_ctx_destroy(self._h)
             self._h = None
 
@@ -386,7 +386,7 @@ class Statevector:
         self.precision_bits = bits
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.tsg_state_destroy(self._h)
             self._h = None
 
@@ -483,7 +483,7 @@ class KernelPlan:
         self.runtime_matrix = runtime_matrix
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.tsg_plan_destroy(self._h)
             self._h = None
 
@@ -522,7 +522,7 @@ class Program:
         self.n_gates = len(fused)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.tsg_program_destroy(self._h)
             self._h = None
 

@@ -9,6 +9,8 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "kernels_dmma.cuh"
+#include "kernels_stream.cuh"
 
 namespace tsg {
 
@@ -161,12 +163,262 @@ void pick_tile(const GateLaunch& g, cudaStream_t s, int num_sms) {
   }
 }
 
+// ----------------------------------------------------------------- stream
+// Insertion masks (SPEC.md:441-449 form) for zeros at sorted `pos` inside a
+// value of `width` bits: x -> sum_i (x & m[i]) << i.
+inline int insertion_masks(const int* pos, int count, int width, uint64_t* out) {
+  int from = 0;
+  for (int i = 0; i <= count; ++i) {
+    const int to = i < count ? pos[i] - i : width;
+    uint64_t m = 0;
+    for (int b = from; b < to && b < width; ++b) m |= uint64_t{1} << b;
+    out[i] = m;
+    from = to > from ? to : from;
+  }
+  return count + 1;
+}
+
+// Tile geometry of k_stream for a full-range launch; false if the state is
+// too small for one tile of the required shape.
+template <typename Real, int KS>
+bool stream_geometry(const GateLaunch& g, StreamParams<Real, KS>& p, size_t* smem, int* stages) {
+  using S = StreamShape<KS>;
+  int tg[24], nt = 0;  // all targets (controls + sub-targets), ascending
+  {
+    int a = 0, b = 0;
+    while (a < g.n_ctrl || b < g.ks) {
+      if (b >= g.ks || (a < g.n_ctrl && g.ctrl[a] < g.sub_targets[b])) tg[nt++] = g.ctrl[a++];
+      else tg[nt++] = g.sub_targets[b++];
+    }
+  }
+  int L = S::LOG2G;
+  for (;;) {
+    int below = 0;
+    for (int i = 0; i < nt; ++i) below += tg[i] < L;
+    if (S::LOG2G + below == L) break;
+    L = S::LOG2G + below;
+  }
+  int n_low = 0, high_pos[24], n_high = 0, run_pos[8], n_run = 0;
+  for (int i = 0; i < nt; ++i) {
+    if (tg[i] < L) ++n_low;
+    else high_pos[n_high++] = tg[i] - L;
+  }
+  for (int b = 0; b < g.ks; ++b)
+    if (g.sub_targets[b] >= L) run_pos[n_run++] = g.sub_targets[b];
+  if (L + n_high > g.n) return false;
+  const int tile_bits = g.n - L - n_high;
+  p.n_tiles = uint64_t{1} << tile_bits;
+  p.L = L;
+  p.n_runs = 1 << n_run;
+  p.ctrl_or = g.fixed_or;
+  p.n_tmask = insertion_masks(high_pos, n_high, tile_bits, p.tmask);
+  int low_pos[24];
+  for (int i = 0; i < n_low; ++i) low_pos[i] = tg[i];
+  uint64_t gm[kMaxMasks + 12];
+  p.n_gmask = insertion_masks(low_pos, n_low, S::LOG2G, gm);
+  if (p.n_gmask > kMaxMasks || p.n_tmask > kMaxMasks) return false;
+  for (int i = 0; i < p.n_gmask; ++i) p.gmask[i] = static_cast<uint32_t>(gm[i]);
+  for (int r = 0; r < p.n_runs; ++r) {
+    uint64_t o = 0;
+    for (int b = 0; b < n_run; ++b) o |= static_cast<uint64_t>((r >> b) & 1) << run_pos[b];
+    p.roff[r] = o;
+  }
+  for (int j = 0; j < (1 << KS); ++j) {
+    uint32_t low = 0, run = 0;
+    int hb = 0;
+    for (int b = 0; b < KS; ++b) {
+      const uint32_t bit = (j >> b) & 1u;
+      if (g.sub_targets[b] < L) low |= bit << g.sub_targets[b];
+      else run |= bit << hb++;
+    }
+    p.soff[j] = (run << L) + low;
+  }
+  const size_t stage = 2 * (size_t{1} << L) * p.n_runs * sizeof(Real);
+  *stages = 3 * stage + 64 <= 200 * 1024 ? 3 : 2;
+  *smem = *stages * stage + 64;
+  return *smem <= 220 * 1024;
+}
+
+template <typename Real, int KS, int STAGES, bool SP>
+void launch_stream(const StreamParams<Real, KS>& p, size_t smem, cudaStream_t s, int num_sms) {
+  auto kern = k_stream<Real, KS, STAGES, SP>;
+  static size_t configured_smem = 0;
+  static int per_sm = 1;
+  if (configured_smem < smem) {
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "k_stream smem");
+    configured_smem = smem;
+  }
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, StreamShape<KS>::kThreads, smem),
+             "k_stream occupancy");
+  const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * std::max(per_sm, 1));
+  kern<<<static_cast<unsigned>(blocks), StreamShape<KS>::kThreads, smem, s>>>(p);
+  cuda_check(cudaGetLastError(), "k_stream launch");
+}
+
+template <typename Real, int KS>
+bool try_stream(const GateLaunch& g, cudaStream_t s, int num_sms) {
+  StreamParams<Real, KS> p;
+  std::memset(&p, 0, sizeof p);
+  size_t smem = 0;
+  int stages = 3;
+  if (!stream_geometry<Real, KS>(g, p, &smem, &stages)) return false;
+  p.re = static_cast<Real*>(g.re);
+  p.im = static_cast<Real*>(g.im);
+  constexpr int D = 1 << KS;
+  for (int e = 0; e < D * D; ++e) {
+    p.mr[e] = static_cast<Real>(g.m_re[e]);
+    p.mi[e] = static_cast<Real>(g.m_im[e]);
+    p.ms[e] = static_cast<Real>(g.m_re[e] + g.m_im[e]);
+    if (p.mr[e] != Real(0)) p.nz[(3 * e) >> 5] |= 1u << ((3 * e) & 31);
+    if (p.mi[e] != Real(0)) p.nz[(3 * e + 1) >> 5] |= 1u << ((3 * e + 1) & 31);
+    if (p.ms[e] != Real(0)) p.nz[(3 * e + 2) >> 5] |= 1u << ((3 * e + 2) & 31);
+  }
+  if (stages == 3) {
+    g.sparse ? launch_stream<Real, KS, 3, true>(p, smem, s, num_sms) : launch_stream<Real, KS, 3, false>(p, smem, s, num_sms);
+  } else {
+    g.sparse ? launch_stream<Real, KS, 2, true>(p, smem, s, num_sms) : launch_stream<Real, KS, 2, false>(p, smem, s, num_sms);
+  }
+  return true;
+}
+
+// ------------------------------------------------------------ stream_dmma
+template <int KS>
+bool dmma_geometry(const GateLaunch& g, DmmaParams<KS>& p, size_t* smem, int* stages) {
+  using S = DmmaShape<KS>;
+  int tg[24], nt = 0;  // all targets (controls + sub-targets), ascending
+  {
+    int a = 0, b = 0;
+    while (a < g.n_ctrl || b < g.ks) {
+      if (b >= g.ks || (a < g.n_ctrl && g.ctrl[a] < g.sub_targets[b])) tg[nt++] = g.ctrl[a++];
+      else tg[nt++] = g.sub_targets[b++];
+    }
+  }
+  int L = S::LOG2G;
+  for (;;) {
+    int below = 0;
+    for (int i = 0; i < nt; ++i) below += tg[i] < L;
+    if (S::LOG2G + below == L) break;
+    L = S::LOG2G + below;
+  }
+  int n_low = 0, high_pos[24], n_high = 0, run_pos[8], n_run = 0, low_pos[24];
+  for (int i = 0; i < nt; ++i) {
+    if (tg[i] < L) low_pos[n_low++] = tg[i];
+    else high_pos[n_high++] = tg[i] - L;
+  }
+  for (int b = 0; b < g.ks; ++b)
+    if (g.sub_targets[b] >= L) run_pos[n_run++] = g.sub_targets[b];
+  if (L + n_high > g.n) return false;
+  const int tile_bits = g.n - L - n_high;
+  p.n_tiles = uint64_t{1} << tile_bits;
+  p.L = L;
+  p.n_runs = 1 << n_run;
+  p.run_stride = (1u << L) + kRunPad;
+  const uint64_t low_mask = (uint64_t{1} << L) - 1;
+  p.ctrl_hi = g.fixed_or & ~low_mask;
+  p.ctrl_lo = static_cast<uint32_t>(g.fixed_or & low_mask);
+  p.n_tmask = insertion_masks(high_pos, n_high, tile_bits, p.tmask);
+  uint64_t gm[kMaxMasks + 12];
+  p.n_gmask = insertion_masks(low_pos, n_low, S::LOG2G, gm);
+  if (p.n_gmask > kMaxMasks || p.n_tmask > kMaxMasks) return false;
+  for (int i = 0; i < p.n_gmask; ++i) p.gmask[i] = static_cast<uint32_t>(gm[i]);
+  for (int r = 0; r < p.n_runs; ++r) {
+    uint64_t o = 0;
+    for (int b = 0; b < n_run; ++b) o |= static_cast<uint64_t>((r >> b) & 1) << run_pos[b];
+    p.roff[r] = o;
+  }
+  for (int j = 0; j < (1 << KS); ++j) {
+    uint32_t low = 0, run = 0;
+    int hb = 0;
+    for (int b = 0; b < KS; ++b) {
+      const uint32_t bit = (j >> b) & 1u;
+      if (g.sub_targets[b] < L) low |= bit << g.sub_targets[b];
+      else run |= bit << hb++;
+    }
+    p.soff[j] = run * p.run_stride + low;
+  }
+  const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(double);
+  *stages = 3 * stage + 64 <= 200 * 1024 ? 3 : 2;
+  *smem = *stages * stage + 64;
+  return *smem <= 220 * 1024;
+}
+
+template <int KS, int STAGES, bool SP>
+void launch_dmma(const DmmaParams<KS>& p, size_t smem, cudaStream_t s, int num_sms) {
+  auto kern = k_stream_dmma<KS, STAGES, SP>;
+  static size_t configured_smem = 0;
+  if (configured_smem < smem) {
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "dmma smem");
+    configured_smem = smem;
+  }
+  int per_sm = 1;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaShape<KS>::kThreads, smem),
+             "dmma occupancy");
+  const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * std::max(per_sm, 1));
+  kern<<<static_cast<unsigned>(blocks), DmmaShape<KS>::kThreads, smem, s>>>(p);
+  cuda_check(cudaGetLastError(), "k_stream_dmma launch");
+}
+
+template <int KS>
+bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
+  using S = DmmaShape<KS>;
+  if (!g.dev_mat) return false;
+  DmmaParams<KS> p;
+  std::memset(&p, 0, sizeof p);
+  size_t smem = 0;
+  int stages = 3;
+  if (!dmma_geometry<KS>(g, p, &smem, &stages)) return false;
+  p.re = static_cast<double*>(g.re);
+  p.im = static_cast<double*>(g.im);
+  p.mat = static_cast<const double*>(g.dev_mat);
+  constexpr int D = S::D;
+  for (int rb = 0; rb < S::RB; ++rb)
+    for (int k = 0; k < S::KST; ++k) {
+      bool nzr = false, nzi = false, nzs = false;
+      for (int r = 8 * rb; r < 8 * rb + 8; ++r)
+        for (int c = 4 * k; c < 4 * k + 4; ++c) {
+          nzr |= g.m_re[r * D + c] != 0.0;
+          nzi |= g.m_im[r * D + c] != 0.0;
+          nzs |= (g.m_re[r * D + c] + g.m_im[r * D + c]) != 0.0;
+        }
+      const int bit = rb * S::KST + k;
+      p.nzblk[0] |= static_cast<uint32_t>(nzr) << bit;
+      p.nzblk[1] |= static_cast<uint32_t>(nzi) << bit;
+      p.nzblk[2] |= static_cast<uint32_t>(nzs) << bit;
+    }
+  const bool sparse = (p.nzblk[0] & p.nzblk[1] & p.nzblk[2]) != (S::RB * S::KST >= 32 ? ~0u : ((1u << (S::RB * S::KST)) - 1));
+  if (stages == 3) {
+    sparse ? launch_dmma<KS, 3, true>(p, smem, s, num_sms) : launch_dmma<KS, 3, false>(p, smem, s, num_sms);
+  } else {
+    sparse ? launch_dmma<KS, 2, true>(p, smem, s, num_sms) : launch_dmma<KS, 2, false>(p, smem, s, num_sms);
+  }
+  return true;
+}
+
+// Full-range non-diagonal sub-gates of 3..5 qubits: complex128 on the DMMA
+// pipe (k_stream_dmma), complex64 ks=3 on the SIMT k_stream.
+template <typename Real>
+bool launch_stream_if(const GateLaunch& g, cudaStream_t s, int num_sms) {
+  if (!g.full_range || (g.klass != 2 && g.klass != 3)) return false;
+  if constexpr (sizeof(Real) == 8) {
+    switch (g.ks) {
+      case 3: return try_dmma<3>(g, s, num_sms);
+      case 4: return try_dmma<4>(g, s, num_sms);
+      case 5: return try_dmma<5>(g, s, num_sms);
+      default: return false;
+    }
+  } else {
+    if (g.ks == 3) return try_stream<Real, 3>(g, s, num_sms);
+    return false;
+  }
+}
+
 // ------------------------------------------------------------------ entry
 template <typename Real>
 int launch_gate_impl(const GateLaunch& g, cudaStream_t s, int num_sms) {
   constexpr int DM = PrecisionTraits<Real>::kDirectMax;
   int klass = g.klass;
   if (klass == 0) return 0;
+  if (launch_stream_if<Real>(g, s, num_sms)) return 1;
   if (klass == 1 && !g.full_range) klass = g.ks <= DM ? 2 : 3;  // sub-range: group-space kernels
   if (klass == 2 && g.ks > DM) klass = 3;
   if (klass == 1) {

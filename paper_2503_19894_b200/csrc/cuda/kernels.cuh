@@ -257,7 +257,7 @@ template <typename Real, int KS, int G, int RT, int GT>
 __global__ void __launch_bounds__(256) k_tile(const __grid_constant__ TileParams<Real> p) {
   using S = TileShape<Real, KS, G, RT, GT>;
   constexpr int D = S::D;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Real* Xr = reinterpret_cast<Real*>(smem_raw);  // [D][G]
   Real* Xi = Xr + D * G;
   Real* Mt = Xi + D * G;  // [D cols][D rows][2] : Mt[(c*D + r)*2 + {0,1}]
