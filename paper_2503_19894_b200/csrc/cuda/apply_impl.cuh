@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <stdexcept>
+#include <cstdlib>
 #include <string>
 
 #include "kernels.cuh"
@@ -336,9 +337,13 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<KS>& p, size_t* smem, int* st
     }
     p.soff[j] = run * p.run_stride + low;
   }
+  // Two CTAs per SM beat deeper pipelines (measured): 3 stages when two CTAs
+  // still fit in shared memory, else 2.
   const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(double);
-  *stages = 3 * stage + 64 <= 200 * 1024 ? 3 : 2;
-  *smem = *stages * stage + 64;
+  const size_t fixed = dmma_m_smem_bytes<KS>() + 128;
+  const size_t per_cta = 110 * 1024;
+  *stages = 3 * stage + fixed <= per_cta ? 3 : 2;
+  *smem = *stages * stage + fixed;
   return *smem <= 220 * 1024;
 }
 
@@ -351,10 +356,10 @@ void launch_dmma(const DmmaParams<KS>& p, size_t smem, cudaStream_t s, int num_s
     configured_smem = smem;
   }
   int per_sm = 1;
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaShape<KS>::kThreads, smem),
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaShape<KS>::kThreads + 32, smem),
              "dmma occupancy");
   const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * std::max(per_sm, 1));
-  kern<<<static_cast<unsigned>(blocks), DmmaShape<KS>::kThreads, smem, s>>>(p);
+  kern<<<static_cast<unsigned>(blocks), DmmaShape<KS>::kThreads + 32, smem, s>>>(p);
   cuda_check(cudaGetLastError(), "k_stream_dmma launch");
 }
 
@@ -386,24 +391,78 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
       p.nzblk[2] |= static_cast<uint32_t>(nzs) << bit;
     }
   const bool sparse = (p.nzblk[0] & p.nzblk[1] & p.nzblk[2]) != (S::RB * S::KST >= 32 ? ~0u : ((1u << (S::RB * S::KST)) - 1));
-  if (stages == 3) {
-    sparse ? launch_dmma<KS, 3, true>(p, smem, s, num_sms) : launch_dmma<KS, 3, false>(p, smem, s, num_sms);
-  } else {
-    sparse ? launch_dmma<KS, 2, true>(p, smem, s, num_sms) : launch_dmma<KS, 2, false>(p, smem, s, num_sms);
+  switch (stages) {
+    case 5: sparse ? launch_dmma<KS, 5, true>(p, smem, s, num_sms) : launch_dmma<KS, 5, false>(p, smem, s, num_sms); break;
+    case 4: sparse ? launch_dmma<KS, 4, true>(p, smem, s, num_sms) : launch_dmma<KS, 4, false>(p, smem, s, num_sms); break;
+    case 3: sparse ? launch_dmma<KS, 3, true>(p, smem, s, num_sms) : launch_dmma<KS, 3, false>(p, smem, s, num_sms); break;
+    default: sparse ? launch_dmma<KS, 2, true>(p, smem, s, num_sms) : launch_dmma<KS, 2, false>(p, smem, s, num_sms); break;
   }
   return true;
 }
 
+// ---------------------------------------------------------- dmma_direct
+template <int KS>
+bool try_dmma_direct(const GateLaunch& g, cudaStream_t s, int num_sms) {
+  using S = DdShape<KS>;
+  if (!g.dev_mat) return false;
+  const uint64_t count = g.g_end - g.g_begin;
+  if (count % S::GI != 0 || count == 0) return false;
+  DdParams<KS> p;
+  std::memset(&p, 0, sizeof p);
+  p.re = static_cast<double*>(g.re);
+  p.im = static_cast<double*>(g.im);
+  p.mat = static_cast<const double*>(g.dev_mat);
+  p.g_begin = g.g_begin;
+  p.n_items = count / S::GI;
+  p.fixed_or = g.fixed_or;
+  p.n_masks = g.n_masks;
+  for (int i = 0; i < g.n_masks; ++i) p.masks[i] = g.masks[i];
+  for (int j = 0; j < S::D; ++j) p.off[j] = g.off[j];
+  bool all = true;
+  for (int rb = 0; rb < S::RB; ++rb)
+    for (int k = 0; k < S::KST; ++k) {
+      bool nz[3] = {false, false, false};
+      for (int r = 8 * rb; r < 8 * rb + 8; ++r)
+        for (int c = 4 * k; c < 4 * k + 4; ++c) {
+          nz[0] |= g.m_re[r * S::D + c] != 0.0;
+          nz[1] |= g.m_im[r * S::D + c] != 0.0;
+          nz[2] |= (g.m_re[r * S::D + c] + g.m_im[r * S::D + c]) != 0.0;
+        }
+      for (int m = 0; m < 3; ++m) {
+        p.nzblk[m] |= static_cast<uint32_t>(nz[m]) << (rb * S::KST + k);
+        all &= nz[m];
+      }
+    }
+  auto kern = all ? k_dmma_direct<KS, false> : k_dmma_direct<KS, true>;
+  int per_sm = 1;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * S::kWarps, 0), "dmma_direct occupancy");
+  const uint64_t blocks =
+      std::min<uint64_t>((p.n_items + S::kWarps - 1) / S::kWarps, uint64_t(num_sms) * std::max(per_sm, 1));
+  kern<<<static_cast<unsigned>(blocks), 32 * S::kWarps, 0, s>>>(p);
+  cuda_check(cudaGetLastError(), "k_dmma_direct launch");
+  return true;
+}
+
+inline int dmma_mode() {
+  static int mode = [] {
+    const char* e = std::getenv("TSG_DMMA_MODE");
+    if (!e) return 0;
+    return std::string(e) == "direct" ? 1 : (std::string(e) == "stream" ? 2 : 0);
+  }();
+  return mode;
+}
+
 // Full-range non-diagonal sub-gates of 3..5 qubits: complex128 on the DMMA
-// pipe (k_stream_dmma), complex64 ks=3 on the SIMT k_stream.
+// pipe (k_stream_dmma or k_dmma_direct), complex64 ks=3 on the SIMT k_stream.
 template <typename Real>
 bool launch_stream_if(const GateLaunch& g, cudaStream_t s, int num_sms) {
   if (!g.full_range || (g.klass != 2 && g.klass != 3)) return false;
   if constexpr (sizeof(Real) == 8) {
+    const bool direct = dmma_mode() == 1;
     switch (g.ks) {
-      case 3: return try_dmma<3>(g, s, num_sms);
-      case 4: return try_dmma<4>(g, s, num_sms);
-      case 5: return try_dmma<5>(g, s, num_sms);
+      case 3: return direct ? try_dmma_direct<3>(g, s, num_sms) : try_dmma<3>(g, s, num_sms);
+      case 4: return direct ? try_dmma_direct<4>(g, s, num_sms) : try_dmma<4>(g, s, num_sms);
+      case 5: return direct ? try_dmma_direct<5>(g, s, num_sms) : try_dmma<5>(g, s, num_sms);
       default: return false;
     }
   } else {

@@ -17,9 +17,15 @@
 // Mr / Mi / Ms that is all zero skips its DMMA (warp-uniform), which is the
 // block form of SPEC's zero-skipping.
 //
-// Runs are laid out in shared memory with a stride of 2^L + 8 doubles so the
-// four k-rows of a B fragment (different runs when the targets are high) fall
-// in different bank halves: each LDS.64 costs the minimum two wavefronts.
+// Runs are laid out in shared memory with a stride of 2^L + 4 doubles: 64-bit
+// shared loads are served per half-warp, and a stride of 8 banks puts the four
+// k-rows of a B fragment (different runs when the targets are high) in four
+// distinct bank quarters, so each LDS.64 costs the minimum two wavefronts.
+//
+// Warp roles: warp W (the last) is the producer -- one lane issues every bulk
+// load (full[s] mbarrier, complete_tx) and bulk store (after empty[s]); warps
+// 0..W-1 only wait on full[s], run the DMMA product, synchronise among
+// themselves with a named barrier and arrive on empty[s].
 #pragma once
 
 #include <cstdint>
@@ -28,7 +34,7 @@
 
 namespace tsg {
 
-constexpr int kRunPad = 8;  // doubles between runs in shared memory
+constexpr int kRunPad = 4;  // doubles between runs in shared memory
 
 template <int KS>
 struct DmmaShape {
@@ -80,32 +86,116 @@ __device__ __forceinline__ uint32_t dmma_group_base(const DmmaParams<KS>& p, uin
   return b | p.ctrl_lo;
 }
 
+// M fragments live in registers for ks <= 4; for ks = 5 they are staged in
+// shared memory in fragment order ([3][KST][RB][32 lanes], conflict-free
+// LDS.64) so the consumer warps fit 2 CTAs per SM.
+template <int KS>
+__host__ __device__ constexpr bool dmma_m_in_regs() {
+  return KS <= 4;
+}
+template <int KS>
+__host__ __device__ constexpr size_t dmma_m_smem_bytes() {
+  return dmma_m_in_regs<KS>() ? 0 : size_t{3} * DmmaShape<KS>::KST * DmmaShape<KS>::RB * 32 * sizeof(double);
+}
+
 template <int KS, int STAGES, bool SPARSE>
-__global__ void __launch_bounds__(DmmaShape<KS>::kThreads) k_stream_dmma(const __grid_constant__ DmmaParams<KS> p) {
+__global__ void __launch_bounds__(DmmaShape<KS>::kThreads + 32, 2) k_stream_dmma(const __grid_constant__ DmmaParams<KS> p) {
   using S = DmmaShape<KS>;
+  constexpr bool MREG = dmma_m_in_regs<KS>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t run_len = 1u << p.L;
   const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
-  double* buf = reinterpret_cast<double*>(smem_raw);  // [STAGES][2][stage_elems]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double) * 2 * STAGES * stage_elems);
+  double* mfrag = reinterpret_cast<double*>(smem_raw);  // [3][KST][RB][32] when !MREG
+  double* buf = reinterpret_cast<double*>(smem_raw + dmma_m_smem_bytes<KS>());  // [STAGES][2][stage_elems]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(buf) +
+                                               sizeof(double) * 2 * STAGES * stage_elems);
+  uint64_t* empty = full + STAGES;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t run_bytes = run_len * sizeof(double);
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], S::W);
+    }
+    mbar_fence_init();
+  }
+  if constexpr (!MREG) {
+    constexpr int DD = S::D * S::D;
+    constexpr int NF = 3 * S::KST * S::RB * 32;
+    for (int f = tid; f < NF; f += blockDim.x) {
+      const int ln = f % 32, rbf = (f / 32) % S::RB, k = (f / (32 * S::RB)) % S::KST, m = f / (32 * S::RB * S::KST);
+      mfrag[f] = p.mat[m * DD + (8 * rbf + (ln >> 2)) * S::D + 4 * k + (ln & 3)];
+    }
+  }
+  __syncthreads();
+
+  auto tile_base = [&](uint64_t tile) {
+    uint64_t b = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxMasks; ++i)
+      if (i < p.n_tmask) b += (tile & p.tmask[i]) << i;
+    return (b << p.L) | p.ctrl_hi;
+  };
+
+  if (warp == S::W) {
+    // ---------------- producer warp: TMA bulk loads and stores ------------
+    // Copies are spread over the 32 lanes (lane l owns runs l, l+32, ...);
+    // bulk groups are per thread, so every lane waits for its own stores.
+    auto load = [&](uint64_t tile, int s) {
+      const uint64_t base = tile_base(tile);
+      double* dr = buf + (2 * s) * stage_elems;
+      double* di = dr + stage_elems;
+      if (lane == 0) mbar_expect_tx(&full[s], 2u * run_bytes * static_cast<uint32_t>(p.n_runs));
+      __syncwarp();
+      for (int r = lane; r < p.n_runs; r += 32) {
+        bulk_g2s(dr + r * p.run_stride, p.re + base + p.roff[r], run_bytes, &full[s]);
+        bulk_g2s(di + r * p.run_stride, p.im + base + p.roff[r], run_bytes, &full[s]);
+      }
+    };
+    for (int s = 0; s < STAGES; ++s)
+      if (first + s * step < p.n_tiles) load(first + s * step, s);
+    uint32_t j = 0;
+    for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
+      const int s = static_cast<int>(j % STAGES);
+      mbar_wait(&empty[s], (j / STAGES) & 1u);  // consumers wrote tile j's results
+      const uint64_t base = tile_base(tile);
+      const double* sr = buf + (2 * s) * stage_elems;
+      const double* si = sr + stage_elems;
+      for (int r = lane; r < p.n_runs; r += 32) {
+        bulk_s2g(p.re + base + p.roff[r], sr + r * p.run_stride, run_bytes);
+        bulk_s2g(p.im + base + p.roff[r], si + r * p.run_stride, run_bytes);
+      }
+      bulk_commit();
+      const uint64_t next = tile + STAGES * step;
+      if (next < p.n_tiles) {
+        bulk_wait_read_all();  // this lane's stores have read the stage
+        __syncwarp();
+        load(next, s);
+      }
+    }
+    bulk_wait_all();
+    return;
+  }
+
+  // ---------------- consumer warps: Y = M X on the DMMA pipe --------------
   const int rb = warp / S::WG, wg = warp % S::WG;
   const int lr = lane >> 2, lc = lane & 3;
-  const uint32_t run_bytes = run_len * sizeof(double);
-
-  // M fragments for this warp's row block, for the kernel's lifetime
-  double amr[S::KST], ami[S::KST], ams[S::KST];
-  constexpr int DD = S::D * S::D;
+  double amr[MREG ? S::KST : 1], ami[MREG ? S::KST : 1], ams[MREG ? S::KST : 1];
+  if constexpr (MREG) {
+    constexpr int DD = S::D * S::D;
 #pragma unroll
-  for (int k = 0; k < S::KST; ++k) {
-    const int e = (8 * rb + lr) * S::D + 4 * k + lc;
-    amr[k] = p.mat[e];
-    ami[k] = p.mat[DD + e];
-    ams[k] = p.mat[2 * DD + e];
+    for (int k = 0; k < S::KST; ++k) {
+      const int e = (8 * rb + lr) * S::D + 4 * k + lc;
+      amr[k] = p.mat[e];
+      ami[k] = p.mat[DD + e];
+      ams[k] = p.mat[2 * DD + e];
+    }
   }
-  // per-thread shared offsets: B rows, C rows, group bases (tile independent)
+  const double* mf = mfrag + rb * 32 + lane;  // fragment (m, k) at mf[(m * KST + k) * RB * 32]
   uint32_t offb[S::KST], lbb[S::NR], lbc[S::NR][2];
 #pragma unroll
   for (int k = 0; k < S::KST; ++k) offb[k] = p.soff[4 * k + lc];
@@ -118,44 +208,10 @@ __global__ void __launch_bounds__(DmmaShape<KS>::kThreads) k_stream_dmma(const _
     lbc[nb][1] = dmma_group_base(p, g0 + 2 * lc + 1);
   }
 
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  auto tile_base = [&](uint64_t tile) {
-    uint64_t b = 0;
-#pragma unroll
-    for (int i = 0; i < kMaxMasks; ++i)
-      if (i < p.n_tmask) b += (tile & p.tmask[i]) << i;
-    return (b << p.L) | p.ctrl_hi;
-  };
-  auto issue_load = [&](uint64_t tile, int s) {
-    const uint64_t base = tile_base(tile);
-    double* dr = buf + (2 * s) * stage_elems;
-    double* di = dr + stage_elems;
-    mbar_expect_tx(&bars[s], 2u * run_bytes * static_cast<uint32_t>(p.n_runs));
-    for (int r = 0; r < p.n_runs; ++r) {
-      bulk_g2s(dr + r * p.run_stride, p.re + base + p.roff[r], run_bytes, &bars[s]);
-      bulk_g2s(di + r * p.run_stride, p.im + base + p.roff[r], run_bytes, &bars[s]);
-    }
-  };
-
-  const uint64_t first = blockIdx.x, step = gridDim.x;
-  if (tid == 0)
-    for (int s = 0; s < STAGES; ++s)
-      if (first + s * step < p.n_tiles) issue_load(first + s * step, s);
-
-  uint32_t it = 0;
-  for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++it) {
-    const int s = static_cast<int>(it % STAGES);
-    if (tid == 0 && it > 0) {
-      bulk_wait_read_all();  // the previous stage's bulk store has read smem
-      const uint64_t next = tile + (STAGES - 1) * step;
-      if (next < p.n_tiles) issue_load(next, static_cast<int>((it + STAGES - 1) % STAGES));
-    }
-    mbar_wait(&bars[s], (it / STAGES) & 1u);
+  uint32_t j = 0;
+  for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
+    const int s = static_cast<int>(j % STAGES);
+    mbar_wait(&full[s], (j / STAGES) & 1u);
     double* xr = buf + (2 * s) * stage_elems;
     double* xi = xr + stage_elems;
 
@@ -168,16 +224,27 @@ __global__ void __launch_bounds__(DmmaShape<KS>::kThreads) k_stream_dmma(const _
       const bool use_r = !SPARSE || ((p.nzblk[0] >> bit) & 1u);
       const bool use_i = !SPARSE || ((p.nzblk[1] >> bit) & 1u);
       const bool use_s = !SPARSE || ((p.nzblk[2] >> bit) & 1u);
+      double fr, fi, fs;
+      if constexpr (MREG) {
+        fr = amr[k];
+        fi = ami[k];
+        fs = ams[k];
+      } else {
+        fr = mf[(0 * S::KST + k) * S::RB * 32];
+        fi = mf[(1 * S::KST + k) * S::RB * 32];
+        fs = mf[(2 * S::KST + k) * S::RB * 32];
+      }
 #pragma unroll
       for (int nb = 0; nb < S::NR; ++nb) {
         const double br = xr[lbb[nb] + offb[k]];
         const double bi = xi[lbb[nb] + offb[k]];
-        if (use_r) dmma(t1[nb], amr[k], br);
-        if (use_i) dmma(t2[nb], ami[k], bi);
-        if (use_s) dmma(t3[nb], ams[k], br + bi);
+        if (use_r) dmma(t1[nb], fr, br);
+        if (use_i) dmma(t2[nb], fi, bi);
+        if (use_s) dmma(t3[nb], fs, br + bi);
       }
     }
-    __syncthreads();  // every warp has read the stage: write results in place
+    // all consumer warps have read the stage before anyone overwrites it
+    asm volatile("bar.sync 1, %0;" ::"r"(S::kThreads) : "memory");
 #pragma unroll
     for (int nb = 0; nb < S::NR; ++nb)
 #pragma unroll
@@ -186,18 +253,118 @@ __global__ void __launch_bounds__(DmmaShape<KS>::kThreads) k_stream_dmma(const _
         xr[a] = t1[nb][i] - t2[nb][i];
         xi[a] = t3[nb][i] - t1[nb][i] - t2[nb][i];
       }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      const uint64_t base = tile_base(tile);
-      for (int r = 0; r < p.n_runs; ++r) {
-        bulk_s2g(p.re + base + p.roff[r], xr + r * p.run_stride, run_bytes);
-        bulk_s2g(p.im + base + p.roff[r], xi + r * p.run_stride, run_bytes);
-      }
-      bulk_commit();
+    fence_async_smem();  // generic-proxy writes -> async-proxy bulk store
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+  }
+}
+
+// --------------------------------------------------------------------------
+// k_dmma_direct: the same DMMA product without shared-memory staging of X.
+// Every warp owns work items of 8*NR consecutive groups and runs them
+// independently (no CTA barriers): it loads its B fragments straight from
+// global memory (lane (lr, lc) reads element 4k+lc of group 8nb+lr: every
+// 32-byte sector is fully used), multiplies by M fragments kept in shared
+// memory in fragment order, and stores its C fragments back in place.  All
+// loads of an item precede its stores, and items are disjoint, so the update
+// is in-place safe.
+template <int KS>
+struct DdShape {
+  static constexpr int D = 1 << KS;
+  static constexpr int RB = D / 8;
+  static constexpr int KST = D / 4;
+  static constexpr int NR = KS >= 5 ? 1 : (KS == 4 ? 2 : 4);  // 8-group blocks per item
+  static constexpr int GI = 8 * NR;                            // groups per item
+  static constexpr int kWarps = 4;
+};
+
+template <int KS>
+struct DdParams {
+  double* re;
+  double* im;
+  const double* mat;  // [Mr | Mi | Ms], D x D each (device)
+  uint64_t g_begin;
+  uint64_t n_items;
+  uint64_t fixed_or;
+  uint64_t masks[kMaxMasks];
+  int n_masks;
+  uint64_t off[1 << KS];
+  uint32_t nzblk[3];
+};
+
+template <int KS>
+__device__ __forceinline__ uint64_t dd_base(const DdParams<KS>& p, uint64_t t) {
+  uint64_t b = 0;
+#pragma unroll
+  for (int i = 0; i < kMaxMasks; ++i)
+    if (i < p.n_masks) b += (t & p.masks[i]) << i;
+  return b | p.fixed_or;
+}
+
+template <int KS, bool SPARSE>
+__global__ void __launch_bounds__(32 * DdShape<KS>::kWarps) k_dmma_direct(const __grid_constant__ DdParams<KS> p) {
+  using S = DdShape<KS>;
+  __shared__ double mfrag[3 * S::KST * S::RB * 32];  // [m][k][rb][lane]
+  {
+    constexpr int DD = S::D * S::D;
+    for (int f = threadIdx.x; f < 3 * S::KST * S::RB * 32; f += blockDim.x) {
+      const int ln = f % 32, rbf = (f / 32) % S::RB, k = (f / (32 * S::RB)) % S::KST, m = f / (32 * S::RB * S::KST);
+      mfrag[f] = p.mat[m * DD + (8 * rbf + (ln >> 2)) * S::D + 4 * k + (ln & 3)];
     }
   }
-  if (tid == 0) bulk_wait_all();
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lc = lane & 3;
+  uint64_t offb[S::KST];
+#pragma unroll
+  for (int k = 0; k < S::KST; ++k) offb[k] = p.off[4 * k + lc];
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * S::kWarps;
+  for (uint64_t item = static_cast<uint64_t>(blockIdx.x) * S::kWarps + warp; item < p.n_items; item += stride) {
+    const uint64_t g0 = p.g_begin + item * S::GI;
+    double xr[S::NR][S::KST], xi[S::NR][S::KST];
+#pragma unroll
+    for (int nb = 0; nb < S::NR; ++nb) {
+      const uint64_t b = dd_base(p, g0 + 8 * nb + lr);
+#pragma unroll
+      for (int k = 0; k < S::KST; ++k) {
+        xr[nb][k] = p.re[b + offb[k]];
+        xi[nb][k] = p.im[b + offb[k]];
+      }
+    }
+    double t1[S::RB][S::NR][2], t2[S::RB][S::NR][2], t3[S::RB][S::NR][2];
+#pragma unroll
+    for (int rb = 0; rb < S::RB; ++rb)
+#pragma unroll
+      for (int nb = 0; nb < S::NR; ++nb)
+        t1[rb][nb][0] = t1[rb][nb][1] = t2[rb][nb][0] = t2[rb][nb][1] = t3[rb][nb][0] = t3[rb][nb][1] = 0.0;
+#pragma unroll
+    for (int k = 0; k < S::KST; ++k) {
+#pragma unroll
+      for (int rb = 0; rb < S::RB; ++rb) {
+        const int bit = rb * S::KST + k;
+        const double* mf = mfrag + (k * S::RB + rb) * 32 + lane;
+        const double fr = mf[0], fi = mf[S::KST * S::RB * 32], fs = mf[2 * S::KST * S::RB * 32];
+#pragma unroll
+        for (int nb = 0; nb < S::NR; ++nb) {
+          if (!SPARSE || ((p.nzblk[0] >> bit) & 1u)) dmma(t1[rb][nb], fr, xr[nb][k]);
+          if (!SPARSE || ((p.nzblk[1] >> bit) & 1u)) dmma(t2[rb][nb], fi, xi[nb][k]);
+          if (!SPARSE || ((p.nzblk[2] >> bit) & 1u)) dmma(t3[rb][nb], fs, xr[nb][k] + xi[nb][k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int nb = 0; nb < S::NR; ++nb)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint64_t b = dd_base(p, g0 + 8 * nb + 2 * lc + i);
+#pragma unroll
+        for (int rb = 0; rb < S::RB; ++rb) {
+          const uint64_t a = b + p.off[8 * rb + lr];
+          p.re[a] = t1[rb][nb][i] - t2[rb][nb][i];
+          p.im[a] = t3[rb][nb][i] - t1[rb][nb][i] - t2[rb][nb][i];
+        }
+      }
+  }
 }
 
 }  // namespace tsg
