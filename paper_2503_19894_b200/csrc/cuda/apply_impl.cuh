@@ -128,7 +128,7 @@ void run_tile(const GateLaunch& g, cudaStream_t s, int num_sms) {
   std::memset(&p, 0, sizeof p);
   p.re = static_cast<Real*>(g.re);
   p.im = static_cast<Real*>(g.im);
-  p.mat = static_cast<const Real*>(g.dev_mat);
+  p.mat = static_cast<const double*>(g.dev_mat);
   if (!p.mat) throw std::runtime_error("tile kernel launched without a device matrix");
   p.g_begin = g.g_begin;
   p.n_groups = g.g_end - g.g_begin;
@@ -283,9 +283,9 @@ bool try_stream(const GateLaunch& g, cudaStream_t s, int num_sms) {
 }
 
 // ------------------------------------------------------------ stream_dmma
-template <int KS>
-bool dmma_geometry(const GateLaunch& g, DmmaParams<KS>& p, size_t* smem, int* stages) {
-  using S = DmmaShape<KS>;
+template <typename Real, int KS>
+bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, int* stages) {
+  using S = DShape<Real, KS>;
   int tg[24], nt = 0;  // all targets (controls + sub-targets), ascending
   {
     int a = 0, b = 0;
@@ -313,7 +313,7 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<KS>& p, size_t* smem, int* st
   p.n_tiles = uint64_t{1} << tile_bits;
   p.L = L;
   p.n_runs = 1 << n_run;
-  p.run_stride = (1u << L) + kRunPad;
+  p.run_stride = (1u << L) + kRunPadBytes / sizeof(Real);
   const uint64_t low_mask = (uint64_t{1} << L) - 1;
   p.ctrl_hi = g.fixed_or & ~low_mask;
   p.ctrl_lo = static_cast<uint32_t>(g.fixed_or & low_mask);
@@ -339,7 +339,7 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<KS>& p, size_t* smem, int* st
   }
   // Two CTAs per SM beat deeper pipelines (measured): 3 stages when two CTAs
   // still fit in shared memory, else 2.
-  const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(double);
+  const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(Real);
   const size_t fixed = dmma_m_smem_bytes<KS>() + 128;
   const size_t per_cta = 110 * 1024;
   *stages = 3 * stage + fixed <= per_cta ? 3 : 2;
@@ -347,33 +347,33 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<KS>& p, size_t* smem, int* st
   return *smem <= 220 * 1024;
 }
 
-template <int KS, int STAGES, bool SP>
-void launch_dmma(const DmmaParams<KS>& p, size_t smem, cudaStream_t s, int num_sms) {
-  auto kern = k_stream_dmma<KS, STAGES, SP>;
+template <typename Real, int KS, int STAGES, bool SP>
+void launch_dmma(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int num_sms) {
+  auto kern = k_stream_dmma<Real, KS, STAGES, SP>;
   static size_t configured_smem = 0;
   if (configured_smem < smem) {
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "dmma smem");
     configured_smem = smem;
   }
   int per_sm = 1;
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaShape<KS>::kThreads + 32, smem),
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DShape<Real, KS>::kThreads + 32, smem),
              "dmma occupancy");
   const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * std::max(per_sm, 1));
-  kern<<<static_cast<unsigned>(blocks), DmmaShape<KS>::kThreads + 32, smem, s>>>(p);
+  kern<<<static_cast<unsigned>(blocks), DShape<Real, KS>::kThreads + 32, smem, s>>>(p);
   cuda_check(cudaGetLastError(), "k_stream_dmma launch");
 }
 
-template <int KS>
+template <typename Real, int KS>
 bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
-  using S = DmmaShape<KS>;
+  using S = DShape<Real, KS>;
   if (!g.dev_mat) return false;
-  DmmaParams<KS> p;
+  DmmaParams<Real, KS> p;
   std::memset(&p, 0, sizeof p);
   size_t smem = 0;
   int stages = 3;
-  if (!dmma_geometry<KS>(g, p, &smem, &stages)) return false;
-  p.re = static_cast<double*>(g.re);
-  p.im = static_cast<double*>(g.im);
+  if (!dmma_geometry<Real, KS>(g, p, &smem, &stages)) return false;
+  p.re = static_cast<Real*>(g.re);
+  p.im = static_cast<Real*>(g.im);
   p.mat = static_cast<const double*>(g.dev_mat);
   constexpr int D = S::D;
   for (int rb = 0; rb < S::RB; ++rb)
@@ -392,10 +392,10 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
     }
   const bool sparse = (p.nzblk[0] & p.nzblk[1] & p.nzblk[2]) != (S::RB * S::KST >= 32 ? ~0u : ((1u << (S::RB * S::KST)) - 1));
   switch (stages) {
-    case 5: sparse ? launch_dmma<KS, 5, true>(p, smem, s, num_sms) : launch_dmma<KS, 5, false>(p, smem, s, num_sms); break;
-    case 4: sparse ? launch_dmma<KS, 4, true>(p, smem, s, num_sms) : launch_dmma<KS, 4, false>(p, smem, s, num_sms); break;
-    case 3: sparse ? launch_dmma<KS, 3, true>(p, smem, s, num_sms) : launch_dmma<KS, 3, false>(p, smem, s, num_sms); break;
-    default: sparse ? launch_dmma<KS, 2, true>(p, smem, s, num_sms) : launch_dmma<KS, 2, false>(p, smem, s, num_sms); break;
+    case 5: sparse ? launch_dmma<Real, KS, 5, true>(p, smem, s, num_sms) : launch_dmma<Real, KS, 5, false>(p, smem, s, num_sms); break;
+    case 4: sparse ? launch_dmma<Real, KS, 4, true>(p, smem, s, num_sms) : launch_dmma<Real, KS, 4, false>(p, smem, s, num_sms); break;
+    case 3: sparse ? launch_dmma<Real, KS, 3, true>(p, smem, s, num_sms) : launch_dmma<Real, KS, 3, false>(p, smem, s, num_sms); break;
+    default: sparse ? launch_dmma<Real, KS, 2, true>(p, smem, s, num_sms) : launch_dmma<Real, KS, 2, false>(p, smem, s, num_sms); break;
   }
   return true;
 }
@@ -460,14 +460,18 @@ bool launch_stream_if(const GateLaunch& g, cudaStream_t s, int num_sms) {
   if constexpr (sizeof(Real) == 8) {
     const bool direct = dmma_mode() == 1;
     switch (g.ks) {
-      case 3: return direct ? try_dmma_direct<3>(g, s, num_sms) : try_dmma<3>(g, s, num_sms);
-      case 4: return direct ? try_dmma_direct<4>(g, s, num_sms) : try_dmma<4>(g, s, num_sms);
-      case 5: return direct ? try_dmma_direct<5>(g, s, num_sms) : try_dmma<5>(g, s, num_sms);
+      case 3: return direct ? try_dmma_direct<3>(g, s, num_sms) : try_dmma<double, 3>(g, s, num_sms);
+      case 4: return direct ? try_dmma_direct<4>(g, s, num_sms) : try_dmma<double, 4>(g, s, num_sms);
+      case 5: return direct ? try_dmma_direct<5>(g, s, num_sms) : try_dmma<double, 5>(g, s, num_sms);
       default: return false;
     }
   } else {
-    if (g.ks == 3) return try_stream<Real, 3>(g, s, num_sms);
-    return false;
+    switch (g.ks) {  // complex64: widened to FP64 on the DMMA pipe
+      case 3: return try_dmma<float, 3>(g, s, num_sms);
+      case 4: return try_dmma<float, 4>(g, s, num_sms);
+      case 5: return try_dmma<float, 5>(g, s, num_sms);
+      default: return false;
+    }
   }
 }
 

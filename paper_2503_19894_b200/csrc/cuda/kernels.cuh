@@ -237,7 +237,7 @@ template <typename Real>
 struct TileParams {
   Real* re;
   Real* im;
-  const Real* mat;  // [D*D re][D*D im], row-major
+  const double* mat;  // [D*D re][D*D im][D*D re+im], row-major, FP64 for both precisions
   uint64_t g_begin, n_groups, n_tiles;
   uint64_t fixed_or;
   uint64_t masks[kMaxMasks];
@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(256) k_tile(const __grid_constant__ TileParams
 
   for (int i = threadIdx.x; i < D * D; i += blockDim.x) {
     const int r = i / D, c = i % D;
-    Mt[(c * D + r) * 2] = p.mat[i];
-    Mt[(c * D + r) * 2 + 1] = p.mat[D * D + i];
+    Mt[(c * D + r) * 2] = static_cast<Real>(p.mat[i]);
+    Mt[(c * D + r) * 2 + 1] = static_cast<Real>(p.mat[D * D + i]);
   }
   const int gb = threadIdx.x % (G / GT);
   const int rb = threadIdx.x / (G / GT);

@@ -34,27 +34,41 @@
 
 namespace tsg {
 
-constexpr int kRunPad = 4;  // doubles between runs in shared memory
+// padding between runs in shared memory: 32 bytes = 8 banks, so the four
+// k-rows of a B fragment land in distinct bank quarters (both precisions)
+constexpr int kRunPadBytes = 32;
 
-template <int KS>
+// A tile holds 2^AMPS_LOG2 amplitudes (2048 for complex128, 4096 for
+// complex64 -- the per-tile pipeline latency is roughly fixed, so tiles are
+// sized in amplitudes, measured); every consumer warp owns 8 n-blocks of 8
+// groups for one 8-row block.
+template <int KS, int AMPS_LOG2 = 11, int NRB = 8>
 struct DmmaShape {
   static constexpr int D = 1 << KS;
   static constexpr int RB = D / 8;               // 8-row blocks
   static constexpr int WR = RB;                  // one warp per row block
-  static constexpr int WG = RB >= 4 ? 1 : 4 / RB;
+  static constexpr int LOG2G = AMPS_LOG2 - KS;   // groups per tile
+  static constexpr int G = 1 << LOG2G;
+  static constexpr int NR = NRB;                 // 8-group blocks per warp
+  static constexpr int GW = 8 * NR;              // groups per warp
+  static constexpr int WG = G / GW;              // warps across groups
   static constexpr int W = WR * WG;
   static constexpr int kThreads = 32 * W;
-  static constexpr int G = 64;                   // groups per tile
-  static constexpr int LOG2G = 6;
-  static constexpr int GW = G / WG;              // groups per warp
-  static constexpr int NR = GW / 8;              // 8-group blocks per warp
   static constexpr int KST = D / 4;              // k-steps
+  static_assert(WG >= 1, "tile too small");
 };
+// 8 n-blocks per warp where registers allow; 4 for the widest sub-gates so
+// that 16 consumer warps fit per SM (DMMA issue needs the warps).
+template <typename Real, int KS>
+using DShape = DmmaShape<KS, sizeof(Real) == 8 ? 11 : 12, (KS >= 5 || (sizeof(Real) == 4 && KS >= 4)) ? 4 : 8>;
 
-template <int KS>
+// Real = storage type of the state (double: complex128, float: complex64);
+// the product always runs in FP64 on the DMMA pipe (complex64 amplitudes are
+// widened on load and rounded once on store).
+template <typename Real, int KS>
 struct DmmaParams {
-  double* re;
-  double* im;
+  Real* re;
+  Real* im;
   const double* mat;  // [Mr | Mi | Ms], each D x D row-major (device)
   uint64_t n_tiles;
   uint64_t ctrl_hi;   // active control values at or above bit L
@@ -63,7 +77,7 @@ struct DmmaParams {
   int n_tmask;
   int L;
   int n_runs;
-  uint32_t run_stride;  // 2^L + kRunPad
+  uint32_t run_stride;  // 2^L + kRunPadBytes / sizeof(Real)
   uint32_t gmask[kMaxMasks];
   int n_gmask;
   uint64_t roff[1 << KS];  // global offset of run r
@@ -77,8 +91,8 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int KS>
-__device__ __forceinline__ uint32_t dmma_group_base(const DmmaParams<KS>& p, uint32_t g) {
+template <typename Real, int KS>
+__device__ __forceinline__ uint32_t dmma_group_base(const DmmaParams<Real, KS>& p, uint32_t g) {
   uint32_t b = 0;
 #pragma unroll
   for (int i = 0; i < kMaxMasks; ++i)
@@ -98,22 +112,23 @@ __host__ __device__ constexpr size_t dmma_m_smem_bytes() {
   return dmma_m_in_regs<KS>() ? 0 : size_t{3} * DmmaShape<KS>::KST * DmmaShape<KS>::RB * 32 * sizeof(double);
 }
 
-template <int KS, int STAGES, bool SPARSE>
-__global__ void __launch_bounds__(DmmaShape<KS>::kThreads + 32, 2) k_stream_dmma(const __grid_constant__ DmmaParams<KS> p) {
-  using S = DmmaShape<KS>;
+template <typename Real, int KS, int STAGES, bool SPARSE>
+__global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, KS>::W >= 16 ? 1 : 2)
+    k_stream_dmma(const __grid_constant__ DmmaParams<Real, KS> p) {
+  using S = DShape<Real, KS>;
   constexpr bool MREG = dmma_m_in_regs<KS>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t run_len = 1u << p.L;
   const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
   double* mfrag = reinterpret_cast<double*>(smem_raw);  // [3][KST][RB][32] when !MREG
-  double* buf = reinterpret_cast<double*>(smem_raw + dmma_m_smem_bytes<KS>());  // [STAGES][2][stage_elems]
+  Real* buf = reinterpret_cast<Real*>(smem_raw + dmma_m_smem_bytes<KS>());  // [STAGES][2][stage_elems]
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(buf) +
-                                               sizeof(double) * 2 * STAGES * stage_elems);
+                                               sizeof(Real) * 2 * STAGES * stage_elems);
   uint64_t* empty = full + STAGES;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const uint32_t run_bytes = run_len * sizeof(double);
+  const uint32_t run_bytes = run_len * sizeof(Real);
   const uint64_t first = blockIdx.x, step = gridDim.x;
 
   if (tid == 0) {
@@ -147,8 +162,8 @@ __global__ void __launch_bounds__(DmmaShape<KS>::kThreads + 32, 2) k_stream_dmma
     // bulk groups are per thread, so every lane waits for its own stores.
     auto load = [&](uint64_t tile, int s) {
       const uint64_t base = tile_base(tile);
-      double* dr = buf + (2 * s) * stage_elems;
-      double* di = dr + stage_elems;
+      Real* dr = buf + (2 * s) * stage_elems;
+      Real* di = dr + stage_elems;
       if (lane == 0) mbar_expect_tx(&full[s], 2u * run_bytes * static_cast<uint32_t>(p.n_runs));
       __syncwarp();
       for (int r = lane; r < p.n_runs; r += 32) {
@@ -163,8 +178,8 @@ __global__ void __launch_bounds__(DmmaShape<KS>::kThreads + 32, 2) k_stream_dmma
       const int s = static_cast<int>(j % STAGES);
       mbar_wait(&empty[s], (j / STAGES) & 1u);  // consumers wrote tile j's results
       const uint64_t base = tile_base(tile);
-      const double* sr = buf + (2 * s) * stage_elems;
-      const double* si = sr + stage_elems;
+      const Real* sr = buf + (2 * s) * stage_elems;
+      const Real* si = sr + stage_elems;
       for (int r = lane; r < p.n_runs; r += 32) {
         bulk_s2g(p.re + base + p.roff[r], sr + r * p.run_stride, run_bytes);
         bulk_s2g(p.im + base + p.roff[r], si + r * p.run_stride, run_bytes);
@@ -212,8 +227,8 @@ __global__ void __launch_bounds__(DmmaShape<KS>::kThreads + 32, 2) k_stream_dmma
   for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
     const int s = static_cast<int>(j % STAGES);
     mbar_wait(&full[s], (j / STAGES) & 1u);
-    double* xr = buf + (2 * s) * stage_elems;
-    double* xi = xr + stage_elems;
+    Real* xr = buf + (2 * s) * stage_elems;
+    Real* xi = xr + stage_elems;
 
     double t1[S::NR][2], t2[S::NR][2], t3[S::NR][2];
 #pragma unroll
@@ -236,8 +251,8 @@ __global__ void __launch_bounds__(DmmaShape<KS>::kThreads + 32, 2) k_stream_dmma
       }
 #pragma unroll
       for (int nb = 0; nb < S::NR; ++nb) {
-        const double br = xr[lbb[nb] + offb[k]];
-        const double bi = xi[lbb[nb] + offb[k]];
+        const double br = static_cast<double>(xr[lbb[nb] + offb[k]]);
+        const double bi = static_cast<double>(xi[lbb[nb] + offb[k]]);
         if (use_r) dmma(t1[nb], fr, br);
         if (use_i) dmma(t2[nb], fi, bi);
         if (use_s) dmma(t3[nb], fs, br + bi);
@@ -250,8 +265,8 @@ __global__ void __launch_bounds__(DmmaShape<KS>::kThreads + 32, 2) k_stream_dmma
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const uint32_t a = lbc[nb][i] + offc;
-        xr[a] = t1[nb][i] - t2[nb][i];
-        xi[a] = t3[nb][i] - t1[nb][i] - t2[nb][i];
+        xr[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
+        xi[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
       }
     fence_async_smem();  // generic-proxy writes -> async-proxy bulk store
     __syncwarp();

@@ -275,19 +275,17 @@ tsg::GateLaunch make_launch(const KernelPlan& p, const LaunchStructure& ls) {
   return g;
 }
 
-// the tile kernels stage the sub-matrix from global memory: [D*D re][D*D im]
-// Device copy of the snapped sub-matrix: [Mr | Mi | Mr + Mi], D x D each,
-// row-major, in the state precision (k_tile reads the first two blocks,
-// k_stream_dmma all three).
-std::vector<unsigned char> tile_matrix_bytes(const LaunchStructure& ls, int prec) {
+// Device copy of the snapped sub-matrix for the shared-memory / DMMA kernels:
+// [Mr | Mi | Mr + Mi], D x D each, row-major, FP64 for both state precisions
+// (k_tile reads the first two blocks, k_stream_dmma / k_dmma_direct all three).
+std::vector<unsigned char> tile_matrix_bytes(const LaunchStructure& ls, int /*prec*/) {
   const size_t dd = ls.sub_re.size();
-  std::vector<unsigned char> out(3 * dd * (prec == 64 ? 8 : 4));
+  std::vector<unsigned char> out(3 * dd * sizeof(double));
+  double* d = reinterpret_cast<double*>(out.data());
   for (size_t i = 0; i < dd; ++i) {
-    const double v[3] = {ls.sub_re[i], ls.sub_im[i], ls.sub_re[i] + ls.sub_im[i]};
-    for (int b = 0; b < 3; ++b) {
-      if (prec == 64) reinterpret_cast<double*>(out.data())[b * dd + i] = v[b];
-      else reinterpret_cast<float*>(out.data())[b * dd + i] = static_cast<float>(v[b]);
-    }
+    d[i] = ls.sub_re[i];
+    d[dd + i] = ls.sub_im[i];
+    d[2 * dd + i] = ls.sub_re[i] + ls.sub_im[i];
   }
   return out;
 }
@@ -295,7 +293,7 @@ std::vector<unsigned char> tile_matrix_bytes(const LaunchStructure& ls, int prec
 bool needs_tile_matrix(const tsg::GateLaunch& g, int prec) {
   const int dm = prec == 64 ? 4 : 5;
   if (g.klass == 3) return true;
-  if (g.klass == 2 && (g.ks > dm || (prec == 64 && g.ks >= 3))) return true;  // k_tile / k_stream_dmma
+  if (g.klass == 2 && g.ks >= 3) return true;  // k_stream_dmma / k_dmma_direct / k_tile
   if (g.klass == 1 && g.ks > dm) return true;  // sub-range diagonal falls back to tile
   return false;
 }
