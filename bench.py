@@ -171,9 +171,10 @@ def breakdown(ts, progs, sv, n):
         secs, _ = prog.run_profiled(sv)
         for i, s in enumerate(secs):
             info = prog.gate_info(i)
-            if info["kernel"] == "identity":
-                continue
-            g = groups.setdefault(kernel_key(info), {"seconds": 0.0, "launches": 0, "bytes": 0, "touched": 0})
+            if info["kernel"] == "identity" or info["batched"] == 2:
+                continue  # batch members are applied by the batch launch of an earlier gate
+            key = "k_diag_batch" if info["batched"] == 1 else kernel_key(info)
+            g = groups.setdefault(key, {"seconds": 0.0, "launches": 0, "bytes": 0, "touched": 0})
             g["seconds"] += float(s)
             g["launches"] += 1
             g["bytes"] += 2 * (1 << n) * amp

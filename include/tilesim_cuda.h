@@ -97,6 +97,9 @@ typedef struct tsg_plan_info {
   uint64_t entry_ops;  /* entries with a non-Zero scalar */
   uint64_t loop_count; /* 2^(n-k): groups of the s = 0 loop counter */
   double touched_fraction; /* share of the state the kernel reads+writes */
+  int batched;         /* programs only: 0 own launch, 1 first gate of a diagonal
+                          batch (one streaming pass for the run), 2 applied by
+                          the batch of an earlier gate */
 } tsg_plan_info;
 int tsg_plan_info_get(const tsg_plan* p, tsg_plan_info* out);
 

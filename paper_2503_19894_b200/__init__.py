@@ -66,7 +66,7 @@ def _check(rc: int) -> None:
 class PlanInfo(C.Structure):
     _fields_ = [("k", C.c_int), ("kernel_class", C.c_int), ("sub_k", C.c_int), ("n_controls", C.c_int),
                 ("sparse", C.c_int), ("op_count", _u64), ("entry_ops", _u64), ("loop_count", _u64),
-                ("touched_fraction", C.c_double)]
+                ("touched_fraction", C.c_double), ("batched", C.c_int)]
 
 
 class RunReport(C.Structure):

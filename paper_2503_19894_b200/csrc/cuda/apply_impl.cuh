@@ -475,6 +475,19 @@ bool launch_stream_if(const GateLaunch& g, cudaStream_t s, int num_sms) {
   }
 }
 
+// ---------------------------------------------------------- diag batches
+template <typename Real>
+int launch_diag_batch_impl(const DiagBatchLaunch& b, cudaStream_t s, int num_sms) {
+  if (b.n_gates == 0) return 0;
+  constexpr int V = PrecisionTraits<Real>::kMaxV;  // 16-byte vectors
+  const uint64_t n_work = (uint64_t{1} << b.n) / V;
+  if (n_work == 0 || (uint64_t{1} << b.n) % V != 0) throw std::runtime_error("diagonal batch needs >= 4 amplitudes");
+  if (b.n <= 32) k_diag_batch<Real, V, uint32_t><<<grid_for(n_work, num_sms), 256, 0, s>>>(b, n_work);
+  else k_diag_batch<Real, V, uint64_t><<<grid_for(n_work, num_sms), 256, 0, s>>>(b, n_work);
+  cuda_check(cudaGetLastError(), "k_diag_batch launch");
+  return 1;
+}
+
 // ------------------------------------------------------------------ entry
 template <typename Real>
 int launch_gate_impl(const GateLaunch& g, cudaStream_t s, int num_sms) {

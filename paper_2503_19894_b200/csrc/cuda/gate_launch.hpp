@@ -39,6 +39,27 @@ struct GateLaunch {
 int launch_gate_f64(const GateLaunch& g, cudaStream_t stream, int num_sms);
 int launch_gate_f32(const GateLaunch& g, cudaStream_t stream, int num_sms);
 
+// A run of consecutive full-range diagonal gates applied in ONE streaming
+// pass.  Per element the gates are applied in program order with exactly the
+// arithmetic of k_diag, so the result is bit-identical to separate launches.
+constexpr int kMaxBatch = 16;
+constexpr int kMaxBatchEntries = 1024;  // sum of 2^ks over the batch
+struct DiagBatchLaunch {
+  int n = 0;  // qubits
+  void* re = nullptr;
+  void* im = nullptr;
+  int n_gates = 0;
+  uint64_t cmask[kMaxBatch] = {};  // control qubits of gate g
+  uint64_t cval[kMaxBatch] = {};   // their active values
+  int ks[kMaxBatch] = {};
+  int tq[kMaxBatch][6] = {};       // sub-target qubits
+  int toff[kMaxBatch] = {};        // table offset of gate g
+  int n_entries = 0;
+  const double* tables = nullptr;  // device: interleaved (re, im) diagonal entries, FP64
+};
+int launch_diag_batch_f64(const DiagBatchLaunch& b, cudaStream_t stream, int num_sms);
+int launch_diag_batch_f32(const DiagBatchLaunch& b, cudaStream_t stream, int num_sms);
+
 // Name of the kernel template a launch selects (for reports / profiles).
 const char* kernel_name(const GateLaunch& g, int precision_bits);
 

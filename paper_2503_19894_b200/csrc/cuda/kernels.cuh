@@ -232,6 +232,70 @@ __global__ void __launch_bounds__(256) k_diag(const __grid_constant__ DiagParams
   }
 }
 
+// ------------------------------------------------------- diagonal batches
+// One streaming pass applies a run of diagonal gates (DiagBatchLaunch).
+template <typename Real>
+struct Cplx2;
+template <>
+struct Cplx2<double> {
+  using T = double2;
+};
+template <>
+struct Cplx2<float> {
+  using T = float2;
+};
+
+// Index arithmetic in 32 bits when the state has at most 2^32 amplitudes.
+// A gate whose controls and targets avoid the V low bits has the same factor
+// for all V amplitudes of a thread: it is resolved once per thread.
+template <typename Real, int V, typename Idx>
+__global__ void __launch_bounds__(256) k_diag_batch(const __grid_constant__ DiagBatchLaunch b, uint64_t n_work) {
+  using C2 = typename Cplx2<Real>::T;
+  __shared__ C2 tab[kMaxBatchEntries];
+  for (int i = threadIdx.x; i < b.n_entries; i += blockDim.x)
+    tab[i] = C2{static_cast<Real>(b.tables[2 * i]), static_cast<Real>(b.tables[2 * i + 1])};
+  __syncthreads();
+  Real* re = static_cast<Real*>(b.re);
+  Real* im = static_cast<Real*>(b.im);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < n_work; w += stride) {
+    const Idx idx0 = static_cast<Idx>(w * V);
+    Real xr[V], xi[V];
+    load_v<Real, V>(re + idx0, xr);
+    load_v<Real, V>(im + idx0, xi);
+    for (int g = 0; g < b.n_gates; ++g) {
+      const Idx cm = static_cast<Idx>(b.cmask[g]), cv = static_cast<Idx>(b.cval[g]);
+      const int ks = b.ks[g], off = b.toff[g];
+      Idx tmask = 0;
+      for (int t = 0; t < ks; ++t) tmask |= Idx{1} << b.tq[g][t];
+      auto index_of = [&](Idx idx) {
+        unsigned j = 0;
+        for (int t = 0; t < ks; ++t) j |= static_cast<unsigned>(idx >> (b.tq[g][t] - t)) & (1u << t);
+        return j;
+      };
+      auto apply = [&](int v, const C2 d) {
+        const Real r0 = xr[v], i0 = xi[v];
+        xr[v] = fma(d.x, r0, -d.y * i0);  // exactly k_diag's update
+        xi[v] = fma(d.x, i0, d.y * r0);
+      };
+      if (((cm | tmask) & Idx{V - 1}) == 0) {  // same factor for the whole vector
+        if ((idx0 & cm) != cv) continue;
+        const C2 d = tab[off + index_of(idx0)];
+#pragma unroll
+        for (int v = 0; v < V; ++v) apply(v, d);
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const Idx idx = idx0 + v;
+          if ((idx & cm) == cv) apply(v, tab[off + index_of(idx)]);
+        }
+      }
+    }
+    store_v<Real, V>(re + idx0, xr);
+    store_v<Real, V>(im + idx0, xi);
+  }
+}
+
 // ------------------------------------------------------------------- tile
 template <typename Real>
 struct TileParams {

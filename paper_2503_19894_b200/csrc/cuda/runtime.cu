@@ -197,6 +197,13 @@ struct ProgramGate {
   tsg::GateLaunch launch;  // re/im filled per run
   size_t mat_offset = 0;   // into the device arena (tile class)
   bool has_mat = false;
+  int batch = -1;          // >= 0: first gate of diagonal batch `batch`
+  bool in_batch = false;   // applied by an earlier gate's batch launch
+};
+
+struct ProgramBatch {
+  tsg::DiagBatchLaunch launch;  // re/im/tables filled per run
+  size_t table_offset = 0;      // into the device arena
 };
 
 }  // namespace
@@ -206,6 +213,7 @@ struct tsg_program {
   int n = 0;
   int prec = 64;
   std::vector<ProgramGate> gates;
+  std::vector<ProgramBatch> batches;
   void* arena = nullptr;
   double planning_s = 0.0;
   uint64_t launches = 0, bytes = 0, touched_bytes = 0, total_ops = 0;
@@ -318,18 +326,85 @@ void fill_info(const KernelPlan& p, const LaunchStructure& ls, tsg_plan_info* ou
   out->entry_ops = p.entry_ops.size();
   out->loop_count = uint64_t{1} << (p.n - p.gate.k());
   out->touched_fraction = touched_fraction(ls);
+  out->batched = 0;
 }
 
 void run_program(tsg_state* st, tsg_program* prog, std::vector<cudaEvent_t>* marks) {
   for (size_t i = 0; i < prog->gates.size(); ++i) {
-    tsg::GateLaunch g = prog->gates[i].launch;
+    const ProgramGate& pg = prog->gates[i];
+    if (marks) ck(cudaEventRecord((*marks)[i], st->stream), "event");
+    if (pg.in_batch) continue;
+    if (pg.batch >= 0) {
+      tsg::DiagBatchLaunch b = prog->batches[pg.batch].launch;
+      b.re = st->re;
+      b.im = st->im;
+      b.tables = reinterpret_cast<const double*>(static_cast<unsigned char*>(prog->arena) +
+                                                 prog->batches[pg.batch].table_offset);
+      st->prec == 64 ? tsg::launch_diag_batch_f64(b, st->stream, st->ctx->num_sms)
+                     : tsg::launch_diag_batch_f32(b, st->stream, st->ctx->num_sms);
+      continue;
+    }
+    tsg::GateLaunch g = pg.launch;
     g.re = st->re;
     g.im = st->im;
-    if (prog->gates[i].has_mat) g.dev_mat = static_cast<unsigned char*>(prog->arena) + prog->gates[i].mat_offset;
-    if (marks) ck(cudaEventRecord((*marks)[i], st->stream), "event");
+    if (pg.has_mat) g.dev_mat = static_cast<unsigned char*>(prog->arena) + pg.mat_offset;
     launch(st, g);
   }
   if (marks) ck(cudaEventRecord(marks->back(), st->stream), "event");
+}
+
+// Group runs of consecutive diagonal gates into one streaming launch when
+// that moves fewer bytes than launching them separately (a separate launch
+// touches only its active slice: touched_fraction = 2^-controls).
+void plan_diagonal_batches(tsg_program* prog, std::vector<unsigned char>& arena) {
+  if (prog->n < 2) return;
+  auto batchable = [&](const ProgramGate& g) {
+    return g.ls.klass == KernelClass::Diagonal && g.ls.ks <= 6 && !g.has_mat;
+  };
+  size_t i = 0;
+  while (i < prog->gates.size()) {
+    if (!batchable(prog->gates[i])) {
+      ++i;
+      continue;
+    }
+    size_t j = i;
+    int entries = 0;
+    double touched = 0.0;
+    while (j < prog->gates.size() && batchable(prog->gates[j]) && j - i < static_cast<size_t>(tsg::kMaxBatch) &&
+           entries + (1 << prog->gates[j].ls.ks) <= tsg::kMaxBatchEntries) {
+      entries += 1 << prog->gates[j].ls.ks;
+      touched += touched_fraction(prog->gates[j].ls);
+      ++j;
+    }
+    if (j - i >= 2 && touched > 1.0) {
+      ProgramBatch pb;
+      tsg::DiagBatchLaunch& b = pb.launch;
+      b.n = prog->n;
+      std::vector<double> tab;
+      for (size_t q = i; q < j; ++q) {
+        const LaunchStructure& ls = prog->gates[q].ls;
+        const int g = b.n_gates++;
+        for (int c : ls.controls) b.cmask[g] |= uint64_t{1} << c;
+        b.cval[g] = ls.control_values;
+        b.ks[g] = ls.ks;
+        for (int t = 0; t < ls.ks; ++t) b.tq[g][t] = ls.sub_targets[t];
+        b.toff[g] = static_cast<int>(tab.size() / 2);
+        const int d = 1 << ls.ks;
+        for (int e = 0; e < d; ++e) {
+          tab.push_back(ls.sub_re[e * d + e]);
+          tab.push_back(ls.sub_im[e * d + e]);
+        }
+        prog->gates[q].in_batch = q != i;
+      }
+      b.n_entries = static_cast<int>(tab.size() / 2);
+      pb.table_offset = (arena.size() + 255) & ~size_t{255};
+      arena.resize(pb.table_offset + tab.size() * sizeof(double));
+      std::memcpy(arena.data() + pb.table_offset, tab.data(), tab.size() * sizeof(double));
+      prog->gates[i].batch = static_cast<int>(prog->batches.size());
+      prog->batches.push_back(pb);
+    }
+    i = j;
+  }
 }
 
 }  // namespace
@@ -732,12 +807,15 @@ int tsg_program_create(tsg_ctx* ctx, const tsc_circuit* fused, double zero_tol, 
         pg.has_mat = true;
       }
       prog->total_ops += pg.plan.profile.op_count;
-      if (pg.ls.klass != KernelClass::Identity) {
-        ++prog->launches;
-        prog->bytes += 2 * (uint64_t{1} << prog->n) * amp;
-        prog->touched_bytes += static_cast<uint64_t>(2.0 * std::ldexp(1.0, prog->n) * amp * touched_fraction(pg.ls));
-      }
       prog->gates.push_back(std::move(pg));
+    }
+    if (!std::getenv("TSG_NO_DIAG_BATCH")) plan_diagonal_batches(prog.get(), arena);
+    for (const ProgramGate& pg : prog->gates) {  // one launch per batch or per non-identity gate
+      if (pg.in_batch || pg.ls.klass == KernelClass::Identity) continue;
+      ++prog->launches;
+      prog->bytes += 2 * (uint64_t{1} << prog->n) * amp;
+      const double frac = pg.batch >= 0 ? 1.0 : touched_fraction(pg.ls);
+      prog->touched_bytes += static_cast<uint64_t>(2.0 * std::ldexp(1.0, prog->n) * amp * frac);
     }
     if (!arena.empty()) {
       ck(cudaMalloc(&prog->arena, arena.size()), "cudaMalloc program arena");
@@ -856,12 +934,99 @@ int tsg_program_gate_info(const tsg_program* prog, uint64_t i, tsg_plan_info* ou
     require(prog && out, "null argument");
     require(i < prog->gates.size(), "gate index out of range");
     fill_info(prog->gates[i].plan, prog->gates[i].ls, out);
+    out->batched = prog->gates[i].in_batch ? 2 : (prog->gates[i].batch >= 0 ? 1 : 0);
+    if (out->batched == 1) out->touched_fraction = 1.0;
+    if (out->batched == 2) out->touched_fraction = 0.0;
   })
 }
 
-int tsg_bench_cost_model(tsg_ctx*, int, int, int, int, uint64_t, tsc_cost_model**) {
-  tsg_detail::set_error("tsg_bench_cost_model: not built yet");
-  return TSG_ERR_SIM;
+// bench_cost_model on the device.  For k in [1, k_max] and
+// density levels {diagonal, quarter, half, dense} (the diagonal level is a
+// B200 addition: diagonal gates run on the streaming kernel and are the
+// cheapest class), a seeded random gate on two random target sets is planned
+// exactly as run_circuit plans it and timed with CUDA events on a 2^bench_n
+// scratch state; spg = median seconds / 2^(n-k).  `threads` is recorded as 1
+// (one device); the host string names the device and clocks.
+int tsg_bench_cost_model(tsg_ctx* ctx, int bench_n, int k_max, int precision_bits, int repetitions, uint64_t seed,
+                         tsc_cost_model** out) {
+  TSG_TRY({
+    require(ctx && out, "null argument");
+    require(bench_n >= 8 && bench_n <= 34, "bench_n must be in [8, 34]");
+    require(k_max >= 1 && k_max <= 6 && k_max < bench_n, "k_max must be in [1, 6]");
+    require(repetitions >= 1, "repetitions must be >= 1");
+    tsg_state* st = nullptr;
+    if (int rc = tsg_state_create(ctx, bench_n, precision_bits, &st)) throw SimError(tsg_last_error());
+    std::unique_ptr<tsg_state, int (*)(tsg_state*)> guard(st, tsg_state_destroy);
+    if (int rc = tsg_state_init_random(st, seed)) throw SimError(tsg_last_error());
+    CostModel cm;
+    cm.bench_n = bench_n;
+    cm.precision = precision_bits == 64 ? "f64" : "f32";
+    cm.host = ctx->name + " sm_100a, " + std::to_string(ctx->num_sms) + " SMs, CUDA-event timed";
+    Prng rng(seed);
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    void* dev_mat = nullptr;
+    ck(cudaMalloc(&dev_mat, 3 * 4096 * sizeof(double)), "cudaMalloc bench matrix");
+    for (int k = 1; k <= k_max; ++k) {
+      for (int level = 0; level < 4; ++level) {  // 0 diag, 1 quarter, 2 half, 3 dense
+        std::vector<double> times;
+        uint64_t ops = 0;
+        for (int trial = 0; trial < 2; ++trial) {
+          std::vector<int> pool(bench_n);
+          for (int i = 0; i < bench_n; ++i) pool[i] = i;
+          for (int i = bench_n - 1; i > 0; --i) std::swap(pool[i], pool[rng.next_below(i + 1)]);
+          std::vector<int> targets(pool.begin(), pool.begin() + k);
+          std::sort(targets.begin(), targets.end());
+          GateMatrix m = random_unitary(k, rng);
+          const uint64_t D = m.dim();
+          if (level == 0) {
+            for (uint64_t r = 0; r < D; ++r)
+              for (uint64_t c = 0; c < D; ++c)
+                if (r != c) m.at(r, c) = 0.0;
+          } else if (level < 3) {
+            const double keep = level == 1 ? 0.25 : 0.5;
+            for (uint64_t r = 0; r < D; ++r)
+              for (uint64_t c = 0; c < D; ++c)
+                if (r != c && rng.uniform() >= keep) m.at(r, c) = 0.0;
+          }
+          KernelPlan plan = plan_kernel(make_gate(m, targets), bench_n, 0, 1e-8, 1e-8, false);
+          const LaunchStructure ls = derive_launch(plan, nullptr, precision_bits);
+          tsg::GateLaunch g = make_launch(plan, ls);
+          g.re = st->re;
+          g.im = st->im;
+          if (needs_tile_matrix(g, precision_bits)) {
+            const auto bytes = tile_matrix_bytes(ls, precision_bits);
+            ck(cudaMemcpy(dev_mat, bytes.data(), bytes.size(), cudaMemcpyHostToDevice), "bench matrix upload");
+            g.dev_mat = dev_mat;
+          }
+          ops = std::max(ops, plan.profile.op_count);
+          launch(st, g);  // warm-up (first-use kernel attributes)
+          for (int r = 0; r < repetitions; ++r) {
+            ck(cudaEventRecord(e0, st->stream), "event");
+            launch(st, g);
+            ck(cudaEventRecord(e1, st->stream), "event");
+            ck(cudaEventSynchronize(e1), "event sync");
+            float ms = 0.f;
+            ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+            times.push_back(ms * 1e-3);
+          }
+        }
+        std::sort(times.begin(), times.end());
+        const double med = times[times.size() / 2];
+        CostRecord rec;
+        rec.k = k;
+        rec.op_count = ops;
+        rec.threads = 1;
+        rec.seconds_per_group = std::max(med, 1e-9) / std::ldexp(1.0, bench_n - k);
+        cm.records.push_back(rec);
+      }
+    }
+    cudaFree(dev_mat);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *out = new tsc_cost_model{std::move(cm)};
+  })
 }
 
 }  // extern "C"
