@@ -131,6 +131,8 @@ typedef struct tsg_run_report {
   uint64_t bytes;      /* algorithmic bytes per run: sum of 2*2^n*B_amp over launched gates */
   uint64_t touched_bytes; /* bytes the kernels actually read+write (controls skip slices) */
   uint64_t total_op_count;
+  uint64_t exchanged_bytes; /* sharded runs: bytes this rank sent to peers */
+  double exchange_s;        /* sharded runs: device seconds spent in exchanges */
 } tsg_run_report;
 
 int tsg_program_create(tsg_ctx* ctx, const tsc_circuit* fused, double zero_tol, double one_tol, int precision_bits,
@@ -189,6 +191,46 @@ int tsc_cost_model_parse(const char* text, tsc_cost_model** out);
 int tsc_cost_model_destroy(tsc_cost_model* cm);
 int tsc_cost_model_serialize(const tsc_cost_model* cm, char* buf, size_t cap, size_t* needed);
 int tsc_estimate_cost(const tsc_cost_model* cm, int k, uint64_t op_count, int threads, int n, double* seconds);
+
+/* ----------------------------------------------- sharding (host planner) ---
+ * include/tilesim/shard.hpp: 2^n_global ranks, physical bits >= n - n_global
+ * select the rank.  Op kinds: 0 local gate, 1 rank-selected sub-block
+ * (no communication), 2 swaps of (global position, local position) pairs. */
+typedef struct tsc_shard_plan tsc_shard_plan;
+int tsc_shard_plan_create(const tsc_circuit* fused, int n_global, double zero_tol, double one_tol,
+                          tsc_shard_plan** out);
+int tsc_shard_plan_destroy(tsc_shard_plan* p);
+int tsc_shard_plan_info(const tsc_shard_plan* p, int* n_qubits, int* n_global, uint64_t* n_ops, uint64_t* swaps,
+                        uint64_t* rank_blocks);
+/* op i: kind, gate (k, sorted physical targets, matrix 2*4^k; k = 0 for swaps),
+ * swap pairs (2 ints each, *n_swaps of them), index of the source gate */
+int tsc_shard_plan_op(const tsc_shard_plan* p, uint64_t i, int* kind, int* k, int* targets, double* matrix,
+                      int* n_swaps, int* swap_pairs, int* source_gate);
+/* local sub-gate of a rank-block op for `rank` (k may be 0: a scalar) */
+int tsc_shard_rank_subgate(const tsc_shard_plan* p, uint64_t i, uint64_t rank, int* k, int* targets, double* matrix);
+/* logical qubit -> physical position after the last op (n ints) */
+int tsc_shard_final_pos(const tsc_shard_plan* p, int* pos);
+
+/* --------------------------------------------- sharded execution (device) ---
+ * Virtual shards: 2^n_global shard buffers on ONE device, swaps as device
+ * copies -- the single-GPU emulation of the distributed path.  Host arrays
+ * are the full state in logical order (fp64 SoA, 2^n entries). */
+int tsg_vshard_run(tsg_ctx* ctx, const tsc_shard_plan* plan, int precision_bits, const double* re_in,
+                   const double* im_in, double* re_out, double* im_out, tsg_run_report* report);
+
+/* One process per GPU over NCCL (dlopen'ed libnccl.so.2).  Rank 0 creates
+ * the id, every rank passes the same 128 bytes (e.g. broadcast over
+ * torch.distributed), world = 2^n_global. */
+typedef struct tsg_dist tsg_dist;
+int tsg_dist_unique_id(unsigned char id[128]);
+int tsg_dist_create(tsg_ctx* ctx, int n_qubits, int precision_bits, int n_global, int rank, const unsigned char id[128],
+                    tsg_dist** out);
+int tsg_dist_destroy(tsg_dist* d);
+int tsg_dist_init_basis(tsg_dist* d, uint64_t logical_index);  /* identity qubit map */
+int tsg_dist_run(tsg_dist* d, const tsc_shard_plan* plan, tsg_run_report* report);
+/* this rank's 2^(n-n_global) amplitudes (physical order of the last plan) */
+int tsg_dist_download_local(tsg_dist* d, double* re, double* im);
+int tsg_dist_local_sumsq(tsg_dist* d, double* out);
 
 /* bench_cost_model on the GPU: for k in [1, k_max] and
  * densities {dense, half, quarter}, times the real kernel on a 2^bench_n

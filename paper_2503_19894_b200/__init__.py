@@ -71,7 +71,8 @@ class PlanInfo(C.Structure):
 
 class RunReport(C.Structure):
     _fields_ = [("planning_s", C.c_double), ("execution_s", C.c_double), ("gates", _u64), ("launches", _u64),
-                ("bytes", _u64), ("touched_bytes", _u64), ("total_op_count", _u64)]
+                ("bytes", _u64), ("touched_bytes", _u64), ("total_op_count", _u64), ("exchanged_bytes", _u64),
+                ("exchange_s", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -563,3 +564,141 @@ def bench_cost_model(bench_n: int = 28, k_max: int = 6, precision: str = "f64", 
     _check(_lib.tsg_bench_cost_model(ctx._h, bench_n, k_max, 64 if precision in ("f64", "c128") else 32,
                                      repetitions, seed, C.byref(h)))
     return CostModel(_handle=h.value)
+
+
+# ============================================================== sharding ===
+_sig("tsc_shard_plan_create", [_vp, C.c_int, C.c_double, C.c_double, C.POINTER(_vp)])
+_sig("tsc_shard_plan_destroy", [_vp])
+_sig("tsc_shard_plan_info", [_vp, _ip, _ip, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)])
+_sig("tsc_shard_plan_op", [_vp, _u64, _ip, _ip, _ip, _dp, _ip, _ip, _ip])
+_sig("tsc_shard_rank_subgate", [_vp, _u64, _u64, _ip, _ip, _dp])
+_sig("tsc_shard_final_pos", [_vp, _ip])
+_sig("tsg_vshard_run", [_vp, _vp, C.c_int, _dp, _dp, _dp, _dp, C.POINTER(RunReport)])
+_sig("tsg_dist_unique_id", [C.POINTER(C.c_ubyte)])
+_sig("tsg_dist_create", [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_ubyte), C.POINTER(_vp)])
+_sig("tsg_dist_destroy", [_vp])
+_sig("tsg_dist_init_basis", [_vp, _u64])
+_sig("tsg_dist_run", [_vp, _vp, C.POINTER(RunReport)])
+_sig("tsg_dist_download_local", [_vp, _dp, _dp])
+_sig("tsg_dist_local_sumsq", [_vp, _dp])
+
+SHARD_KINDS = ("local", "rank_block", "swap")
+
+
+class ShardPlan:
+    """Global-qubit sharding of a fused circuit over 2^n_global ranks (tilesim/shard.hpp)."""
+
+    def __init__(self, fused: Circuit, n_global: int, zero_tol=1e-8, one_tol=1e-8):
+        h = _vp()
+        _check(_lib.tsc_shard_plan_create(fused._h, n_global, zero_tol, one_tol, C.byref(h)))
+        self._h = h.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tsc_shard_plan_destroy(self._h)
+            self._h = None
+
+    def info(self) -> dict:
+        n, g = C.c_int(), C.c_int()
+        ops, sw, rb = _u64(), _u64(), _u64()
+        _check(_lib.tsc_shard_plan_info(self._h, C.byref(n), C.byref(g), C.byref(ops), C.byref(sw), C.byref(rb)))
+        return {"n": n.value, "n_global": g.value, "n_local": n.value - g.value, "ops": ops.value,
+                "swaps": sw.value, "rank_blocks": rb.value}
+
+    def op(self, i: int) -> dict:
+        kind, k, ns, src = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        t = (C.c_int * 12)()
+        m = np.zeros(2 * 4 ** 6)
+        sp = (C.c_int * 64)()
+        _check(_lib.tsc_shard_plan_op(self._h, i, C.byref(kind), C.byref(k), t, m.ctypes.data_as(_dp), C.byref(ns),
+                                      sp, C.byref(src)))
+        gate = None
+        if kind.value != 2:
+            d = 1 << k.value
+            gate = Gate(list(t)[: k.value], m[: 2 * d * d].view(np.complex128).reshape(d, d).copy())
+        return {"kind": SHARD_KINDS[kind.value], "gate": gate, "source_gate": src.value,
+                "swaps": [(sp[2 * s], sp[2 * s + 1]) for s in range(ns.value)]}
+
+    def ops(self):
+        return [self.op(i) for i in range(self.info()["ops"])]
+
+    def rank_subgate(self, i: int, rank: int) -> Gate:
+        k = C.c_int()
+        t = (C.c_int * 12)()
+        m = np.zeros(2 * 4 ** 6)
+        _check(_lib.tsc_shard_rank_subgate(self._h, i, rank, C.byref(k), t, m.ctypes.data_as(_dp)))
+        d = 1 << k.value
+        return Gate(list(t)[: k.value], m[: 2 * d * d].view(np.complex128).reshape(d, d).copy())
+
+    def final_pos(self):
+        info = self.info()
+        pos = (C.c_int * info["n"])()
+        _check(_lib.tsc_shard_final_pos(self._h, pos))
+        return list(pos)
+
+
+def physical_permutation(final_pos, n: int) -> np.ndarray:
+    """phys[x] = physical index of logical basis state x under final_pos."""
+    x = np.arange(1 << n, dtype=np.uint64)
+    phys = np.zeros(1 << n, dtype=np.uint64)
+    for q, p in enumerate(final_pos):
+        phys |= ((x >> np.uint64(q)) & np.uint64(1)) << np.uint64(p)
+    return phys
+
+
+def vshard_run(plan: ShardPlan, re: np.ndarray, im: np.ndarray, precision: str = "f64", ctx: Context | None = None):
+    """Run a shard plan on 2^n_global virtual shards of ONE device (single-GPU
+    emulation of the distributed path).  Inputs/outputs: full state, logical order."""
+    ctx = ctx or default_context()
+    re = np.ascontiguousarray(re, dtype=np.float64)
+    im = np.ascontiguousarray(im, dtype=np.float64)
+    ore, oim = np.empty_like(re), np.empty_like(im)
+    r = RunReport()
+    _check(_lib.tsg_vshard_run(ctx._h, plan._h, 64 if precision in ("f64", "c128") else 32, re.ctypes.data_as(_dp),
+                               im.ctypes.data_as(_dp), ore.ctypes.data_as(_dp), oim.ctypes.data_as(_dp), C.byref(r)))
+    return ore, oim, r.as_dict()
+
+
+class DistState:
+    """This rank's shard of a 2^n statevector over 2^n_global processes (NCCL)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(_lib.tsg_dist_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, n: int, n_global: int, rank: int, uid: bytes, precision: str = "f64",
+                 ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        buf = (C.c_ubyte * 128)(*uid)
+        h = _vp()
+        _check(_lib.tsg_dist_create(self.ctx._h, n, 64 if precision in ("f64", "c128") else 32, n_global, rank, buf,
+                                    C.byref(h)))
+        self._h = h.value
+        self.n, self.n_global, self.rank = n, n_global, rank
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tsg_dist_destroy(self._h)
+            self._h = None
+
+    def init_basis(self, x: int):
+        _check(_lib.tsg_dist_init_basis(self._h, x))
+        return self
+
+    def run(self, plan: ShardPlan) -> dict:
+        r = RunReport()
+        _check(_lib.tsg_dist_run(self._h, plan._h, C.byref(r)))
+        return r.as_dict()
+
+    def download_local(self):
+        m = 1 << (self.n - self.n_global)
+        re, im = np.empty(m), np.empty(m)
+        _check(_lib.tsg_dist_download_local(self._h, re.ctypes.data_as(_dp), im.ctypes.data_as(_dp)))
+        return re, im
+
+    def local_sumsq(self) -> float:
+        out = C.c_double()
+        _check(_lib.tsg_dist_local_sumsq(self._h, C.byref(out)))
+        return out.value

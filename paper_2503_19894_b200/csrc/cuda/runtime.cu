@@ -856,6 +856,8 @@ static void fill_report(const tsg_program* prog, double exec_s, tsg_run_report* 
   r->bytes = prog->bytes;
   r->touched_bytes = prog->touched_bytes;
   r->total_op_count = prog->total_ops;
+  r->exchanged_bytes = 0;
+  r->exchange_s = 0.0;
 }
 
 static cudaGraphExec_t program_graph(tsg_state* st, tsg_program* prog) {
@@ -1030,3 +1032,5 @@ int tsg_bench_cost_model(tsg_ctx* ctx, int bench_n, int k_max, int precision_bit
 }
 
 }  // extern "C"
+
+#include "shard_exec.cuh"

@@ -198,3 +198,83 @@ int tsc_estimate_cost(const tsc_cost_model* cm, int k, uint64_t op_count, int th
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- sharding
+extern "C" {
+
+int tsc_shard_plan_create(const tsc_circuit* fused, int n_global, double zero_tol, double one_tol,
+                          tsc_shard_plan** out) {
+  TSG_TRY({
+    require(fused && out, "null argument");
+    *out = new tsc_shard_plan{plan_sharded(fused->c, n_global, zero_tol, one_tol)};
+  })
+}
+
+int tsc_shard_plan_destroy(tsc_shard_plan* p) {
+  delete p;
+  return TSG_OK;
+}
+
+int tsc_shard_plan_info(const tsc_shard_plan* p, int* n_qubits, int* n_global, uint64_t* n_ops, uint64_t* swaps,
+                        uint64_t* rank_blocks) {
+  TSG_TRY({
+    require(p != nullptr, "null handle");
+    if (n_qubits) *n_qubits = p->plan.n;
+    if (n_global) *n_global = p->plan.n_global;
+    if (n_ops) *n_ops = p->plan.ops.size();
+    if (swaps) *swaps = p->plan.swap_count;
+    if (rank_blocks) *rank_blocks = p->plan.rank_block_count;
+  })
+}
+
+static void put_gate(const Gate& g, int* k, int* targets, double* matrix) {
+  if (k) *k = g.k();
+  if (targets)
+    for (int j = 0; j < g.k(); ++j) targets[j] = g.targets[j];
+  if (matrix)
+    for (size_t j = 0; j < g.matrix.entries().size(); ++j) {
+      matrix[2 * j] = g.matrix.entries()[j].real();
+      matrix[2 * j + 1] = g.matrix.entries()[j].imag();
+    }
+}
+
+int tsc_shard_plan_op(const tsc_shard_plan* p, uint64_t i, int* kind, int* k, int* targets, double* matrix,
+                      int* n_swaps, int* swap_pairs, int* source_gate) {
+  TSG_TRY({
+    require(p != nullptr, "null handle");
+    require(i < p->plan.ops.size(), "op index out of range");
+    const ShardOp& op = p->plan.ops[i];
+    if (kind) *kind = static_cast<int>(op.kind);
+    if (op.kind == ShardOp::Kind::Swap) {
+      if (k) *k = 0;
+    } else {
+      put_gate(op.gate, k, targets, matrix);
+    }
+    if (n_swaps) *n_swaps = static_cast<int>(op.swaps.size());
+    if (swap_pairs)
+      for (size_t s = 0; s < op.swaps.size(); ++s) {
+        swap_pairs[2 * s] = op.swaps[s].first;
+        swap_pairs[2 * s + 1] = op.swaps[s].second;
+      }
+    if (source_gate) *source_gate = op.source_gate;
+  })
+}
+
+int tsc_shard_rank_subgate(const tsc_shard_plan* p, uint64_t i, uint64_t rank, int* k, int* targets, double* matrix) {
+  TSG_TRY({
+    require(p != nullptr, "null handle");
+    require(i < p->plan.ops.size(), "op index out of range");
+    require(p->plan.ops[i].kind == ShardOp::Kind::RankBlock, "op is not a rank block");
+    require(rank < (uint64_t{1} << p->plan.n_global), "rank out of range");
+    put_gate(rank_subgate(p->plan.ops[i], p->plan.n_local, rank), k, targets, matrix);
+  })
+}
+
+int tsc_shard_final_pos(const tsc_shard_plan* p, int* pos) {
+  TSG_TRY({
+    require(p && pos, "null argument");
+    for (int q = 0; q < p->plan.n; ++q) pos[q] = p->plan.final_pos[q];
+  })
+}
+
+}  // extern "C"

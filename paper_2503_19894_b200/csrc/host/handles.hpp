@@ -7,10 +7,15 @@
 
 #include "tilesim/fusion.hpp"
 #include "tilesim/ir.hpp"
+#include "tilesim/shard.hpp"
 #include "tilesim_cuda.h"
 
 struct tsc_circuit {
   tilesim::Circuit c;
+};
+
+struct tsc_shard_plan {
+  tilesim::ShardPlan plan;
 };
 
 struct tsc_cost_model {
