@@ -154,13 +154,17 @@ def build_circuits(ts, n, kmax):
 
 
 def kernel_key(info):
-    k = info["kernel"]
-    if k == "direct":
-        return f"k_direct<ks={info['sub_k']},{'sparse' if info['sparse'] else 'dense'}>"
-    if k == "tile":
-        return f"k_tile<ks={info['sub_k']}>"
+    """Name of the kernel the dispatcher runs for a full-range gate
+    (csrc/cuda/apply_impl.cuh launch_gate_impl / launch_stream_if)."""
+    k, ks = info["kernel"], info["sub_k"]
     if k == "diagonal":
-        return f"k_diag<ks={info['sub_k']}>"
+        return f"k_diag<ks={ks}>"
+    if k in ("direct", "tile"):
+        if 3 <= ks <= 5:
+            return f"k_stream_dmma<ks={ks}>"
+        if ks <= 2:
+            return f"k_direct<ks={ks}>"
+        return f"k_tile<ks={ks}>"
     return "none"
 
 
