@@ -153,37 +153,24 @@ def build_circuits(ts, n, kmax):
     return (fq, sq), (fr, sr), time.perf_counter() - t0
 
 
-def kernel_key(info):
-    """Name of the kernel the dispatcher runs for a full-range gate
-    (csrc/cuda/apply_impl.cuh launch_gate_impl / launch_stream_if)."""
-    k, ks = info["kernel"], info["sub_k"]
-    if k == "diagonal":
-        return f"k_diag<ks={ks}>"
-    if k in ("direct", "tile"):
-        if 3 <= ks <= 5:
-            return f"k_stream_dmma<ks={ks}>"
-        if ks <= 2:
-            return f"k_direct<ks={ks}>"
-        return f"k_tile<ks={ks}>"
-    return "none"
-
-
 def breakdown(ts, progs, sv, n):
-    """Per-kernel-class device time from events around every launch."""
+    """Per-kernel device time from CUDA events around every launch step
+    (Program.steps(): single gates, diagonal batches and tile passes)."""
     amp = 16
     groups = {}
     for prog in progs:
         secs, _ = prog.run_profiled(sv)
-        for i, s in enumerate(secs):
-            info = prog.gate_info(i)
-            if info["kernel"] == "identity" or info["batched"] == 2:
-                continue  # batch members are applied by the batch launch of an earlier gate
-            key = "k_diag_batch" if info["batched"] == 1 else kernel_key(info)
-            g = groups.setdefault(key, {"seconds": 0.0, "launches": 0, "bytes": 0, "touched": 0})
-            g["seconds"] += float(s)
+        for st in prog.steps():
+            s = float(secs[st["first_gate"]])  # a step's gates after its first one have zero-length marks
+            info = prog.gate_info(st["first_gate"])
+            key = st["kernel"]
+            g = groups.setdefault(key, {"seconds": 0.0, "launches": 0, "bytes": 0, "touched": 0, "gates": 0})
+            g["seconds"] += s
             g["launches"] += 1
+            g["gates"] += st["n_gates"]
             g["bytes"] += 2 * (1 << n) * amp
-            g["touched"] += int(2 * (1 << n) * amp * info["touched_fraction"])
+            frac = info["touched_fraction"] if st["kind"] == "gate" else 1.0
+            g["touched"] += int(2 * (1 << n) * amp * frac)
     return groups
 
 
@@ -365,7 +352,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": dom_name, "peak_source": peak_kind,
                      "per_launch_bytes": 2 * (1 << n) * 16},
-        "kernels": {k: {"seconds_per_step": v["seconds"], "launches": v["launches"],
+        "kernels": {k: {"seconds_per_step": v["seconds"], "launches": v["launches"], "gates": v["gates"],
                         "GBps_algorithmic": v["bytes"] / v["seconds"] / 1e9,
                         "GBps_touched": v["touched"] / v["seconds"] / 1e9} for k, v in groups.items()},
         "parity": {"qft30_analytic_maxdiff_64_samples": maxdiff, "qft30_norm": qft_norm},
@@ -375,7 +362,7 @@ def run_ours(args):
     }
     if args.breakdown and rank == 0:
         for k, v in sorted(groups.items(), key=lambda kv: -kv[1]["seconds"]):
-            print(f"{k:28s} {v['seconds']*1e3:9.2f} ms {v['launches']:4d} launches "
+            print(f"{k:28s} {v['seconds']*1e3:9.2f} ms {v['launches']:4d} launches {v['gates']:4d} gates "
                   f"{v['bytes']/v['seconds']/1e9:8.0f} GB/s alg {v['touched']/v['seconds']/1e9:8.0f} GB/s touched",
                   file=sys.stderr)
     if rank == 0:

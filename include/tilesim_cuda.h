@@ -97,9 +97,12 @@ typedef struct tsg_plan_info {
   uint64_t entry_ops;  /* entries with a non-Zero scalar */
   uint64_t loop_count; /* 2^(n-k): groups of the s = 0 loop counter */
   double touched_fraction; /* share of the state the kernel reads+writes */
-  int batched;         /* programs only: 0 own launch, 1 first gate of a diagonal
-                          batch (one streaming pass for the run), 2 applied by
-                          the batch of an earlier gate */
+  int batched;         /* programs only: 0 own launch, 1 first gate of a
+                          multi-gate step (diagonal batch or tile pass: one
+                          streaming pass for the run), 2 applied by the step of
+                          an earlier gate */
+  int controls[12];    /* the n_controls peeled control qubits, ascending */
+  int sub_targets[12]; /* the sub_k qubits the kernel mixes, ascending */
 } tsg_plan_info;
 int tsg_plan_info_get(const tsg_plan* p, tsg_plan_info* out);
 
@@ -145,6 +148,21 @@ int tsg_program_enqueue(tsg_state* st, tsg_program* prog, int use_graph);
 int tsg_program_run_profiled(tsg_state* st, tsg_program* prog, double* seconds, tsg_run_report* report);
 /* gate i of the program: kernel class, sub_k, controls, op_count */
 int tsg_program_gate_info(const tsg_program* prog, uint64_t i, tsg_plan_info* out);
+
+/* Launch steps of a program, in order.  A step applies n_gates consecutive
+ * (non-identity) gates of the program with ONE kernel: kind 0 a single gate,
+ * 1 a diagonal batch, 2 a tile pass (tilesim/pass.hpp: one HBM sweep for the
+ * run; high[] are its tile qubits above the contiguous runs). */
+typedef struct tsg_step_info {
+  int kind;
+  uint64_t first_gate;
+  uint64_t n_gates;
+  int n_high;
+  int high[16];
+  char kernel[48]; /* kernel template, e.g. "k_pass", "k_stream_dmma<ks=5>" */
+} tsg_step_info;
+int tsg_program_step_count(const tsg_program* prog, uint64_t* out);
+int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* out);
 
 /* --------------------------------------------------- circuit IR (host) ---
  * C exports of the kept C++ surface (include/tilesim/ir.hpp, fusion.hpp). */
@@ -196,6 +214,14 @@ int tsc_estimate_cost(const tsc_cost_model* cm, int k, uint64_t op_count, int th
  * include/tilesim/shard.hpp: 2^n_global ranks, physical bits >= n - n_global
  * select the rank.  Op kinds: 0 local gate, 1 rank-selected sub-block
  * (no communication), 2 swaps of (global position, local position) pairs. */
+/* Tile-pass grouping (tilesim/pass.hpp) of a fused circuit, as
+ * tsg_program_create would do it for precision_bits.  Host only.
+ * step_of_gate[n_gates]: step index of each gate (-1: identity, no launch);
+ * step_is_pass[n_gates] and step_high[16 * n_gates] (-1 padded) describe
+ * steps 0 .. *n_steps - 1 (there are never more steps than gates). */
+int tsc_plan_passes(const tsc_circuit* fused, int precision_bits, double zero_tol, double one_tol, int* step_of_gate,
+                    int* step_is_pass, int* step_high, uint64_t* n_steps);
+
 typedef struct tsc_shard_plan tsc_shard_plan;
 int tsc_shard_plan_create(const tsc_circuit* fused, int n_global, double zero_tol, double one_tol,
                           tsc_shard_plan** out);

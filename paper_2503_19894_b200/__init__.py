@@ -66,7 +66,16 @@ def _check(rc: int) -> None:
 class PlanInfo(C.Structure):
     _fields_ = [("k", C.c_int), ("kernel_class", C.c_int), ("sub_k", C.c_int), ("n_controls", C.c_int),
                 ("sparse", C.c_int), ("op_count", _u64), ("entry_ops", _u64), ("loop_count", _u64),
-                ("touched_fraction", C.c_double), ("batched", C.c_int)]
+                ("touched_fraction", C.c_double), ("batched", C.c_int), ("controls", C.c_int * 12),
+                ("sub_targets", C.c_int * 12)]
+
+
+def _plan_info_dict(pi) -> dict:
+    d = {f: getattr(pi, f) for f, _ in PlanInfo._fields_}
+    d["kernel"] = KERNEL_CLASSES[pi.kernel_class]
+    d["controls"] = list(pi.controls[:pi.n_controls])
+    d["sub_targets"] = list(pi.sub_targets[:pi.sub_k])
+    return d
 
 
 class RunReport(C.Structure):
@@ -76,6 +85,14 @@ class RunReport(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class StepInfo(C.Structure):
+    _fields_ = [("kind", C.c_int), ("first_gate", _u64), ("n_gates", _u64), ("n_high", C.c_int),
+                ("high", C.c_int * 16), ("kernel", C.c_char * 48)]
+
+
+STEP_KINDS = ("gate", "diag_batch", "pass")
 
 
 class _FusionConfigC(C.Structure):
@@ -127,6 +144,9 @@ _sig("tsg_program_run", [_vp, _vp, C.c_int, C.POINTER(RunReport)])
 _sig("tsg_program_enqueue", [_vp, _vp, C.c_int])
 _sig("tsg_program_run_profiled", [_vp, _vp, _dp, C.POINTER(RunReport)])
 _sig("tsg_program_gate_info", [_vp, _u64, C.POINTER(PlanInfo)])
+_sig("tsg_program_step_count", [_vp, C.POINTER(_u64)])
+_sig("tsg_program_step_info", [_vp, _u64, C.POINTER(StepInfo)])
+_sig("tsc_plan_passes", [_vp, C.c_int, C.c_double, C.c_double, _ip, _ip, _ip, C.POINTER(_u64)])
 _sig("tsg_bench_cost_model", [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _u64, C.POINTER(_vp)])
 _sig("tsc_circuit_create", [C.c_int, C.POINTER(_vp)])
 _sig("tsc_circuit_destroy", [_vp])
@@ -491,9 +511,7 @@ class KernelPlan:
     def info(self) -> dict:
         pi = PlanInfo()
         _check(_lib.tsg_plan_info_get(self._h, C.byref(pi)))
-        d = {f: getattr(pi, f) for f, _ in PlanInfo._fields_}
-        d["kernel"] = KERNEL_CLASSES[pi.kernel_class]
-        return d
+        return _plan_info_dict(pi)
 
 
 def plan_kernel(gate: Gate, n: int, s: int = 0, zero_tol=1e-8, one_tol=1e-8, runtime_matrix=False) -> KernelPlan:
@@ -542,12 +560,41 @@ class Program:
         _check(_lib.tsg_program_run_profiled(sv._h, self._h, secs.ctypes.data_as(_dp), C.byref(r)))
         return secs[: self.n_gates], r.as_dict()
 
+    def steps(self) -> list:
+        """Launch steps in order: {kind, first_gate, n_gates, high, kernel} (tsg_program_step_info)."""
+        cnt = _u64()
+        _check(_lib.tsg_program_step_count(self._h, C.byref(cnt)))
+        out = []
+        for i in range(cnt.value):
+            si = StepInfo()
+            _check(_lib.tsg_program_step_info(self._h, i, C.byref(si)))
+            out.append({"kind": STEP_KINDS[si.kind], "first_gate": si.first_gate, "n_gates": si.n_gates,
+                        "high": list(si.high[:si.n_high]), "kernel": si.kernel.decode()})
+        return out
+
     def gate_info(self, i: int) -> dict:
         pi = PlanInfo()
         _check(_lib.tsg_program_gate_info(self._h, i, C.byref(pi)))
-        d = {f: getattr(pi, f) for f, _ in PlanInfo._fields_}
-        d["kernel"] = KERNEL_CLASSES[pi.kernel_class]
-        return d
+        return _plan_info_dict(pi)
+
+
+def plan_passes(fused: Circuit, precision: str = "f64", zero_tol=1e-8, one_tol=1e-8) -> list:
+    """Host-only tile-pass grouping (tilesim/pass.hpp) exactly as Program builds it:
+    a list of steps {"gates": [...], "is_pass": bool, "high": [...]} in launch order."""
+    bits = {"f64": 64, "f32": 32, "c128": 64, "c64": 32}[precision]
+    g = max(1, len(fused))
+    sog = np.zeros(g, dtype=np.int32)
+    isp = np.zeros(g, dtype=np.int32)
+    high = np.zeros(16 * g, dtype=np.int32)
+    ns = _u64()
+    _check(_lib.tsc_plan_passes(fused._h, bits, zero_tol, one_tol, sog.ctypes.data_as(_ip), isp.ctypes.data_as(_ip),
+                                high.ctypes.data_as(_ip), C.byref(ns)))
+    steps = [{"gates": [], "is_pass": bool(isp[s]), "high": [int(h) for h in high[16 * s:16 * s + 16] if h >= 0]}
+             for s in range(ns.value)]
+    for gi in range(len(fused)):
+        if sog[gi] >= 0:
+            steps[sog[gi]]["gates"].append(gi)
+    return steps
 
 
 def run_circuit(c: Circuit, sv: Statevector, zero_tol=1e-8, one_tol=1e-8, use_graph=True) -> dict:

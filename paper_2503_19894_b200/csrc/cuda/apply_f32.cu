@@ -7,7 +7,7 @@ int launch_diag_batch_f32(const DiagBatchLaunch& b, cudaStream_t s, int num_sms)
   return launch_diag_batch_impl<float>(b, s, num_sms);
 }
 
-const char* kernel_name(const GateLaunch& g, int precision_bits) {
+std::string kernel_name(const GateLaunch& g, int precision_bits) {
   return precision_bits == 64 ? kernel_name_impl<double>(g) : kernel_name_impl<float>(g);
 }
 }  // namespace tsg

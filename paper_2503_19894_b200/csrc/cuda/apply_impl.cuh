@@ -165,20 +165,6 @@ void pick_tile(const GateLaunch& g, cudaStream_t s, int num_sms) {
 }
 
 // ----------------------------------------------------------------- stream
-// Insertion masks (SPEC.md:441-449 form) for zeros at sorted `pos` inside a
-// value of `width` bits: x -> sum_i (x & m[i]) << i.
-inline int insertion_masks(const int* pos, int count, int width, uint64_t* out) {
-  int from = 0;
-  for (int i = 0; i <= count; ++i) {
-    const int to = i < count ? pos[i] - i : width;
-    uint64_t m = 0;
-    for (int b = from; b < to && b < width; ++b) m |= uint64_t{1} << b;
-    out[i] = m;
-    from = to > from ? to : from;
-  }
-  return count + 1;
-}
-
 // Tile geometry of k_stream for a full-range launch; false if the state is
 // too small for one tile of the required shape.
 template <typename Real, int KS>
@@ -531,17 +517,22 @@ int launch_gate_impl(const GateLaunch& g, cudaStream_t s, int num_sms) {
   return 1;
 }
 
+// Name of the kernel template launch_gate_impl selects for a full-range
+// launch (reports / profiles), e.g. "k_stream_dmma<ks=5>".
 template <typename Real>
-const char* kernel_name_impl(const GateLaunch& g) {
+std::string kernel_name_impl(const GateLaunch& g) {
   constexpr int DM = PrecisionTraits<Real>::kDirectMax;
+  const std::string ks = "<ks=" + std::to_string(g.ks);
   int klass = g.klass;
+  if (klass == 0) return "none";
+  if (g.full_range && (klass == 2 || klass == 3) && g.ks >= 3 && g.ks <= 5 && g.dev_mat)
+    return (dmma_mode() == 1 && sizeof(Real) == 8 ? "k_dmma_direct" : "k_stream_dmma") + ks + ">";
   if (klass == 1 && !g.full_range) klass = g.ks <= DM ? 2 : 3;
   if (klass == 2 && g.ks > DM) klass = 3;
   switch (klass) {
-    case 0: return "none";
-    case 1: return "k_diag";
-    case 2: return g.sparse ? "k_direct<sparse>" : "k_direct<dense>";
-    default: return "k_tile";
+    case 1: return "k_diag" + ks + ">";
+    case 2: return "k_direct" + ks + (g.sparse ? ",sparse>" : ",dense>");
+    default: return "k_tile" + ks + ">";
   }
 }
 

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 
 #include <cuda_runtime.h>
 
@@ -11,6 +12,20 @@ namespace tsg {
 
 constexpr int kMaxMasks = 13;  // k + 1 startIdx masks, k <= 12
 constexpr int kMaxSub = 6;     // largest non-diagonal sub-gate on the GPU
+
+// Insertion masks (SPEC.md:441-449 form) for zeros at sorted `pos` inside a
+// value of `width` bits: x -> sum_i (x & m[i]) << i.
+inline int insertion_masks(const int* pos, int count, int width, uint64_t* out) {
+  int from = 0;
+  for (int i = 0; i <= count; ++i) {
+    const int to = i < count ? pos[i] - i : width;
+    uint64_t m = 0;
+    for (int b = from; b < to && b < width; ++b) m |= uint64_t{1} << b;
+    out[i] = m;
+    from = to > from ? to : from;
+  }
+  return count + 1;
+}
 
 struct GateLaunch {
   int klass = 0;   // tilesim::KernelClass
@@ -61,6 +76,82 @@ int launch_diag_batch_f64(const DiagBatchLaunch& b, cudaStream_t stream, int num
 int launch_diag_batch_f32(const DiagBatchLaunch& b, cudaStream_t stream, int num_sms);
 
 // Name of the kernel template a launch selects (for reports / profiles).
-const char* kernel_name(const GateLaunch& g, int precision_bits);
+std::string kernel_name(const GateLaunch& g, int precision_bits);
+
+// ------------------------------------------------------------ tile passes
+// A pass applies a run of fused gates to the state in ONE read + write of
+// HBM (k_pass, kernels_pass.cuh).  The state is cut into tiles of 2^M
+// amplitudes: the "tile qubits" are the low run bits [0, L) plus M - L high
+// qubits; every other qubit is fixed per tile.  A gate joins a pass when its
+// non-control sub-targets are tile qubits (GEN op) or when it is diagonal
+// (DIAG op: out-of-tile targets and controls are constants of the tile).
+// Tile coordinates: position p < L is qubit p; position L + h is high[h].
+constexpr int kPassThreads = 512;   // consumer threads (16 warps) + 1 producer warp
+constexpr int kPassLogThreads = 9;
+constexpr int kPassMaxOps = 128;  // ops + RUN headers per pass
+constexpr int kPassMaxBlob = 56 * 1024;  // run offsets + op table + op data, staged in smem
+constexpr int kPassPadBytes = 32;        // padding between runs in shared memory (bank spread)
+
+// Op kinds.  GEN ops mix 2^ks amplitudes (ks = mixed qubits, all tile
+// qubits) with one of 2^nb blocks selected by the block qubits
+// (tilesim::mixed_bits).  A RUN header precedes every maximal run of
+// consecutive diagonal ops; the run's ops are ordered by class (diagonal
+// gates commute), each class by where its in-tile bits sit relative to the
+// consumer's amplitude map x = tid + i * kPassThreads:
+//   DiagT  in-tile bits only on thread-id positions (or none): one factor per
+//          thread and tile
+//   DiagI  in-tile bits only on iteration positions: one factor per i,
+//          shared by all threads of the tile
+//   DiagX  both: a table lookup per amplitude
+//   Perm   a GEN op whose blocks are monomial (one nonzero per row: X, CX,
+//          SWAP, CCX, permutations with phases): a gather and one complex
+//          multiply per amplitude instead of a dense product
+enum PassOpKind : int32_t { kPassRun = 0, kPassDiagT = 1, kPassDiagI = 2, kPassDiagX = 3, kPassGen = 4, kPassPerm = 5 };
+
+struct PassOp {  // 192 bytes, built on the host, read from shared memory
+  int32_t kind;
+  int32_t ks;           // DIAG: table bits; GEN: mixed qubits; RUN: number of DiagT ops
+  int32_t data_off;     // byte offset of the op's data in the blob
+  int32_t n_out;        // table / block index bits taken from the tile base (out_gbit -> out_jbit)
+  int32_t log2_groups;  // GEN: groups per tile (when < kPassThreads, 2^log2_rsplit threads share a group)
+  int32_t run_i;        // RUN: number of DiagI ops
+  int32_t run_x;        // RUN: number of DiagX ops
+  int32_t aux_off;      // DiagT / DiagX: thread table offset; GEN: offset of the blocks
+  uint32_t ictl_mask, ictl_val;  // DIAG: controls on the iteration bits
+  int32_t log2_rsplit;  // GEN: the group's output rows are split over 2^log2_rsplit threads
+  uint32_t pad;
+  uint64_t cout_mask, cout_val;  // controls outside the tile (global bits)
+  uint8_t out_gbit[8], out_jbit[8];
+  uint32_t dep[8];  // DIAG: table-index bits set by iteration bit k
+  uint8_t reserved[80];
+};
+static_assert(sizeof(PassOp) == 192, "PassOp layout");
+
+// Blob: [run offsets: 2^(M-L) x u64][PassOp x n_ops][op data].  Op data:
+//   DIAG  table[2^ks + 1] {re, im} (state precision; the last entry is 1 and
+//         stands in for inactive controls); DiagT / DiagX also thr[512] u8 at
+//         aux_off: table-index bits on thread-id positions, 0xff when the
+//         controls on thread-id positions are inactive for that thread
+//   GEN   soff[2^ks] u32 (16-byte block), et[512] u32, ek[max(1, groups/512)] u32:
+//         group g = tid + 512 k sits at padded offset (et[tid] + ek[k]) & 0xffff
+//         and uses block ((et[tid] + ek[k]) >> 16) | (bits from the tile
+//         base); then at aux_off the 2^nb blocks, 2^ks x 2^ks {re, im}
+//         row-major each
+//   Perm  as GEN up to aux_off; there, per block: src[2^ks] u32 (padded
+//         offset of the source element of each row; 16-byte block) and
+//         val[2^ks] {re, im}
+struct PassLaunch {
+  int n = 0;          // state qubits
+  int tile_log2 = 0;  // M
+  int run_log2 = 0;   // L
+  int high[16] = {};  // tile qubits >= L, ascending (M - L of them)
+  void* re = nullptr;
+  void* im = nullptr;
+  const void* blob = nullptr;  // device
+  int blob_bytes = 0;
+  int n_ops = 0;
+};
+int launch_pass_f64(const PassLaunch& p, cudaStream_t stream, int num_sms);
+int launch_pass_f32(const PassLaunch& p, cudaStream_t stream, int num_sms);
 
 }  // namespace tsg

@@ -1,0 +1,512 @@
+// k_pass: a run of fused gates applied in ONE streaming pass over HBM.
+//
+// Every gate in a fused circuit reads and writes the whole state once
+// (2 * 2^n * B_amp bytes), so a circuit of G gates costs G HBM passes.  A
+// pass kernel loads a tile of 2^M amplitudes into shared memory, applies a
+// whole op list to it there, and writes it back once: G gates cost one pass
+// plus their arithmetic.  Tiles are the 2^(M-L) runs of 2^L contiguous
+// amplitudes selected by the pass's high tile qubits (PassLaunch::high): a
+// warp moves two whole 256-byte runs per 16-byte-per-thread access.  Every
+// consumer thread prefetches its share of tile j + STAGES - 1 with cp.async
+// while the CTA works on tile j (STAGES tiles in flight per SM), and writes
+// tile j back with 16-byte stores.  One bulk copy per run from a single
+// producer warp could not keep up: ~1 TB/s chip-wide for 256-byte runs
+// (profiles/r01 microbench: bulk-copy issue is ~300 cycles per thread).
+//
+// Ops (PassOp, gate_launch.hpp), in program order:
+//   GEN   a non-diagonal sub-gate, block-diagonal in its "block" qubits
+//         (tilesim::mixed_bits): the mixed qubits are tile qubits, the block
+//         qubits (anywhere) select one 2^ks x 2^ks block per group.  One
+//         thread per group: gather the 2^ks amplitudes from shared memory,
+//         the dense row-by-column product with k_direct's FMA order (Zero
+//         scalars are exact zeros of the snapped matrix), scatter in place.
+//   RUN   a run of consecutive diagonal sub-gates (they commute; the host
+//         orders them by class).  The amplitudes x = tid + i * kPassThreads
+//         of a thread stay in registers for the whole run.  Table-index bits
+//         outside the tile are per-tile constants (computed once per tile
+//         for every op), DiagT ops (in-tile bits on thread-id positions only)
+//         fold into one factor per thread, DiagI ops (in-tile bits on
+//         iteration positions only) into one factor per iteration i shared
+//         through shared memory, DiagX ops are applied amplitude by
+//         amplitude.  Inactive controls select an identity entry appended to
+//         every table (no divergent branches).
+// The CTA synchronises with a barrier between ops that touch different
+// amplitude sets.
+#pragma once
+
+#include <cstdint>
+
+#include "kernels_dmma.cuh"
+
+namespace tsg {
+
+template <typename Real>
+struct Real2Of;
+template <>
+struct Real2Of<double> {
+  using T = double2;
+};
+template <>
+struct Real2Of<float> {
+  using T = float2;
+};
+
+struct PassParams {
+  void* re;
+  void* im;
+  const unsigned char* blob;  // device copy, staged into shared memory
+  int blob_bytes;             // multiple of 16
+  int n_ops;
+  uint64_t n_tiles;
+  uint64_t tmask[kMaxMasks];  // tile id -> bits >= L (pre-shift), zeros at the high tile qubits
+  int n_tmask;
+};
+
+template <typename Real, int M, int L>
+struct PassShape {
+  static constexpr int kRuns = 1 << (M - L);
+  static constexpr int kRunLen = 1 << L;
+  static constexpr int kStride = kRunLen + kPassPadBytes / static_cast<int>(sizeof(Real));
+  static constexpr int kStageElems = kRuns * kStride;
+  static constexpr int kIter = (1 << M) / kPassThreads;  // amplitudes per thread in RUN ops
+  static constexpr int kIterBits = M - kPassLogThreads;
+  static_assert(kIter >= 1 && kIterBits <= 8, "tile / thread geometry");
+  static constexpr size_t kFiBytes = 2 * kIter * 2 * sizeof(Real);       // DiagI factors, double-buffered by tile
+  static constexpr size_t kTcBytes = 2 * kPassMaxOps * sizeof(uint32_t);  // per-tile op constants, double-buffered
+  static constexpr size_t smem_bytes(int blob_bytes, int stages) {
+    return ((static_cast<size_t>(blob_bytes) + 127) & ~size_t{127}) +
+           static_cast<size_t>(stages) * 2 * kStageElems * sizeof(Real) + kFiBytes + kTcBytes;
+  }
+};
+
+__device__ __forceinline__ void consumer_bar() { __syncthreads(); }
+
+// padded shared-memory offset of tile coordinate x
+template <int L, int STRIDE>
+__device__ __forceinline__ uint32_t pass_addr(uint32_t x) {
+  return (x >> L) * STRIDE + (x & ((1u << L) - 1));
+}
+
+template <typename Real>
+__device__ __forceinline__ void cmul_acc(Real& ar, Real& ai, Real br, Real bi) {
+  const Real r = fma(ar, br, -ai * bi);
+  ai = fma(ar, bi, ai * br);
+  ar = r;
+}
+
+// --------------------------------------------------------------------- GEN
+// Work item w = tid + kPassThreads * k: group g = w mod G' (G' = groups when
+// groups >= kPassThreads), rows [R r, R r + R) with r = w / groups and
+// R = D >> log2_rsplit.  With a row split every thread holds one item: all
+// read their group, a consumer barrier, then all write (in place).
+template <typename Real, int KS, int M, int L, int RSPLIT>
+__device__ __forceinline__ void pass_gen(const PassOp& op, const unsigned char* blob, uint32_t jo, Real* xr,
+                                         Real* xi, int tid) {
+  using R2 = typename Real2Of<Real>::T;
+  constexpr int D = 1 << KS;
+  constexpr int R = D / RSPLIT;  // rows per item
+  const unsigned char* data = blob + op.data_off;
+  const uint32_t* soff_p = reinterpret_cast<const uint32_t*>(data);
+  const uint32_t* et = reinterpret_cast<const uint32_t*>(data + ((4 * D + 15) & ~15));
+  const uint32_t* ek = et + kPassThreads;
+  const R2* blocks = reinterpret_cast<const R2*>(blob + op.aux_off);
+  uint32_t soff[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) soff[j] = soff_p[j];
+  const uint32_t n_groups = 1u << op.log2_groups;
+  const uint32_t e0 = et[tid];
+  const int r0 = RSPLIT > 1 ? (tid >> op.log2_groups) * R : 0;
+  uint32_t k = 0;
+  for (uint32_t g = tid; g < (RSPLIT > 1 ? uint32_t(kPassThreads) : n_groups); g += kPassThreads, ++k) {
+    const uint32_t e = e0 + ek[k];
+    const uint32_t a = e & 0xffffu;
+    const R2* mat = blocks + ((e >> 16) | jo) * (D * D) + r0 * D;
+    Real vr[D], vi[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      vr[j] = xr[a + soff[j]];
+      vi[j] = xi[a + soff[j]];
+    }
+    Real yr[R], yi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      yr[r] = Real(0);
+      yi[r] = Real(0);
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const R2 m = mat[r * D + c];
+        yr[r] = fma(m.x, vr[c], yr[r]);  // k_direct's order
+        yi[r] = fma(m.x, vi[c], yi[r]);
+        yr[r] = fma(-m.y, vi[c], yr[r]);
+        yi[r] = fma(m.y, vr[c], yi[r]);
+      }
+      if constexpr (RSPLIT == 1) {
+        xr[a + soff[r]] = yr[r];
+        xi[a + soff[r]] = yi[r];
+      }
+    }
+    if constexpr (RSPLIT > 1) {
+      consumer_bar();  // every item of the tile has read its group
+      if ((tid >> op.log2_groups) < RSPLIT) {  // threads without an item only join the barrier
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t so = soff_p[r0 + r];
+          xr[a + so] = yr[r];
+          xi[a + so] = yi[r];
+        }
+      }
+    }
+  }
+}
+
+// Perm: row r of the group takes element src[r] times val[r]; items as GEN
+// (a row split gathers only the item's rows; a barrier separates the
+// gathers from the in-place writes).
+template <typename Real, int KS, int M, int L, int RSPLIT>
+__device__ __forceinline__ void pass_perm(const PassOp& op, const unsigned char* blob, uint32_t jo, Real* xr,
+                                          Real* xi, int tid) {
+  using R2 = typename Real2Of<Real>::T;
+  constexpr int D = 1 << KS;
+  constexpr int R = D / RSPLIT;
+  const unsigned char* data = blob + op.data_off;
+  const uint32_t* soff_p = reinterpret_cast<const uint32_t*>(data);
+  const uint32_t* et = reinterpret_cast<const uint32_t*>(data + ((4 * D + 15) & ~15));
+  const uint32_t* ek = et + kPassThreads;
+  constexpr int kSrcBytes = (4 * D + 15) & ~15;
+  constexpr int kBlockBytes = kSrcBytes + D * static_cast<int>(sizeof(R2));
+  const uint32_t n_groups = 1u << op.log2_groups;
+  const uint32_t e0 = et[tid];
+  const int r0 = RSPLIT > 1 ? (tid >> op.log2_groups) * R : 0;
+  const bool active = RSPLIT == 1 || (tid >> op.log2_groups) < RSPLIT;
+  uint32_t k = 0;
+  for (uint32_t g = tid; g < (RSPLIT > 1 ? uint32_t(kPassThreads) : n_groups); g += kPassThreads, ++k) {
+    const uint32_t e = e0 + ek[k];
+    const uint32_t a = e & 0xffffu;
+    const unsigned char* blk = blob + op.aux_off + ((e >> 16) | jo) * kBlockBytes;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(blk) + r0;
+    const R2* val = reinterpret_cast<const R2*>(blk + kSrcBytes) + r0;
+    Real vr[R], vi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t sa = a + src[r];
+      vr[r] = xr[sa];
+      vi[r] = xi[sa];
+    }
+    if constexpr (RSPLIT > 1) consumer_bar();  // every item has gathered before anyone writes
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const R2 m = val[r];
+        const Real yr = fma(-m.y, vi[r], m.x * vr[r]);  // k_direct's order for one nonzero entry
+        const Real yi = fma(m.y, vr[r], m.x * vi[r]);
+        const uint32_t so = soff_p[r0 + r];
+        xr[a + so] = yr;
+        xi[a + so] = yi;
+      }
+    }
+  }
+}
+
+template <typename Real, int KS, int M, int L>
+__device__ __forceinline__ void pass_perm_split(const PassOp& op, const unsigned char* blob, uint32_t jo, Real* xr,
+                                                Real* xi, int tid) {
+  constexpr int D = 1 << KS;
+  switch (op.log2_rsplit) {  // KS >= 4 always has a row split (see pass_gen_split)
+    case 0:
+      if constexpr (KS <= 3) pass_perm<Real, KS, M, L, 1>(op, blob, jo, xr, xi, tid);
+      break;
+    case 1:
+      if constexpr (D >= 2) pass_perm<Real, KS, M, L, 2>(op, blob, jo, xr, xi, tid);
+      break;
+    case 2:
+      if constexpr (D >= 4) pass_perm<Real, KS, M, L, 4>(op, blob, jo, xr, xi, tid);
+      break;
+    default:
+      if constexpr (D >= 8) pass_perm<Real, KS, M, L, 8>(op, blob, jo, xr, xi, tid);
+      break;
+  }
+}
+
+template <typename Real, int KS, int M, int L>
+__device__ __forceinline__ void pass_gen_split(const PassOp& op, const unsigned char* blob, uint32_t jo, Real* xr,
+                                               Real* xi, int tid) {
+  constexpr int D = 1 << KS;
+  // tiles hold <= 2^12 amplitudes, so KS >= 4 always has < kPassThreads groups and a row split
+  switch (op.log2_rsplit) {
+    case 0:
+      if constexpr (KS <= 3) pass_gen<Real, KS, M, L, 1>(op, blob, jo, xr, xi, tid);
+      break;
+    case 1:
+      if constexpr (D >= 2) pass_gen<Real, KS, M, L, 2>(op, blob, jo, xr, xi, tid);
+      break;
+    case 2:
+      if constexpr (D >= 4) pass_gen<Real, KS, M, L, 4>(op, blob, jo, xr, xi, tid);
+      break;
+    default:
+      if constexpr (D >= 8) pass_gen<Real, KS, M, L, 8>(op, blob, jo, xr, xi, tid);
+      break;
+  }
+}
+
+template <typename Real, int M, int L>
+__device__ __forceinline__ void pass_gen_dispatch(const PassOp& op, const unsigned char* blob, uint32_t jo, Real* xr,
+                                                  Real* xi, int tid) {
+  if (op.kind == kPassPerm) {
+    switch (op.ks) {
+      case 1: pass_perm_split<Real, 1, M, L>(op, blob, jo, xr, xi, tid); break;
+      case 2: pass_perm_split<Real, 2, M, L>(op, blob, jo, xr, xi, tid); break;
+      case 3: pass_perm_split<Real, 3, M, L>(op, blob, jo, xr, xi, tid); break;
+      case 4: pass_perm_split<Real, 4, M, L>(op, blob, jo, xr, xi, tid); break;
+      default: pass_perm_split<Real, 5, M, L>(op, blob, jo, xr, xi, tid); break;
+    }
+    return;
+  }
+  switch (op.ks) {
+    case 1: pass_gen_split<Real, 1, M, L>(op, blob, jo, xr, xi, tid); break;
+    case 2: pass_gen_split<Real, 2, M, L>(op, blob, jo, xr, xi, tid); break;
+    case 3: pass_gen_split<Real, 3, M, L>(op, blob, jo, xr, xi, tid); break;
+    case 4: pass_gen_split<Real, 4, M, L>(op, blob, jo, xr, xi, tid); break;
+    default:
+      if constexpr (sizeof(Real) == 4) {
+        if (op.ks == 5) pass_gen_split<Real, 5, M, L>(op, blob, jo, xr, xi, tid);
+      }
+      break;
+  }
+}
+
+// --------------------------------------------------------------------- RUN
+template <typename Real>
+__device__ __forceinline__ typename Real2Of<Real>::T diag_entry(const PassOp& op, const unsigned char* blob,
+                                                                 uint32_t j) {
+  return reinterpret_cast<const typename Real2Of<Real>::T*>(blob + op.data_off)[j];
+}
+
+// The RUN header at ops[o] is followed by nT DiagT, nI DiagI and nX DiagX
+// ops.  Returns the index of the op after the run.
+template <typename Real, int M, int L>
+__device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const unsigned char* blob, const uint32_t* tcs,
+                                             int tid, Real (&ar)[PassShape<Real, M, L>::kIter],
+                                             Real (&ai)[PassShape<Real, M, L>::kIter],
+                                             typename Real2Of<Real>::T* fi_tab) {
+  using S = PassShape<Real, M, L>;
+  using R2 = typename Real2Of<Real>::T;
+  const int nT = ops[o].ks, nI = ops[o].run_i, nX = ops[o].run_x;
+  ++o;
+  // DiagT: one factor per thread (the loads of consecutive ops are independent)
+  Real ftr = Real(1), fti = Real(0);
+#pragma unroll 4
+  for (int t = 0; t < nT; ++t) {
+    const PassOp& op = ops[o + t];
+    const uint32_t tc = tcs[o + t];
+    const uint32_t tv = blob[op.aux_off + tid];
+    // inactive (tc = ~0 or tv = 0xff) selects the identity entry 2^ks (<= 128)
+    const R2 d = diag_entry<Real>(op, blob, min(tc | tv, 1u << op.ks));
+    cmul_acc(ftr, fti, d.x, d.y);
+  }
+  o += nT;
+  // DiagI: factor of iteration i = tid, computed by threads tid < kIter
+  if (nI > 0) {
+    if (tid < S::kIter) {
+      Real fir = Real(1), fii = Real(0);
+#pragma unroll 4
+      for (int t = 0; t < nI; ++t) {
+        const PassOp& op = ops[o + t];
+        const uint32_t tc = tcs[o + t];
+        uint32_t j = tc;
+#pragma unroll
+        for (int k = 0; k < S::kIterBits; ++k)
+          if ((tid >> k) & 1) j |= op.dep[k];
+        const bool act = (static_cast<uint32_t>(tid) & op.ictl_mask) == op.ictl_val;
+        const R2 d = diag_entry<Real>(op, blob, min(act ? j : ~0u, 1u << op.ks));
+        cmul_acc(fir, fii, d.x, d.y);
+      }
+      fi_tab[tid] = R2{fir, fii};
+    }
+    o += nI;
+  }
+  // DiagX: amplitude by amplitude, k_diag's update
+  for (int t = 0; t < nX; ++t, ++o) {
+    const PassOp& op = ops[o];
+    const uint32_t tc = tcs[o];
+    const uint32_t tv = blob[op.aux_off + tid];
+    if ((tc >> 31) || tv == 0xffu) continue;
+    const uint32_t jc = tc | tv;
+    uint32_t dep[S::kIterBits];
+#pragma unroll
+    for (int k = 0; k < S::kIterBits; ++k) dep[k] = op.dep[k];
+    const uint32_t im = op.ictl_mask, iv = op.ictl_val, one = 1u << op.ks;
+#pragma unroll
+    for (int i = 0; i < S::kIter; ++i) {
+      uint32_t j = jc;
+#pragma unroll
+      for (int k = 0; k < S::kIterBits; ++k)
+        if ((i >> k) & 1) j |= dep[k];
+      const R2 d = diag_entry<Real>(op, blob, (static_cast<uint32_t>(i) & im) == iv ? j : one);
+      const Real r0 = ar[i], i0 = ai[i];
+      ar[i] = fma(d.x, r0, -d.y * i0);
+      ai[i] = fma(d.x, i0, d.y * r0);
+    }
+  }
+  if (nI > 0) {  // uniform: every consumer thread read the same header
+    consumer_bar();
+#pragma unroll
+    for (int i = 0; i < S::kIter; ++i) {
+      const R2 f = fi_tab[i];
+      Real gr = ftr, gi = fti;
+      cmul_acc(gr, gi, f.x, f.y);
+      cmul_acc(ar[i], ai[i], gr, gi);
+    }
+  } else if (nT > 0) {
+#pragma unroll
+    for (int i = 0; i < S::kIter; ++i) cmul_acc(ar[i], ai[i], ftr, fti);
+  }
+  return o;
+}
+
+// ------------------------------------------------------------------ kernel
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Tile transfers: 16-byte chunks, chunk c of array (c / kChunksPerArray) at
+// element (c % kChunksPerArray) * kEpc of the tile's run-major order; every
+// consumer thread moves kChunks / kPassThreads chunks (a warp covers 512
+// contiguous bytes = two 256-byte runs).
+template <typename Real, int M, int L>
+struct PassCopy {
+  using S = PassShape<Real, M, L>;
+  static constexpr int kEpc = 16 / sizeof(Real);                   // elements per 16-byte chunk
+  static constexpr int kChunksPerArray = (1 << M) / kEpc;
+  static constexpr int kPerThread = 2 * kChunksPerArray / kPassThreads;
+  static_assert(kPerThread >= 1 && (2 * kChunksPerArray) % kPassThreads == 0, "copy split");
+  static_assert(S::kRunLen % kEpc == 0, "runs are whole chunks");
+};
+
+template <typename Real, int M, int L, int STAGES>
+__global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant__ PassParams p) {
+  using S = PassShape<Real, M, L>;
+  using C = PassCopy<Real, M, L>;
+  using R2 = typename Real2Of<Real>::T;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* blob = smem_raw;
+  const int blob_round = (p.blob_bytes + 127) & ~127;
+  Real* buf = reinterpret_cast<Real*>(smem_raw + blob_round);  // [STAGES][2][kStageElems]
+  R2* fi_tab = reinterpret_cast<R2*>(reinterpret_cast<unsigned char*>(buf) + sizeof(Real) * 2 * STAGES * S::kStageElems);
+  uint32_t* tc_tab = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(fi_tab) + S::kFiBytes);
+  Real* gre = static_cast<Real*>(p.re);
+  Real* gim = static_cast<Real*>(p.im);
+  const int tid = threadIdx.x;
+
+  {  // stage the blob (16-byte vectors)
+    const uint4* src = reinterpret_cast<const uint4*>(p.blob);
+    uint4* dst = reinterpret_cast<uint4*>(blob);
+    for (int i = tid; i < p.blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const uint64_t* roff = reinterpret_cast<const uint64_t*>(blob);
+  const PassOp* ops = reinterpret_cast<const PassOp*>(blob + S::kRuns * sizeof(uint64_t));
+
+  auto tile_base = [&](uint64_t tile) {
+    uint64_t b = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxMasks; ++i)
+      if (i < p.n_tmask) b += (tile & p.tmask[i]) << i;
+    return b << L;
+  };
+  // this thread's chunks: (global element offset within the tile, stage offset)
+  uint32_t c_run[C::kPerThread], c_off[C::kPerThread];
+#pragma unroll
+  for (int q = 0; q < C::kPerThread; ++q) {
+    const int c = tid + q * kPassThreads;
+    const int arr = c / C::kChunksPerArray;
+    const int e = (c % C::kChunksPerArray) * C::kEpc;
+    c_run[q] = static_cast<uint32_t>(e >> L);
+    c_off[q] = static_cast<uint32_t>(arr * S::kStageElems + (e >> L) * S::kStride + (e & (S::kRunLen - 1)));
+  }
+  auto c_global = [&](int q, uint64_t base) -> Real* {
+    const int c = tid + q * kPassThreads;
+    Real* g = c < C::kChunksPerArray ? gre : gim;
+    const int e = (c % C::kChunksPerArray) * C::kEpc;
+    return g + base + roff[c_run[q]] + (e & (S::kRunLen - 1));
+  };
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  // bases of the tiles in flight, computed once at prefetch (ring, oldest first)
+  uint64_t ring[STAGES];
+  auto prefetch = [&](uint64_t tile, int s) {
+#pragma unroll
+    for (int r = 0; r + 1 < STAGES; ++r) ring[r] = ring[r + 1];
+    if (tile < p.n_tiles) {
+      const uint64_t base = tile_base(tile);
+      ring[STAGES - 1] = base;
+      Real* st = buf + (2 * s) * S::kStageElems;
+#pragma unroll
+      for (int q = 0; q < C::kPerThread; ++q) cp_async16(st + c_off[q], c_global(q, base));
+    }
+    cp_async_commit();  // one group per tile slot, empty past the end
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES; ++s) ring[s] = 0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) prefetch(first + s * step, s);
+
+  uint32_t j = 0;
+  for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
+    const int s = static_cast<int>(j % STAGES);
+    const uint64_t tbase = ring[1];  // tile j (ring[1..] = tiles j .. j + STAGES - 2 before this prefetch)
+    // Tile-uniform op constants: table / block index bits outside the tile;
+    // all ones when the controls outside the tile are inactive.  Double-buffered by tile
+    // parity (a thread writing tile j + 2's buffer has passed tile j + 1's
+    // first barrier, so nobody reads tile j's any more).
+    uint32_t* tcs = tc_tab + (j & 1) * kPassMaxOps;
+    for (int o = tid; o < p.n_ops; o += kPassThreads) {
+      const PassOp& op = ops[o];
+      uint32_t v = 0;
+      for (int b = 0; b < op.n_out; ++b) v |= static_cast<uint32_t>((tbase >> op.out_gbit[b]) & 1u) << op.out_jbit[b];
+      tcs[o] = (tbase & op.cout_mask) != op.cout_val ? ~0u : v;
+    }
+    cp_async_wait<STAGES - 2>();  // this thread's chunks of tile j have landed
+    consumer_bar();               // ... and everyone's; the stage of tile j - 1 is stored
+    prefetch(tile + (STAGES - 1) * step, static_cast<int>((j + STAGES - 1) % STAGES));
+    Real* xr = buf + (2 * s) * S::kStageElems;
+    Real* xi = xr + S::kStageElems;
+    int o = 0;
+    while (o < p.n_ops) {
+      if (o > 0) consumer_bar();  // the previous op's writes are visible to every consumer
+      const PassOp& op = ops[o];
+      if (op.kind == kPassRun) {
+        Real ar[S::kIter], ai[S::kIter];
+#pragma unroll
+        for (int i = 0; i < S::kIter; ++i) {
+          const uint32_t a = pass_addr<L, S::kStride>(static_cast<uint32_t>(tid + i * kPassThreads));
+          ar[i] = xr[a];
+          ai[i] = xi[a];
+        }
+        o = pass_diag_run<Real, M, L>(ops, o, blob, tcs, tid, ar, ai, fi_tab + (j & 1) * S::kIter);
+#pragma unroll
+        for (int i = 0; i < S::kIter; ++i) {
+          const uint32_t a = pass_addr<L, S::kStride>(static_cast<uint32_t>(tid + i * kPassThreads));
+          xr[a] = ar[i];
+          xi[a] = ai[i];
+        }
+      } else {
+        // the skip is tile-uniform, so a row-split op's internal barrier stays uniform
+        const uint32_t tc = tcs[o];
+        if (!(tc >> 31)) pass_gen_dispatch<Real, M, L>(op, blob, tc, xr, xi, tid);
+        ++o;
+      }
+    }
+    consumer_bar();  // all ops done: write the tile back
+    const Real* st = buf + (2 * s) * S::kStageElems;
+#pragma unroll
+    for (int q = 0; q < C::kPerThread; ++q)
+      *reinterpret_cast<uint4*>(c_global(q, tbase)) = *reinterpret_cast<const uint4*>(st + c_off[q]);
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace tsg

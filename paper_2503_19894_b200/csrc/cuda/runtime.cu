@@ -9,6 +9,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -19,6 +20,7 @@
 
 #include "../host/handles.hpp"
 #include "gate_launch.hpp"
+#include "tilesim/pass.hpp"
 #include "tilesim/plan.hpp"
 
 using namespace tilesim;
@@ -206,6 +208,21 @@ struct ProgramBatch {
   size_t table_offset = 0;      // into the device arena
 };
 
+struct ProgramPass {
+  tsg::PassLaunch launch;  // re/im/blob filled per run
+  size_t blob_offset = 0;  // into the device arena
+  std::vector<int> gates;
+};
+
+// One launch of a program: a single gate, a diagonal batch or a tile pass.
+enum StepKind : int { kStepGate = 0, kStepBatch = 1, kStepPass = 2 };
+struct ProgramStep {
+  int kind = kStepGate;
+  int gate = 0;   // first gate applied by the step
+  int index = 0;  // batch / pass index
+  int n_gates = 1;
+};
+
 }  // namespace
 
 struct tsg_program {
@@ -214,6 +231,8 @@ struct tsg_program {
   int prec = 64;
   std::vector<ProgramGate> gates;
   std::vector<ProgramBatch> batches;
+  std::vector<ProgramPass> passes;
+  std::vector<ProgramStep> steps;
   void* arena = nullptr;
   double planning_s = 0.0;
   uint64_t launches = 0, bytes = 0, touched_bytes = 0, total_ops = 0;
@@ -327,30 +346,51 @@ void fill_info(const KernelPlan& p, const LaunchStructure& ls, tsg_plan_info* ou
   out->loop_count = uint64_t{1} << (p.n - p.gate.k());
   out->touched_fraction = touched_fraction(ls);
   out->batched = 0;
+  for (size_t i = 0; i < ls.controls.size() && i < 12; ++i) out->controls[i] = ls.controls[i];
+  for (int i = 0; i < ls.ks && i < 12; ++i) out->sub_targets[i] = ls.sub_targets[i];
 }
 
-void run_program(tsg_state* st, tsg_program* prog, std::vector<cudaEvent_t>* marks) {
-  for (size_t i = 0; i < prog->gates.size(); ++i) {
-    const ProgramGate& pg = prog->gates[i];
-    if (marks) ck(cudaEventRecord((*marks)[i], st->stream), "event");
-    if (pg.in_batch) continue;
-    if (pg.batch >= 0) {
-      tsg::DiagBatchLaunch b = prog->batches[pg.batch].launch;
-      b.re = st->re;
-      b.im = st->im;
-      b.tables = reinterpret_cast<const double*>(static_cast<unsigned char*>(prog->arena) +
-                                                 prog->batches[pg.batch].table_offset);
-      st->prec == 64 ? tsg::launch_diag_batch_f64(b, st->stream, st->ctx->num_sms)
-                     : tsg::launch_diag_batch_f32(b, st->stream, st->ctx->num_sms);
-      continue;
-    }
-    tsg::GateLaunch g = pg.launch;
-    g.re = st->re;
-    g.im = st->im;
-    if (pg.has_mat) g.dev_mat = static_cast<unsigned char*>(prog->arena) + pg.mat_offset;
-    launch(st, g);
+void run_step(tsg_state* st, tsg_program* prog, const ProgramStep& step) {
+  unsigned char* arena = static_cast<unsigned char*>(prog->arena);
+  if (step.kind == kStepBatch) {
+    tsg::DiagBatchLaunch b = prog->batches[step.index].launch;
+    b.re = st->re;
+    b.im = st->im;
+    b.tables = reinterpret_cast<const double*>(arena + prog->batches[step.index].table_offset);
+    st->prec == 64 ? tsg::launch_diag_batch_f64(b, st->stream, st->ctx->num_sms)
+                   : tsg::launch_diag_batch_f32(b, st->stream, st->ctx->num_sms);
+    return;
   }
-  if (marks) ck(cudaEventRecord(marks->back(), st->stream), "event");
+  if (step.kind == kStepPass) {
+    tsg::PassLaunch pl = prog->passes[step.index].launch;
+    pl.re = st->re;
+    pl.im = st->im;
+    pl.blob = arena + prog->passes[step.index].blob_offset;
+    st->prec == 64 ? tsg::launch_pass_f64(pl, st->stream, st->ctx->num_sms)
+                   : tsg::launch_pass_f32(pl, st->stream, st->ctx->num_sms);
+    return;
+  }
+  const ProgramGate& pg = prog->gates[step.gate];
+  tsg::GateLaunch g = pg.launch;
+  g.re = st->re;
+  g.im = st->im;
+  if (pg.has_mat) g.dev_mat = arena + pg.mat_offset;
+  launch(st, g);
+}
+
+// marks (profiling): one event before every gate index, the gates a step
+// applies after its first one share the step's interval (zero-length marks).
+void run_program(tsg_state* st, tsg_program* prog, std::vector<cudaEvent_t>* marks) {
+  size_t cursor = 0;
+  for (const ProgramStep& step : prog->steps) {
+    if (marks)
+      for (; cursor <= static_cast<size_t>(step.gate); ++cursor) ck(cudaEventRecord((*marks)[cursor], st->stream), "event");
+    run_step(st, prog, step);
+  }
+  if (marks) {
+    for (; cursor < prog->gates.size(); ++cursor) ck(cudaEventRecord((*marks)[cursor], st->stream), "event");
+    ck(cudaEventRecord(marks->back(), st->stream), "event");
+  }
 }
 
 // Group runs of consecutive diagonal gates into one streaming launch when
@@ -404,6 +444,322 @@ void plan_diagonal_batches(tsg_program* prog, std::vector<unsigned char>& arena)
       prog->batches.push_back(pb);
     }
     i = j;
+  }
+}
+
+// Device blob of one tile pass (layout: gate_launch.hpp, PassLaunch).
+template <typename Real>
+void append_real2(std::vector<unsigned char>& v, double re, double im) {
+  const Real x[2] = {static_cast<Real>(re), static_cast<Real>(im)};
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(x);
+  v.insert(v.end(), b, b + sizeof x);
+}
+
+void pad16(std::vector<unsigned char>& v) { v.resize((v.size() + 15) & ~size_t{15}, 0); }
+
+template <typename T>
+void append_pod(std::vector<unsigned char>& v, const T& x) {
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(&x);
+  v.insert(v.end(), b, b + sizeof(T));
+}
+
+// Tile-pass op record + data for one gate (layout: gate_launch.hpp).  `pos`
+// maps a qubit to its tile coordinate (-1 outside the tile); offsets in the
+// op are relative to the start of `data` and rebased by the caller.
+template <typename Real>
+tsg::PassOp build_pass_op(const LaunchStructure& ls, const std::vector<int>& pos, int M, int L,
+                          std::vector<unsigned char>& data) {
+  constexpr int T = tsg::kPassLogThreads;
+  const int stride = (1 << L) + tsg::kPassPadBytes / static_cast<int>(sizeof(Real));
+  auto padded = [&](uint32_t x) { return (x >> L) * static_cast<uint32_t>(stride) + (x & ((1u << L) - 1)); };
+  tsg::PassOp op;
+  std::memset(&op, 0, sizeof op);
+  const int d = 1 << ls.ks;
+  pad16(data);
+  op.data_off = static_cast<int32_t>(data.size());
+  // controls outside the tile are shared by both op families
+  std::vector<std::pair<int, uint32_t>> cin;  // (tile position, value)
+  for (int c : ls.controls) {
+    const uint32_t v = static_cast<uint32_t>((ls.control_values >> c) & 1u);
+    if (pos[c] < 0) {
+      op.cout_mask |= uint64_t{1} << c;
+      op.cout_val |= static_cast<uint64_t>(v) << c;
+    } else {
+      cin.emplace_back(pos[c], v);
+    }
+  }
+  if (ls.klass == KernelClass::Diagonal) {
+    if (ls.ks > 7) throw SimError("pass: diagonal op wider than 7 qubits");
+    op.ks = ls.ks;
+    uint32_t thr_ctl_mask = 0, thr_ctl_val = 0;
+    std::vector<std::pair<int, int>> thr_bits;  // (tile position < T, table bit)
+    bool on_thread = false, on_iter = false;
+    for (const auto& [p, v] : cin) {
+      if (p < T) {
+        thr_ctl_mask |= 1u << p;
+        thr_ctl_val |= v << p;
+        on_thread = true;
+      } else {
+        op.ictl_mask |= 1u << (p - T);
+        op.ictl_val |= v << (p - T);
+        on_iter = true;
+      }
+    }
+    for (int b = 0; b < ls.ks; ++b) {
+      const int q = ls.sub_targets[b], p = pos[q];
+      if (p < 0) {
+        op.out_gbit[op.n_out] = static_cast<uint8_t>(q);
+        op.out_jbit[op.n_out++] = static_cast<uint8_t>(b);
+      } else if (p < T) {
+        thr_bits.emplace_back(p, b);
+        on_thread = true;
+      } else {
+        op.dep[p - T] |= 1u << b;
+        on_iter = true;
+      }
+    }
+    op.kind = on_thread && on_iter ? tsg::kPassDiagX : (on_iter ? tsg::kPassDiagI : tsg::kPassDiagT);
+    for (int j = 0; j < d; ++j) append_real2<Real>(data, ls.sub_re[j * d + j], ls.sub_im[j * d + j]);
+    append_real2<Real>(data, 1.0, 0.0);  // inactive controls
+    if (op.kind != tsg::kPassDiagI) {
+      pad16(data);
+      op.aux_off = static_cast<int32_t>(data.size());
+      for (int t = 0; t < tsg::kPassThreads; ++t) {
+        uint32_t v = 0;
+        for (const auto& [p, b] : thr_bits) v |= ((static_cast<uint32_t>(t) >> p) & 1u) << b;
+        if ((static_cast<uint32_t>(t) & thr_ctl_mask) != thr_ctl_val) v = 0xffu;
+        data.push_back(static_cast<unsigned char>(v));
+      }
+    }
+    return op;
+  }
+  // GEN: mixed qubits E (tile qubits) and block qubits B (anywhere): the
+  // sub-gate is 2^|B| blocks of 2^|E| x 2^|E| (tilesim::mixed_bits)
+  op.kind = tsg::kPassGen;
+  const std::vector<int> ebits = mixed_bits(ls);
+  std::vector<int> bbits;
+  for (int b = 0; b < ls.ks; ++b)
+    if (std::find(ebits.begin(), ebits.end(), b) == ebits.end()) bbits.push_back(b);
+  const int ke = static_cast<int>(ebits.size()), nb = static_cast<int>(bbits.size());
+  const int de = 1 << ke;
+  op.ks = ke;
+  std::vector<int> zpos;  // tile positions fixed within a group: mixed qubits + in-tile controls
+  uint32_t cin_val = 0;
+  for (const auto& [p, v] : cin) {
+    zpos.push_back(p);
+    cin_val |= v << p;
+  }
+  for (int b : ebits) {
+    const int p = pos[ls.sub_targets[b]];
+    if (p < 0) throw SimError("pass: mixed qubit outside the tile");
+    zpos.push_back(p);
+  }
+  std::vector<std::pair<int, int>> blk_in;  // (tile position, block bit)
+  for (int i = 0; i < nb; ++i) {
+    const int q = ls.sub_targets[bbits[i]], p = pos[q];
+    if (p < 0) {
+      op.out_gbit[op.n_out] = static_cast<uint8_t>(q);
+      op.out_jbit[op.n_out++] = static_cast<uint8_t>(i);
+    } else {
+      blk_in.emplace_back(p, i);
+    }
+  }
+  std::sort(zpos.begin(), zpos.end());
+  const int count = static_cast<int>(zpos.size());
+  uint64_t gm[64];
+  const int n_gm = tsg::insertion_masks(zpos.data(), count, M - count, gm);
+  op.log2_groups = M - count;
+  auto deposit = [&](uint32_t g) {
+    uint64_t x = 0;
+    for (int i = 0; i < n_gm; ++i) x += (g & gm[i]) << i;
+    return static_cast<uint32_t>(x);
+  };
+  auto entry = [&](uint32_t x) {  // padded offset | block bits << 16 (additive over disjoint bits)
+    uint32_t jb = 0;
+    for (const auto& [p, i] : blk_in) jb |= ((x >> p) & 1u) << i;
+    return padded(x) | (jb << 16);
+  };
+  for (int j = 0; j < de; ++j) {
+    uint32_t x = 0;
+    for (int b = 0; b < ke; ++b) x |= static_cast<uint32_t>((j >> b) & 1) << pos[ls.sub_targets[ebits[b]]];
+    append_pod(data, padded(x));
+  }
+  pad16(data);
+  const uint32_t n_groups = 1u << op.log2_groups;
+  // fewer groups than threads: split each group's rows over 2^rsplit threads
+  int rsplit = 0;
+  while ((n_groups << (rsplit + 1)) <= static_cast<uint32_t>(tsg::kPassThreads) && (1 << (rsplit + 1)) <= std::min(de, 8))
+    ++rsplit;
+  op.log2_rsplit = rsplit;
+  if (ke >= 4 && rsplit == 0) throw SimError("pass: an op of >= 4 mixed qubits needs a row split");
+  for (uint32_t t = 0; t < static_cast<uint32_t>(tsg::kPassThreads); ++t) {
+    const uint32_t g = t & (n_groups - 1);
+    append_pod(data, (t < (n_groups << rsplit)) ? entry(deposit(g) | cin_val) : 0u);
+  }
+  const uint32_t n_k = std::max<uint32_t>(1, n_groups / tsg::kPassThreads);
+  for (uint32_t k = 0; k < n_k; ++k) append_pod(data, k == 0 ? 0u : entry(deposit(k * tsg::kPassThreads)));
+  pad16(data);
+  op.aux_off = static_cast<int32_t>(data.size());
+  auto full_index = [&](int je, int jb) {
+    int r = 0;
+    for (int b = 0; b < ke; ++b) r |= ((je >> b) & 1) << ebits[b];
+    for (int b = 0; b < nb; ++b) r |= ((jb >> b) & 1) << bbits[b];
+    return r;
+  };
+  if (monomial(ls)) {  // Perm: per block src[de] then val[de]
+    op.kind = tsg::kPassPerm;
+    std::vector<uint32_t> soffs(de);
+    for (int j = 0; j < de; ++j) {
+      uint32_t x = 0;
+      for (int b = 0; b < ke; ++b) x |= static_cast<uint32_t>((j >> b) & 1) << pos[ls.sub_targets[ebits[b]]];
+      soffs[j] = padded(x);
+    }
+    for (int jb = 0; jb < (1 << nb); ++jb) {
+      std::vector<int> col(de, 0);
+      for (int r = 0; r < de; ++r)
+        for (int c = 0; c < de; ++c) {
+          const int e = full_index(r, jb) * d + full_index(c, jb);
+          if (ls.sub_re[e] != 0.0 || ls.sub_im[e] != 0.0) col[r] = c;
+        }
+      for (int r = 0; r < de; ++r) append_pod(data, soffs[col[r]]);
+      pad16(data);
+      for (int r = 0; r < de; ++r) {
+        const int e = full_index(r, jb) * d + full_index(col[r], jb);
+        append_real2<Real>(data, ls.sub_re[e], ls.sub_im[e]);
+      }
+    }
+    return op;
+  }
+  for (int jb = 0; jb < (1 << nb); ++jb)
+    for (int r = 0; r < de; ++r)
+      for (int c = 0; c < de; ++c) {
+        const int e = full_index(r, jb) * d + full_index(c, jb);
+        append_real2<Real>(data, ls.sub_re[e], ls.sub_im[e]);
+      }
+  return op;
+}
+
+// Device blob of one tile pass (layout: gate_launch.hpp).  Runs of
+// consecutive diagonal gates get a RUN header and are ordered by class
+// (DiagT, DiagI, DiagX; program order within a class -- diagonal gates
+// commute).
+template <typename Real>
+ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const PassConfig& cfg,
+                       std::vector<unsigned char>& arena) {
+  const int n = prog->n, L = cfg.run_log2, M = cfg.tile_log2;
+  const int nh = M - L;
+  if (static_cast<int>(step.high.size()) != nh) throw SimError("pass: high tile qubit count");
+  std::vector<int> pos(n, -1);
+  for (int q = 0; q < L; ++q) pos[q] = q;
+  for (int h = 0; h < nh; ++h) pos[step.high[h]] = L + h;
+
+  std::vector<tsg::PassOp> ops;
+  std::vector<unsigned char> data;
+  size_t i = 0;
+  while (i < step.gates.size()) {
+    const LaunchStructure& ls = prog->gates[step.gates[i]].ls;
+    if (ls.klass != KernelClass::Diagonal) {
+      ops.push_back(build_pass_op<Real>(ls, pos, M, L, data));
+      ++i;
+      continue;
+    }
+    std::vector<tsg::PassOp> cls[3];
+    for (; i < step.gates.size() && prog->gates[step.gates[i]].ls.klass == KernelClass::Diagonal; ++i) {
+      tsg::PassOp op = build_pass_op<Real>(prog->gates[step.gates[i]].ls, pos, M, L, data);
+      cls[op.kind - tsg::kPassDiagT].push_back(op);
+    }
+    tsg::PassOp hdr;
+    std::memset(&hdr, 0, sizeof hdr);
+    hdr.kind = tsg::kPassRun;
+    hdr.ks = static_cast<int32_t>(cls[0].size());
+    hdr.run_i = static_cast<int32_t>(cls[1].size());
+    hdr.run_x = static_cast<int32_t>(cls[2].size());
+    ops.push_back(hdr);
+    for (auto& c : cls) ops.insert(ops.end(), c.begin(), c.end());
+  }
+  if (ops.size() > static_cast<size_t>(tsg::kPassMaxOps)) throw SimError("pass: too many ops");
+  if (std::getenv("TSG_PASS_DEBUG")) {
+    int cnt[5] = {0, 0, 0, 0, 0};
+    for (const tsg::PassOp& op : ops) ++cnt[op.kind];
+    std::fprintf(stderr, "pass gates %zu high", step.gates.size());
+    for (int h : step.high) std::fprintf(stderr, " %d", h);
+    std::fprintf(stderr, ": runs %d diagT %d diagI %d diagX %d gen %d (ks:", cnt[0], cnt[1], cnt[2], cnt[3], cnt[4]);
+    for (const tsg::PassOp& op : ops)
+      if (op.kind == tsg::kPassGen) std::fprintf(stderr, " %d/%d", op.ks, op.log2_rsplit);
+    std::fprintf(stderr, ")\n");
+  }
+  const size_t data_base = (size_t{8} << nh) + ops.size() * sizeof(tsg::PassOp);
+  for (tsg::PassOp& op : ops) {
+    if (op.kind == tsg::kPassRun) continue;
+    op.data_off += static_cast<int32_t>(data_base);
+    if (op.kind != tsg::kPassDiagI) op.aux_off += static_cast<int32_t>(data_base);
+  }
+  std::vector<unsigned char> blob;
+  for (int r = 0; r < (1 << nh); ++r) {
+    uint64_t o = 0;
+    for (int h = 0; h < nh; ++h) o |= static_cast<uint64_t>((r >> h) & 1) << step.high[h];
+    append_pod(blob, o);
+  }
+  const unsigned char* ob = reinterpret_cast<const unsigned char*>(ops.data());
+  blob.insert(blob.end(), ob, ob + ops.size() * sizeof(tsg::PassOp));
+  blob.insert(blob.end(), data.begin(), data.end());
+  pad16(blob);
+  if (blob.size() > static_cast<size_t>(tsg::kPassMaxBlob)) throw SimError("pass: blob exceeds shared-memory budget");
+
+  ProgramPass pp;
+  pp.gates = step.gates;
+  tsg::PassLaunch& pl = pp.launch;
+  pl.n = n;
+  pl.tile_log2 = M;
+  pl.run_log2 = L;
+  for (int h = 0; h < nh; ++h) pl.high[h] = step.high[h];
+  pl.n_ops = static_cast<int>(ops.size());
+  pl.blob_bytes = static_cast<int>(blob.size());
+  pp.blob_offset = (arena.size() + 255) & ~size_t{255};
+  arena.resize(pp.blob_offset + blob.size());
+  std::memcpy(arena.data() + pp.blob_offset, blob.data(), blob.size());
+  return pp;
+}
+
+// Steps of a program: tile passes (tilesim/pass.hpp) when the state holds at
+// least one tile, else per-gate launches with diagonal batches.
+void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
+  const PassConfig cfg = pass_config(prog->prec);
+  const bool use_pass = !std::getenv("TSG_NO_PASS") && prog->n >= cfg.tile_log2;
+  if (use_pass) {
+    std::vector<LaunchStructure> ls;
+    ls.reserve(prog->gates.size());
+    for (const ProgramGate& pg : prog->gates) ls.push_back(pg.ls);
+    for (const PassStep& st : plan_passes(ls, prog->n, cfg)) {
+      ProgramStep step;
+      step.gate = st.gates.front();
+      step.n_gates = static_cast<int>(st.gates.size());
+      if (st.is_pass) {
+        step.kind = kStepPass;
+        step.index = static_cast<int>(prog->passes.size());
+        prog->passes.push_back(prog->prec == 64 ? build_pass<double>(prog, st, cfg, arena)
+                                                : build_pass<float>(prog, st, cfg, arena));
+        for (size_t i = 0; i < st.gates.size(); ++i) {
+          prog->gates[st.gates[i]].batch = i == 0 ? step.index : -1;
+          prog->gates[st.gates[i]].in_batch = i != 0;
+        }
+      }
+      prog->steps.push_back(step);
+    }
+    return;
+  }
+  if (!std::getenv("TSG_NO_DIAG_BATCH")) plan_diagonal_batches(prog, arena);
+  for (size_t i = 0; i < prog->gates.size(); ++i) {
+    const ProgramGate& pg = prog->gates[i];
+    if (pg.in_batch || pg.ls.klass == KernelClass::Identity) continue;
+    ProgramStep step;
+    step.gate = static_cast<int>(i);
+    if (pg.batch >= 0) {
+      step.kind = kStepBatch;
+      step.index = pg.batch;
+      step.n_gates = prog->batches[pg.batch].launch.n_gates;
+    }
+    prog->steps.push_back(step);
   }
 }
 
@@ -809,12 +1165,11 @@ int tsg_program_create(tsg_ctx* ctx, const tsc_circuit* fused, double zero_tol, 
       prog->total_ops += pg.plan.profile.op_count;
       prog->gates.push_back(std::move(pg));
     }
-    if (!std::getenv("TSG_NO_DIAG_BATCH")) plan_diagonal_batches(prog.get(), arena);
-    for (const ProgramGate& pg : prog->gates) {  // one launch per batch or per non-identity gate
-      if (pg.in_batch || pg.ls.klass == KernelClass::Identity) continue;
+    plan_steps(prog.get(), arena);
+    for (const ProgramStep& step : prog->steps) {  // one launch per step
       ++prog->launches;
       prog->bytes += 2 * (uint64_t{1} << prog->n) * amp;
-      const double frac = pg.batch >= 0 ? 1.0 : touched_fraction(pg.ls);
+      const double frac = step.kind != kStepGate ? 1.0 : touched_fraction(prog->gates[step.gate].ls);
       prog->touched_bytes += static_cast<uint64_t>(2.0 * std::ldexp(1.0, prog->n) * amp * frac);
     }
     if (!arena.empty()) {
@@ -939,6 +1294,39 @@ int tsg_program_gate_info(const tsg_program* prog, uint64_t i, tsg_plan_info* ou
     out->batched = prog->gates[i].in_batch ? 2 : (prog->gates[i].batch >= 0 ? 1 : 0);
     if (out->batched == 1) out->touched_fraction = 1.0;
     if (out->batched == 2) out->touched_fraction = 0.0;
+  })
+}
+
+int tsg_program_step_count(const tsg_program* prog, uint64_t* out) {
+  TSG_TRY({
+    require(prog && out, "null argument");
+    *out = prog->steps.size();
+  })
+}
+
+int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* out) {
+  TSG_TRY({
+    require(prog && out, "null argument");
+    require(i < prog->steps.size(), "step index out of range");
+    const ProgramStep& st = prog->steps[i];
+    std::memset(out, 0, sizeof *out);
+    out->kind = st.kind;
+    out->first_gate = static_cast<uint64_t>(st.gate);
+    out->n_gates = static_cast<uint64_t>(st.n_gates);
+    std::string name;
+    if (st.kind == kStepPass) {
+      const ProgramPass& pp = prog->passes[st.index];
+      out->n_high = pp.launch.tile_log2 - pp.launch.run_log2;
+      for (int h = 0; h < out->n_high; ++h) out->high[h] = pp.launch.high[h];
+      name = "k_pass";
+    } else if (st.kind == kStepBatch) {
+      name = "k_diag_batch";
+    } else {
+      tsg::GateLaunch g = prog->gates[st.gate].launch;
+      if (prog->gates[st.gate].has_mat) g.dev_mat = prog->arena;
+      name = tsg::kernel_name(g, prog->prec);
+    }
+    std::strncpy(out->kernel, name.c_str(), sizeof(out->kernel) - 1);
   })
 }
 

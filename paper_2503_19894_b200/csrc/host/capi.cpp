@@ -3,6 +3,7 @@
 #include <cstring>
 
 #include "handles.hpp"
+#include "tilesim/pass.hpp"
 
 namespace tsg_detail {
 static thread_local std::string g_last_error;
@@ -201,6 +202,32 @@ int tsc_estimate_cost(const tsc_cost_model* cm, int k, uint64_t op_count, int th
 
 // ---------------------------------------------------------------- sharding
 extern "C" {
+
+int tsc_plan_passes(const tsc_circuit* fused, int precision_bits, double zero_tol, double one_tol, int* step_of_gate,
+                    int* step_is_pass, int* step_high, uint64_t* n_steps) {
+  TSG_TRY({
+    require(fused && n_steps, "null argument");
+    require(precision_bits == 64 || precision_bits == 32, "precision_bits must be 64 or 32");
+    const int n = fused->c.n_qubits;
+    std::vector<LaunchStructure> ls;
+    for (const Gate& g : fused->c.gates) {
+      const KernelPlan plan = plan_kernel(g, n, 0, zero_tol, one_tol, false);
+      ls.push_back(precision_bits == 64 ? plan.launch : derive_launch(plan, nullptr, precision_bits));
+    }
+    const auto steps = plan_passes(ls, n, pass_config(precision_bits));
+    if (step_of_gate)
+      for (size_t g = 0; g < ls.size(); ++g) step_of_gate[g] = -1;
+    for (size_t s = 0; s < steps.size(); ++s) {
+      if (step_of_gate)
+        for (int g : steps[s].gates) step_of_gate[g] = static_cast<int>(s);
+      if (step_is_pass) step_is_pass[s] = steps[s].is_pass ? 1 : 0;
+      if (step_high)
+        for (int h = 0; h < 16; ++h)
+          step_high[16 * s + h] = h < static_cast<int>(steps[s].high.size()) ? steps[s].high[h] : -1;
+    }
+    *n_steps = steps.size();
+  })
+}
 
 int tsc_shard_plan_create(const tsc_circuit* fused, int n_global, double zero_tol, double one_tol,
                           tsc_shard_plan** out) {

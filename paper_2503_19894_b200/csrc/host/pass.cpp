@@ -1,0 +1,175 @@
+// Tile-pass planning (include/tilesim/pass.hpp).  Host only: the device blob
+// for a planned pass is built in cuda/runtime.cu (build_pass_blob).
+#include "tilesim/pass.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+namespace tilesim {
+
+PassConfig pass_config(int precision_bits) {
+  PassConfig c;
+  if (precision_bits == 64) {
+    c.tile_log2 = 11;  // 32 KiB of complex128 per tile
+    c.run_log2 = 5;    // 256-byte runs per array
+    c.max_gen_ks = 4;  // dense ks = 5 complex128 is FP64-bound: own DMMA kernel
+    c.amp_real_bytes = 8;
+  } else {
+    c.tile_log2 = 12;
+    c.run_log2 = 6;
+    c.max_gen_ks = 5;
+    c.amp_real_bytes = 4;
+  }
+  const char* f = std::getenv("TSG_PASS_FORCE");
+  c.force = f && f[0] == '1';
+  return c;
+}
+
+namespace {
+
+constexpr int kPassOpRecord = 192;  // sizeof(tsg::PassOp)
+constexpr int kThreads = 512;       // tsg::kPassThreads (consumer threads of k_pass)
+
+}  // namespace
+
+std::vector<int> mixed_bits(const LaunchStructure& ls) {
+  const int d = 1 << ls.ks;
+  int mixed = 0;
+  for (int r = 0; r < d; ++r)
+    for (int c = 0; c < d; ++c)
+      if (ls.sub_re[r * d + c] != 0.0 || ls.sub_im[r * d + c] != 0.0) mixed |= r ^ c;
+  std::vector<int> out;
+  for (int b = 0; b < ls.ks; ++b)
+    if ((mixed >> b) & 1) out.push_back(b);
+  return out;
+}
+
+bool monomial(const LaunchStructure& ls) {
+  const int d = 1 << ls.ks;
+  for (int r = 0; r < d; ++r) {
+    int nz = 0;
+    for (int c = 0; c < d; ++c) nz += ls.sub_re[r * d + c] != 0.0 || ls.sub_im[r * d + c] != 0.0;
+    if (nz != 1) return false;
+  }
+  return true;
+}
+
+PassRole pass_role(const LaunchStructure& ls, const PassConfig& cfg) {
+  switch (ls.klass) {
+    case KernelClass::Identity: return PassRole::Standalone;
+    case KernelClass::Diagonal: return ls.ks <= 7 ? PassRole::Diag : PassRole::Standalone;
+    default: {
+      const int ke = static_cast<int>(mixed_bits(ls).size());
+      const int kmax = monomial(ls) ? 5 : cfg.max_gen_ks;
+      if (ke < 1 || ke > kmax || ls.ks - ke > 8) return PassRole::Standalone;
+      if (ke + static_cast<int>(ls.controls.size()) > 15) return PassRole::Standalone;
+      return PassRole::Gen;
+    }
+  }
+}
+
+int pass_op_bytes(const LaunchStructure& ls, const PassConfig& cfg) {
+  const int cplx = 2 * cfg.amp_real_bytes;
+  int data = 0;
+  if (ls.klass == KernelClass::Diagonal) {
+    // table + identity entry, per-thread index bits; a RUN header may be added
+    data = ((((1 << ls.ks) + 1) * cplx + 15) & ~15) + kThreads + kPassOpRecord;
+  } else {
+    const int ke = static_cast<int>(mixed_bits(ls).size());
+    const int d = 1 << ke, blocks = 1 << (ls.ks - ke);
+    const int groups = 1 << std::max(0, cfg.tile_log2 - ke);  // upper bound: controls may fall outside the tile
+    const int block_bytes = monomial(ls) ? ((4 * d + 15) & ~15) + d * cplx : d * d * cplx;
+    data = ((4 * d + 15) & ~15) + 4 * kThreads + 4 * std::max(1, groups / kThreads) + 16 + blocks * block_bytes;
+  }
+  return kPassOpRecord + ((data + 15) & ~15);
+}
+
+double pass_op_sweeps(const LaunchStructure& ls, const PassConfig& cfg) {
+  if (ls.klass == KernelClass::Diagonal) return cfg.diag_sweeps;
+  if (monomial(ls)) return cfg.perm_sweeps * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
+  const int ke = static_cast<int>(mixed_bits(ls).size());
+  return cfg.gen_sweeps[std::min(ke, 5)] * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
+}
+
+double standalone_sweeps(const LaunchStructure& ls, const PassConfig& cfg) {
+  return cfg.standalone_sweeps * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
+}
+
+std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int n, const PassConfig& cfg) {
+  std::vector<PassStep> steps;
+  const int L = cfg.run_log2, M = cfg.tile_log2;
+  const int hmax = M - L;
+  const bool passes_possible = n >= M;
+  const int run_table = 8 << hmax;
+
+  std::vector<int> cur;      // gates of the open pass
+  std::vector<int> cur_high; // mixed qubits >= L of the open pass
+  int cur_bytes = run_table;
+
+  auto emit_standalone = [&](int g) {
+    PassStep s;
+    s.gates.push_back(g);
+    steps.push_back(std::move(s));
+  };
+  auto flush = [&]() {
+    if (cur.empty()) return;
+    double alone = 0.0, inside = cfg.base_sweeps;
+    for (int g : cur) {
+      alone += standalone_sweeps(gates[g], cfg);
+      inside += pass_op_sweeps(gates[g], cfg);
+    }
+    if (cfg.force || (cur.size() >= 2 && inside < alone)) {
+      PassStep s;
+      s.is_pass = true;
+      s.gates = cur;
+      s.high = cur_high;
+      // pad with the lowest free qubits above the runs (fills the tile)
+      for (int q = L; q < n && static_cast<int>(s.high.size()) < hmax; ++q)
+        if (std::find(s.high.begin(), s.high.end(), q) == s.high.end()) s.high.push_back(q);
+      std::sort(s.high.begin(), s.high.end());
+      steps.push_back(std::move(s));
+    } else {
+      for (int g : cur) emit_standalone(g);
+    }
+    cur.clear();
+    cur_high.clear();
+    cur_bytes = run_table;
+  };
+
+  for (int i = 0; i < static_cast<int>(gates.size()); ++i) {
+    const LaunchStructure& ls = gates[i];
+    if (ls.klass == KernelClass::Identity) continue;
+    PassRole role = passes_possible ? pass_role(ls, cfg) : PassRole::Standalone;
+    if (role != PassRole::Standalone && !cfg.force && pass_op_sweeps(ls, cfg) >= standalone_sweeps(ls, cfg))
+      role = PassRole::Standalone;  // cheaper on its own kernel
+    if (role == PassRole::Standalone) {
+      flush();
+      emit_standalone(i);
+      continue;
+    }
+    std::vector<int> mixed;  // qubits the gate mixes (must be tile qubits)
+    if (role == PassRole::Gen)
+      for (int b : mixed_bits(ls)) mixed.push_back(ls.sub_targets[b]);
+    std::vector<int> need = cur_high;
+    for (int q : mixed)
+      if (q >= L && std::find(need.begin(), need.end(), q) == need.end()) need.push_back(q);
+    const int bytes = pass_op_bytes(ls, cfg);
+    // ops + RUN headers must stay within kPassMaxOps (128): at most 2 records per gate
+    const bool fits = static_cast<int>(need.size()) <= hmax && 2 * (static_cast<int>(cur.size()) + 1) <= 128 &&
+                      static_cast<int>(cur.size()) < cfg.max_ops && cur_bytes + bytes <= cfg.max_blob;
+    if (!fits) {
+      flush();
+      need.clear();
+      for (int q : mixed)
+        if (q >= L) need.push_back(q);
+    }
+    cur.push_back(i);
+    cur_high = need;
+    cur_bytes += bytes;
+  }
+  flush();
+  return steps;
+}
+
+}  // namespace tilesim

@@ -1,0 +1,54 @@
+"""Micro-cases for the tile-pass kernel (design measurements, not product):
+each case is a small synthetic gate list at n=28 whose gates all fit one pass;
+prints device ms per pass and the same gates without passes."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2503_19894_b200 as ts  # noqa: E402
+from tests._util import random_gate_matrix  # noqa: E402
+
+N = int(os.environ.get("PB_N", 28))
+PREC = os.environ.get("PB_PREC", "f64")
+
+
+def case(name, gates):
+    c = ts.Circuit(N)
+    for q, kind in gates:
+        c.add_matrix(sorted(q), random_gate_matrix(len(q), sum(q) * 7 + len(name), kind))
+    out = []
+    for no_pass in (False, True):
+        if no_pass:
+            os.environ["TSG_NO_PASS"] = "1"
+        prog = ts.Program(c, PREC)
+        os.environ.pop("TSG_NO_PASS", None)
+        sv = ts.Statevector(N, PREC).init_basis(3)
+        prog.run(sv)
+        best = min(prog.run(sv)["execution_s"] for _ in range(3))
+        out.append((best * 1e3, [s["kernel"] for s in prog.steps()]))
+    sweep_ms = 2 * (1 << N) * (16 if PREC == "f64" else 8) / 6.5e12 * 1e3
+    print(f"{name:28s} pass {out[0][0]:7.3f} ms  no-pass {out[1][0]:7.3f} ms  (1 sweep at 6.5 TB/s: {sweep_ms:.3f} ms) "
+          f"steps {out[0][1]}")
+
+
+sel = sys.argv[1:] or None
+cases = {
+    "empty-ish (1 diag T)": [([2, 3], "diag"), ([1, 4], "diag")],
+    "2x gen ks1 low": [([1], "dense"), ([3], "dense")],
+    "2x gen ks1 high": [([7], "dense"), ([9], "dense")],
+    "2x gen ks2": [([6, 7], "dense"), ([8, 9], "dense")],
+    "2x gen ks3": [([5, 6, 7], "dense"), ([8, 9, 10], "dense")],
+    "2x gen ks4": [([5, 6, 7, 8], "dense"), ([7, 8, 9, 10], "dense")],
+    "2x gen ks4 low": [([0, 1, 2, 3], "dense"), ([1, 2, 3, 4], "dense")],
+    "8x diag X": [([0, 1, 9, 10], "diag")] * 8,
+    "8x diag T": [([0, 1, 20, 21], "diag")] * 8,
+    "8x diag I": [([9, 10, 20, 21], "diag")] * 8,
+    "8x diag C": [([22, 23, 24, 25], "diag")] * 8,
+    "4x perm ks2": [([6, 7], "perm"), ([8, 9], "perm"), ([1, 7], "perm"), ([2, 9], "perm")],
+    "4x perm ks4": [([0, 1, 9, 10], "perm"), ([2, 3, 7, 8], "perm"), ([0, 2, 9, 7], "perm"), ([5, 6, 7, 8], "perm")],
+}
+for k, v in cases.items():
+    if sel is None or any(s in k for s in sel):
+        case(k, v)
