@@ -59,6 +59,15 @@ std::vector<int> mixed_bits(const LaunchStructure& ls);
 // permutation with phases): a pass applies it as a gather (Perm op).
 bool monomial(const LaunchStructure& ls);
 
+// Block decomposition of a non-diagonal sub-gate over its block bits: one
+// launch structure per block value, with the block qubits added to the
+// controls (the plan's exact-identity control peeling, generalised to
+// non-identity blocks).  Identity blocks are dropped.  Every result touches
+// 2^-|B| of the state with a 2^|E|-qubit sub-gate, so a 5-qubit gate with one
+// block qubit costs two 4-qubit half-sweeps instead of one FP64-bound
+// 5-qubit sweep.  Returns {ls} when every bit is mixed.
+std::vector<LaunchStructure> split_blocks(const LaunchStructure& ls, int precision_bits);
+
 // How one gate can be executed inside a pass (or not at all).
 PassRole pass_role(const LaunchStructure& ls, const PassConfig& cfg);
 

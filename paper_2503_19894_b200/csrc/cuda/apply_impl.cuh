@@ -287,13 +287,18 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
     if (S::LOG2G + below == L) break;
     L = S::LOG2G + below;
   }
+  // element bit b of the launch's element order (GateLaunch::perm, a qubit
+  // permutation) is qubit st[b]; runs follow the same order, so the smem
+  // layout of the permuted gate is that of a gate on targets st[]
+  int st[8];
+  for (int b = 0; b < g.ks; ++b) st[b] = g.sub_targets[__builtin_ctz(static_cast<unsigned>(g.perm[1 << b]))];
   int n_low = 0, high_pos[24], n_high = 0, run_pos[8], n_run = 0, low_pos[24];
   for (int i = 0; i < nt; ++i) {
     if (tg[i] < L) low_pos[n_low++] = tg[i];
     else high_pos[n_high++] = tg[i] - L;
   }
   for (int b = 0; b < g.ks; ++b)
-    if (g.sub_targets[b] >= L) run_pos[n_run++] = g.sub_targets[b];
+    if (st[b] >= L) run_pos[n_run++] = st[b];
   if (L + n_high > g.n) return false;
   const int tile_bits = g.n - L - n_high;
   p.n_tiles = uint64_t{1} << tile_bits;
@@ -318,7 +323,7 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
     int hb = 0;
     for (int b = 0; b < KS; ++b) {
       const uint32_t bit = (j >> b) & 1u;
-      if (g.sub_targets[b] < L) low |= bit << g.sub_targets[b];
+      if (st[b] < L) low |= bit << st[b];
       else run |= bit << hb++;
     }
     p.soff[j] = run * p.run_stride + low;
@@ -367,9 +372,10 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
       bool nzr = false, nzi = false, nzs = false;
       for (int r = 8 * rb; r < 8 * rb + 8; ++r)
         for (int c = 4 * k; c < 4 * k + 4; ++c) {
-          nzr |= g.m_re[r * D + c] != 0.0;
-          nzi |= g.m_im[r * D + c] != 0.0;
-          nzs |= (g.m_re[r * D + c] + g.m_im[r * D + c]) != 0.0;
+          const int e = g.perm[r] * D + g.perm[c];
+          nzr |= g.m_re[e] != 0.0;
+          nzi |= g.m_im[e] != 0.0;
+          nzs |= (g.m_re[e] + g.m_im[e]) != 0.0;
         }
       const int bit = rb * S::KST + k;
       p.nzblk[0] |= static_cast<uint32_t>(nzr) << bit;
@@ -403,16 +409,17 @@ bool try_dmma_direct(const GateLaunch& g, cudaStream_t s, int num_sms) {
   p.fixed_or = g.fixed_or;
   p.n_masks = g.n_masks;
   for (int i = 0; i < g.n_masks; ++i) p.masks[i] = g.masks[i];
-  for (int j = 0; j < S::D; ++j) p.off[j] = g.off[j];
+  for (int j = 0; j < S::D; ++j) p.off[j] = g.off[g.perm[j]];  // element order of dev_mat
   bool all = true;
   for (int rb = 0; rb < S::RB; ++rb)
     for (int k = 0; k < S::KST; ++k) {
       bool nz[3] = {false, false, false};
       for (int r = 8 * rb; r < 8 * rb + 8; ++r)
         for (int c = 4 * k; c < 4 * k + 4; ++c) {
-          nz[0] |= g.m_re[r * S::D + c] != 0.0;
-          nz[1] |= g.m_im[r * S::D + c] != 0.0;
-          nz[2] |= (g.m_re[r * S::D + c] + g.m_im[r * S::D + c]) != 0.0;
+          const int e = g.perm[r] * S::D + g.perm[c];
+          nz[0] |= g.m_re[e] != 0.0;
+          nz[1] |= g.m_im[e] != 0.0;
+          nz[2] |= (g.m_re[e] + g.m_im[e]) != 0.0;
         }
       for (int m = 0; m < 3; ++m) {
         p.nzblk[m] |= static_cast<uint32_t>(nz[m]) << (rb * S::KST + k);

@@ -48,6 +48,11 @@ struct GateLaunch {
   const double* m_re = nullptr;     // host: snapped sub-matrix, row-major
   const double* m_im = nullptr;
   const void* dev_mat = nullptr;    // device copy for Tile: [D*D re][D*D im] in state precision
+  // Element order of the DMMA kernels: row / column j of dev_mat is row /
+  // column perm[j] of the sub-gate (a qubit reordering chosen on the host so
+  // that zero structure falls into whole 8x4 DMMA tiles).  Identity unless
+  // the full-range DMMA path runs.
+  uint8_t perm[1 << kMaxSub] = {};
 };
 
 // Launch on `stream`; returns the number of kernels enqueued (0 for identity).

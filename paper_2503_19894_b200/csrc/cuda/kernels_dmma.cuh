@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
       const bool use_r = !SPARSE || ((p.nzblk[0] >> bit) & 1u);
       const bool use_i = !SPARSE || ((p.nzblk[1] >> bit) & 1u);
       const bool use_s = !SPARSE || ((p.nzblk[2] >> bit) & 1u);
+      if (SPARSE && !(use_r || use_i || use_s)) continue;  // zero k-step of this row block: no loads either
       double fr, fi, fs;
       if constexpr (MREG) {
         fr = amr[k];

@@ -199,6 +199,11 @@ struct ProgramGate {
   tsg::GateLaunch launch;  // re/im filled per run
   size_t mat_offset = 0;   // into the device arena (tile class)
   bool has_mat = false;
+  // standalone launches of a block-decomposed gate (tilesim::split_blocks);
+  // empty: `launch` applies the gate
+  std::vector<LaunchStructure> sub_ls;
+  std::vector<tsg::GateLaunch> subs;
+  std::vector<size_t> sub_mat;  // arena offset, or SIZE_MAX without a device matrix
   int batch = -1;          // >= 0: first gate of diagonal batch `batch`
   bool in_batch = false;   // applied by an earlier gate's batch launch
 };
@@ -279,6 +284,8 @@ double state_norm(tsg_state* st) {
   return std::sqrt(fetch_sum(st, g));
 }
 
+void choose_dmma_perm(tsg::GateLaunch& g, const LaunchStructure& ls);
+
 // fill a GateLaunch from a plan's launch structure
 tsg::GateLaunch make_launch(const KernelPlan& p, const LaunchStructure& ls) {
   tsg::GateLaunch g;
@@ -299,22 +306,75 @@ tsg::GateLaunch make_launch(const KernelPlan& p, const LaunchStructure& ls) {
   g.g_begin = 0;
   g.g_end = uint64_t{1} << (p.n - p.gate.k());
   g.full_range = true;
+  choose_dmma_perm(g, ls);
   return g;
 }
 
 // Device copy of the snapped sub-matrix for the shared-memory / DMMA kernels:
 // [Mr | Mi | Mr + Mi], D x D each, row-major, FP64 for both state precisions
-// (k_tile reads the first two blocks, k_stream_dmma / k_dmma_direct all three).
-std::vector<unsigned char> tile_matrix_bytes(const LaunchStructure& ls, int /*prec*/) {
+// (k_tile reads the first two blocks, k_stream_dmma / k_dmma_direct all
+// three), rows and columns in the launch's element order (GateLaunch::perm).
+std::vector<unsigned char> tile_matrix_bytes(const LaunchStructure& ls, const tsg::GateLaunch& g) {
   const size_t dd = ls.sub_re.size();
+  const int D = 1 << ls.ks;
   std::vector<unsigned char> out(3 * dd * sizeof(double));
   double* d = reinterpret_cast<double*>(out.data());
-  for (size_t i = 0; i < dd; ++i) {
-    d[i] = ls.sub_re[i];
-    d[dd + i] = ls.sub_im[i];
-    d[2 * dd + i] = ls.sub_re[i] + ls.sub_im[i];
-  }
+  for (int r = 0; r < D; ++r)
+    for (int c = 0; c < D; ++c) {
+      const size_t i = static_cast<size_t>(r) * D + c, e = static_cast<size_t>(g.perm[r]) * D + g.perm[c];
+      d[i] = ls.sub_re[e];
+      d[dd + i] = ls.sub_im[e];
+      d[2 * dd + i] = ls.sub_re[e] + ls.sub_im[e];
+    }
   return out;
+}
+
+// Nonzero 8 x 4 tiles of [Mr | Mi | Mr + Mi] (the DMMA kernels skip the
+// others) with rows / columns in element order P.
+int dmma_tiles(const LaunchStructure& ls, const int* P) {
+  const int D = 1 << ls.ks;
+  int tiles = 0;
+  for (int m = 0; m < 3; ++m)
+    for (int rb = 0; rb < D / 8; ++rb)
+      for (int k = 0; k < D / 4; ++k) {
+        bool nz = false;
+        for (int r = 8 * rb; r < 8 * rb + 8 && !nz; ++r)
+          for (int c = 4 * k; c < 4 * k + 4 && !nz; ++c) {
+            const size_t e = static_cast<size_t>(P[r]) * D + P[c];
+            const double v = m == 0 ? ls.sub_re[e] : (m == 1 ? ls.sub_im[e] : ls.sub_re[e] + ls.sub_im[e]);
+            nz = v != 0.0;
+          }
+        tiles += nz;
+      }
+  return tiles;
+}
+
+// Element order of a launch: identity, except for full-range sub-gates of
+// 3..5 qubits (the DMMA stream kernels), which take the qubit order with the
+// fewest nonzero DMMA tiles (<= 5! orders; ties keep the sorted order).
+// Block-diagonal and tensor-product zero structure then fills whole tiles.
+void choose_dmma_perm(tsg::GateLaunch& g, const LaunchStructure& ls) {
+  const int D = 1 << g.ks;
+  for (int j = 0; j < (1 << tsg::kMaxSub); ++j) g.perm[j] = static_cast<uint8_t>(j < D ? j : 0);
+  if (!g.full_range || (g.klass != 2 && g.klass != 3) || g.ks < 3 || g.ks > 5) return;
+  static const bool disabled = std::getenv("TSG_NO_DMMA_PERM") != nullptr;
+  if (disabled) return;
+  int bits[5] = {0, 1, 2, 3, 4}, P[32], best[32];
+  for (int j = 0; j < D; ++j) best[j] = j;
+  int best_tiles = dmma_tiles(ls, best);
+  do {
+    for (int j = 0; j < D; ++j) {
+      int x = 0;
+      for (int b = 0; b < g.ks; ++b) x |= ((j >> b) & 1) << bits[b];
+      P[j] = x;
+    }
+    const int t = dmma_tiles(ls, P);
+    if (t < best_tiles) {
+      best_tiles = t;
+      std::copy(P, P + D, best);
+    }
+  } while (std::next_permutation(bits, bits + g.ks));
+  for (int j = 0; j < D; ++j) g.perm[j] = static_cast<uint8_t>(best[j]);
 }
 
 bool needs_tile_matrix(const tsg::GateLaunch& g, int prec) {
@@ -371,6 +431,16 @@ void run_step(tsg_state* st, tsg_program* prog, const ProgramStep& step) {
     return;
   }
   const ProgramGate& pg = prog->gates[step.gate];
+  if (!pg.subs.empty()) {
+    for (size_t i = 0; i < pg.subs.size(); ++i) {
+      tsg::GateLaunch g = pg.subs[i];
+      g.re = st->re;
+      g.im = st->im;
+      if (pg.sub_mat[i] != SIZE_MAX) g.dev_mat = arena + pg.sub_mat[i];
+      launch(st, g);
+    }
+    return;
+  }
   tsg::GateLaunch g = pg.launch;
   g.re = st->re;
   g.im = st->im;
@@ -746,6 +816,33 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
       }
       prog->steps.push_back(step);
     }
+    // standalone 5..6-qubit sub-gates with block qubits: one launch per block
+    // (2^-|B| of the state each, 2^|E|-qubit sub-gates off the FP64 roof)
+    if (!std::getenv("TSG_NO_BLOCK_SPLIT"))
+      for (const ProgramStep& step : prog->steps) {
+        if (step.kind != kStepGate) continue;
+        ProgramGate& pg = prog->gates[step.gate];
+        if (pg.ls.ks < 5) continue;
+        std::vector<LaunchStructure> parts = split_blocks(pg.ls, prog->prec);
+        if (parts.size() == 1 && parts[0].ks == pg.ls.ks) continue;
+        pg.sub_ls = std::move(parts);
+        for (const LaunchStructure& sl : pg.sub_ls) {
+          tsg::GateLaunch g = make_launch(pg.plan, sl);
+          size_t off = SIZE_MAX;
+          if (needs_tile_matrix(g, prog->prec)) {
+            const auto bytes = tile_matrix_bytes(sl, g);
+            off = (arena.size() + 255) & ~size_t{255};
+            arena.resize(off + bytes.size());
+            std::copy(bytes.begin(), bytes.end(), arena.begin() + off);
+          }
+          pg.subs.push_back(g);
+          pg.sub_mat.push_back(off);
+        }
+        for (size_t i = 0; i < pg.subs.size(); ++i) {  // host matrices of the (now stable) parts
+          pg.subs[i].m_re = pg.sub_ls[i].sub_re.data();
+          pg.subs[i].m_im = pg.sub_ls[i].sub_im.data();
+        }
+      }
     return;
   }
   if (!std::getenv("TSG_NO_DIAG_BATCH")) plan_diagonal_batches(prog, arena);
@@ -1121,9 +1218,10 @@ int tsg_apply(tsg_state* st, const tsg_plan* pc, const double* matrix_override, 
     g.g_begin = t_begin;
     g.g_end = t_end;
     g.full_range = t_begin == 0 && t_end == groups;
+    choose_dmma_perm(g, ls);
     if (t_begin == t_end) return TSG_OK;
     if (needs_tile_matrix(g, st->prec)) {
-      const auto bytes = tile_matrix_bytes(ls, st->prec);
+      const auto bytes = tile_matrix_bytes(ls, g);
       if (p->dev_mat_bytes < bytes.size()) {
         if (p->dev_mat) ck(cudaFree(p->dev_mat), "cudaFree");
         ck(cudaMalloc(&p->dev_mat, bytes.size()), "cudaMalloc plan matrix");
@@ -1156,7 +1254,7 @@ int tsg_program_create(tsg_ctx* ctx, const tsc_circuit* fused, double zero_tol, 
       pg.ls = precision_bits == 64 ? pg.plan.launch : derive_launch(pg.plan, nullptr, precision_bits);
       pg.launch = make_launch(pg.plan, pg.ls);
       if (needs_tile_matrix(pg.launch, precision_bits)) {
-        const auto bytes = tile_matrix_bytes(pg.ls, precision_bits);
+        const auto bytes = tile_matrix_bytes(pg.ls, pg.launch);
         pg.mat_offset = (arena.size() + 255) & ~size_t{255};
         arena.resize(pg.mat_offset + bytes.size());
         std::copy(bytes.begin(), bytes.end(), arena.begin() + pg.mat_offset);
@@ -1166,10 +1264,16 @@ int tsg_program_create(tsg_ctx* ctx, const tsc_circuit* fused, double zero_tol, 
       prog->gates.push_back(std::move(pg));
     }
     plan_steps(prog.get(), arena);
-    for (const ProgramStep& step : prog->steps) {  // one launch per step
-      ++prog->launches;
+    for (const ProgramStep& step : prog->steps) {  // one launch per step (block splits: one per part)
+      const ProgramGate& pg = prog->gates[step.gate];
+      const bool split = step.kind == kStepGate && !pg.subs.empty();
+      prog->launches += split ? pg.subs.size() : 1;
       prog->bytes += 2 * (uint64_t{1} << prog->n) * amp;
-      const double frac = step.kind != kStepGate ? 1.0 : touched_fraction(prog->gates[step.gate].ls);
+      double frac = step.kind != kStepGate ? 1.0 : touched_fraction(pg.ls);
+      if (split) {
+        frac = 0.0;
+        for (const LaunchStructure& sl : pg.sub_ls) frac += touched_fraction(sl);
+      }
       prog->touched_bytes += static_cast<uint64_t>(2.0 * std::ldexp(1.0, prog->n) * amp * frac);
     }
     if (!arena.empty()) {
@@ -1321,6 +1425,11 @@ int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* ou
       name = "k_pass";
     } else if (st.kind == kStepBatch) {
       name = "k_diag_batch";
+    } else if (!prog->gates[st.gate].subs.empty()) {  // block split: "<part kernel> xN split"
+      const ProgramGate& pg = prog->gates[st.gate];
+      tsg::GateLaunch g = pg.subs[0];
+      if (pg.sub_mat[0] != SIZE_MAX) g.dev_mat = prog->arena;
+      name = tsg::kernel_name(g, prog->prec) + " x" + std::to_string(pg.subs.size()) + " split";
     } else {
       tsg::GateLaunch g = prog->gates[st.gate].launch;
       if (prog->gates[st.gate].has_mat) g.dev_mat = prog->arena;
@@ -1386,7 +1495,7 @@ int tsg_bench_cost_model(tsg_ctx* ctx, int bench_n, int k_max, int precision_bit
           g.re = st->re;
           g.im = st->im;
           if (needs_tile_matrix(g, precision_bits)) {
-            const auto bytes = tile_matrix_bytes(ls, precision_bits);
+            const auto bytes = tile_matrix_bytes(ls, g);
             ck(cudaMemcpy(dev_mat, bytes.data(), bytes.size(), cudaMemcpyHostToDevice), "bench matrix upload");
             g.dev_mat = dev_mat;
           }

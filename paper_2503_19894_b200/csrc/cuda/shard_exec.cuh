@@ -104,7 +104,7 @@ std::unique_ptr<PreparedRank> prepare_rank(const ShardPlan& plan, uint64_t rank,
     po.launch = make_launch(po.plan, po.ls);
     po.skip = po.ls.klass == KernelClass::Identity;
     if (!po.skip && needs_tile_matrix(po.launch, prec)) {
-      const auto bytes = tile_matrix_bytes(po.ls, prec);
+      const auto bytes = tile_matrix_bytes(po.ls, po.launch);
       po.mat_off = (arena.size() + 255) & ~size_t{255};
       arena.resize(po.mat_off + bytes.size());
       std::copy(bytes.begin(), bytes.end(), arena.begin() + po.mat_off);

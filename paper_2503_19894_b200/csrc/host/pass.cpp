@@ -55,6 +55,63 @@ bool monomial(const LaunchStructure& ls) {
   return true;
 }
 
+std::vector<LaunchStructure> split_blocks(const LaunchStructure& ls, int precision_bits) {
+  if (ls.klass != KernelClass::Direct && ls.klass != KernelClass::Tile) return {ls};
+  const std::vector<int> ebits = mixed_bits(ls);
+  if (static_cast<int>(ebits.size()) == ls.ks || ebits.empty()) return {ls};
+  std::vector<int> bbits;
+  for (int b = 0; b < ls.ks; ++b)
+    if (std::find(ebits.begin(), ebits.end(), b) == ebits.end()) bbits.push_back(b);
+  const int ke = static_cast<int>(ebits.size()), nb = static_cast<int>(bbits.size());
+  const int d = 1 << ls.ks, de = 1 << ke;
+  const int direct_max = precision_bits == 64 ? 4 : 5;
+  std::vector<LaunchStructure> out;
+  for (int jb = 0; jb < (1 << nb); ++jb) {
+    LaunchStructure s;
+    s.controls = ls.controls;
+    s.control_values = ls.control_values;
+    int base = 0;
+    for (int i = 0; i < nb; ++i) {
+      const int q = ls.sub_targets[bbits[i]];
+      s.controls.push_back(q);
+      s.control_values |= static_cast<uint64_t>((jb >> i) & 1) << q;
+      base |= ((jb >> i) & 1) << bbits[i];
+    }
+    std::sort(s.controls.begin(), s.controls.end());
+    s.ks = ke;
+    for (int b : ebits) s.sub_targets.push_back(ls.sub_targets[b]);
+    s.offsets.resize(de);
+    std::vector<int> full(de);
+    for (int j = 0; j < de; ++j) {
+      uint64_t q = 0;
+      int f = base;
+      for (int b = 0; b < ke; ++b) {
+        q |= static_cast<uint64_t>((j >> b) & 1) << s.sub_targets[b];
+        f |= ((j >> b) & 1) << ebits[b];
+      }
+      s.offsets[j] = q;
+      full[j] = f;
+    }
+    s.sub_re.resize(de * de);
+    s.sub_im.resize(de * de);
+    bool diagonal = true, identity = true;
+    for (int r = 0; r < de; ++r)
+      for (int c = 0; c < de; ++c) {
+        const double re = ls.sub_re[full[r] * d + full[c]], im = ls.sub_im[full[r] * d + full[c]];
+        s.sub_re[r * de + c] = re;
+        s.sub_im[r * de + c] = im;
+        s.nonzero_scalars += (re != 0.0) + (im != 0.0);
+        if (r != c && (re != 0.0 || im != 0.0)) diagonal = false;
+        if (!(re == (r == c ? 1.0 : 0.0) && im == 0.0)) identity = false;
+      }
+    if (identity) continue;
+    s.klass = diagonal ? KernelClass::Diagonal : (ke <= direct_max ? KernelClass::Direct : KernelClass::Tile);
+    s.sparse = s.nonzero_scalars * 4 <= 3 * static_cast<uint64_t>(2 * de * de);
+    out.push_back(std::move(s));
+  }
+  return out;
+}
+
 PassRole pass_role(const LaunchStructure& ls, const PassConfig& cfg) {
   switch (ls.klass) {
     case KernelClass::Identity: return PassRole::Standalone;

@@ -7,6 +7,8 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("PB_ROOT"):  # a variant build of the package (design experiments)
+    sys.path.insert(0, os.environ["PB_ROOT"])
 import paper_2503_19894_b200 as ts  # noqa: E402
 from tests._util import random_gate_matrix  # noqa: E402
 
@@ -15,9 +17,16 @@ PREC = os.environ.get("PB_PREC", "f64")
 
 
 def case(name, gates):
-    c = ts.Circuit(N)
-    for q, kind in gates:
-        c.add_matrix(sorted(q), random_gate_matrix(len(q), sum(q) * 7 + len(name), kind))
+    if gates == "rqc":  # the 5-qubit fused gates of RQC-n (k <= 5)
+        fused, _ = ts.run_fusion(ts.gen_benchmark("rqc", N, 20, 42), ts.FusionConfig(k_max=5))
+        c = ts.Circuit(N)
+        for g in fused.gates():
+            if g.k == 5:
+                c.add_matrix(g.targets, g.matrix)
+    else:
+        c = ts.Circuit(N)
+        for q, kind in gates:
+            c.add_matrix(sorted(q), random_gate_matrix(len(q), sum(q) * 7 + len(name), kind))
     out = []
     for no_pass in (False, True):
         if no_pass:
@@ -46,6 +55,13 @@ cases = {
     "8x diag T": [([0, 1, 20, 21], "diag")] * 8,
     "8x diag I": [([9, 10, 20, 21], "diag")] * 8,
     "8x diag C": [([22, 23, 24, 25], "diag")] * 8,
+    "ks5 dense 0-4": [([0, 1, 2, 3, 4], "dense")],
+    "ks5 dense 3-7": [([3, 4, 5, 6, 7], "dense")],
+    "ks5 dense 5-9": [([5, 6, 7, 8, 9], "dense")],
+    "ks5 dense 7-11": [([7, 8, 9, 10, 11], "dense")],
+    "ks5 dense 20-24": [([20, 21, 22, 23, 24], "dense")],
+    "ks5 diag-ish 7-11": [([7, 8, 9, 10, 11], "controlled")],
+    "ks5 rqc-like": "rqc",
     "4x perm ks2": [([6, 7], "perm"), ([8, 9], "perm"), ([1, 7], "perm"), ([2, 9], "perm")],
     "4x perm ks4": [([0, 1, 9, 10], "perm"), ([2, 3, 7, 8], "perm"), ([0, 2, 9, 7], "perm"), ([5, 6, 7, 8], "perm")],
 }
