@@ -141,7 +141,7 @@ static_assert(sizeof(PassOp) == 192, "PassOp layout");
 //         group g = tid + 512 k sits at padded offset (et[tid] + ek[k]) & 0xffff
 //         and uses block ((et[tid] + ek[k]) >> 16) | (bits from the tile
 //         base); then at aux_off the 2^nb blocks, 2^ks x 2^ks {re, im}
-//         row-major each
+//         row-major each plus one padding entry (block stride 4^ks + 1)
 //   Perm  as GEN up to aux_off; there, per block: src[2^ks] u32 (padded
 //         offset of the source element of each row; 16-byte block) and
 //         val[2^ks] {re, im}

@@ -120,7 +120,8 @@ __device__ __forceinline__ void pass_gen(const PassOp& op, const unsigned char* 
   for (uint32_t g = tid; g < (RSPLIT > 1 ? uint32_t(kPassThreads) : n_groups); g += kPassThreads, ++k) {
     const uint32_t e = e0 + ek[k];
     const uint32_t a = e & 0xffffu;
-    const R2* mat = blocks + ((e >> 16) | jo) * (D * D) + r0 * D;
+    // blocks are D*D + 1 entries apart: lanes reading different blocks hit different banks
+    const R2* mat = blocks + ((e >> 16) | jo) * (D * D + 1) + r0 * D;
     Real vr[D], vi[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
@@ -418,41 +419,46 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
       if (i < p.n_tmask) b += (tile & p.tmask[i]) << i;
     return b << L;
   };
-  // this thread's chunks: (global element offset within the tile, stage offset)
-  uint32_t c_run[C::kPerThread], c_off[C::kPerThread];
+  // this thread's chunks: array, global element offset within the tile, stage offset
+  Real* c_arr[C::kPerThread];
+  uint64_t c_gofs[C::kPerThread];
+  uint32_t c_off[C::kPerThread];
 #pragma unroll
   for (int q = 0; q < C::kPerThread; ++q) {
     const int c = tid + q * kPassThreads;
     const int arr = c / C::kChunksPerArray;
     const int e = (c % C::kChunksPerArray) * C::kEpc;
-    c_run[q] = static_cast<uint32_t>(e >> L);
+    c_arr[q] = arr ? gim : gre;
+    c_gofs[q] = roff[e >> L] + (e & (S::kRunLen - 1));
     c_off[q] = static_cast<uint32_t>(arr * S::kStageElems + (e >> L) * S::kStride + (e & (S::kRunLen - 1)));
   }
-  auto c_global = [&](int q, uint64_t base) -> Real* {
-    const int c = tid + q * kPassThreads;
-    Real* g = c < C::kChunksPerArray ? gre : gim;
-    const int e = (c % C::kChunksPerArray) * C::kEpc;
-    return g + base + roff[c_run[q]] + (e & (S::kRunLen - 1));
-  };
   const uint64_t first = blockIdx.x, step = gridDim.x;
-  // bases of the tiles in flight, computed once at prefetch (ring, oldest first)
+  // Tile bases of the prefetch stream, stepped in the masked domain: with
+  // the non-tile bits forced to 1, adding deposit(step) carries across them
+  // (pdep(t + s) = ((pdep(t) | ~mask) + pdep(s)) & mask).
+  const uint64_t tmask_all = tile_base(p.n_tiles - 1);  // every tile-id bit position
+  const uint64_t dstep = tile_base(step);
+  uint64_t pbase = tile_base(first);
+  // bases of the tiles in flight (ring, oldest first)
   uint64_t ring[STAGES];
-  auto prefetch = [&](uint64_t tile, int s) {
+  uint64_t ptile = first;
+  auto prefetch = [&](int s) {
 #pragma unroll
     for (int r = 0; r + 1 < STAGES; ++r) ring[r] = ring[r + 1];
-    if (tile < p.n_tiles) {
-      const uint64_t base = tile_base(tile);
-      ring[STAGES - 1] = base;
+    if (ptile < p.n_tiles) {
+      ring[STAGES - 1] = pbase;
       Real* st = buf + (2 * s) * S::kStageElems;
 #pragma unroll
-      for (int q = 0; q < C::kPerThread; ++q) cp_async16(st + c_off[q], c_global(q, base));
+      for (int q = 0; q < C::kPerThread; ++q) cp_async16(st + c_off[q], c_arr[q] + pbase + c_gofs[q]);
     }
     cp_async_commit();  // one group per tile slot, empty past the end
+    ptile += step;
+    pbase = ((pbase | ~tmask_all) + dstep) & tmask_all;
   };
 #pragma unroll
   for (int s = 0; s < STAGES; ++s) ring[s] = 0;
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) prefetch(first + s * step, s);
+  for (int s = 0; s < STAGES - 1; ++s) prefetch(s);
 
   uint32_t j = 0;
   for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
     }
     cp_async_wait<STAGES - 2>();  // this thread's chunks of tile j have landed
     consumer_bar();               // ... and everyone's; the stage of tile j - 1 is stored
-    prefetch(tile + (STAGES - 1) * step, static_cast<int>((j + STAGES - 1) % STAGES));
+    prefetch(static_cast<int>((j + STAGES - 1) % STAGES));
     Real* xr = buf + (2 * s) * S::kStageElems;
     Real* xi = xr + S::kStageElems;
     int o = 0;
@@ -504,7 +510,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
     const Real* st = buf + (2 * s) * S::kStageElems;
 #pragma unroll
     for (int q = 0; q < C::kPerThread; ++q)
-      *reinterpret_cast<uint4*>(c_global(q, tbase)) = *reinterpret_cast<const uint4*>(st + c_off[q]);
+      *reinterpret_cast<uint4*>(c_arr[q] + tbase + c_gofs[q]) = *reinterpret_cast<const uint4*>(st + c_off[q]);
   }
   cp_async_wait<0>();
 }

@@ -700,12 +700,14 @@ tsg::PassOp build_pass_op(const LaunchStructure& ls, const std::vector<int>& pos
     }
     return op;
   }
-  for (int jb = 0; jb < (1 << nb); ++jb)
+  for (int jb = 0; jb < (1 << nb); ++jb) {
     for (int r = 0; r < de; ++r)
       for (int c = 0; c < de; ++c) {
         const int e = full_index(r, jb) * d + full_index(c, jb);
         append_real2<Real>(data, ls.sub_re[e], ls.sub_im[e]);
       }
+    append_real2<Real>(data, 0.0, 0.0);  // bank padding between blocks
+  }
   return op;
 }
 

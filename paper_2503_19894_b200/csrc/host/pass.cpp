@@ -136,7 +136,7 @@ int pass_op_bytes(const LaunchStructure& ls, const PassConfig& cfg) {
     const int ke = static_cast<int>(mixed_bits(ls).size());
     const int d = 1 << ke, blocks = 1 << (ls.ks - ke);
     const int groups = 1 << std::max(0, cfg.tile_log2 - ke);  // upper bound: controls may fall outside the tile
-    const int block_bytes = monomial(ls) ? ((4 * d + 15) & ~15) + d * cplx : d * d * cplx;
+    const int block_bytes = monomial(ls) ? ((4 * d + 15) & ~15) + d * cplx : (d * d + 1) * cplx;
     data = ((4 * d + 15) & ~15) + 4 * kThreads + 4 * std::max(1, groups / kThreads) + 16 + blocks * block_bytes;
   }
   return kPassOpRecord + ((data + 15) & ~15);
