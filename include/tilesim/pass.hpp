@@ -24,7 +24,7 @@ struct PassConfig {
   int run_log2 = 5;      // L: contiguous run length = 2^L (>= 256 bytes per array)
   int max_ops = 96;      // ops per pass
   int max_gen_ks = 4;    // widest non-diagonal sub-gate inside a pass
-  int max_blob = 56 * 1024;  // bytes of run offsets + op table + op data
+  int max_blob = 36 * 1024;  // bytes of run offsets + op table + op data
   int amp_real_bytes = 8;    // sizeof(Real) of the state
   // B200 cost model of a pass, in units of one state sweep (2 * 2^n * B_amp
   // bytes at HBM speed), measured with scripts/pass_bench.py at n = 28
@@ -33,8 +33,10 @@ struct PassConfig {
   // (touched share for controlled gates).
   double base_sweeps = 1.3;
   double diag_sweeps = 0.08;
-  double gen_sweeps[6] = {0.0, 0.45, 0.55, 0.8, 1.4, 2.0};
-  double perm_sweeps = 0.2;
+  double gen_sweeps[6] = {0.0, 0.45, 0.55, 0.8, 1.4, 2.0};  // through shared memory
+  double perm_sweeps = 0.45;
+  int reg_bits = 3;             // register positions a register op may mix (2^M / 256 amplitudes per thread)
+  double reg_gen_sweeps = 0.3;  // an op on register positions, with its share of layout changes
   double standalone_sweeps = 1.08;
   // testing: every eligible gate joins (no cost test, single-gate passes allowed);
   // pass_config() sets it when the environment has TSG_PASS_FORCE=1

@@ -91,60 +91,81 @@ std::string kernel_name(const GateLaunch& g, int precision_bits);
 // non-control sub-targets are tile qubits (GEN op) or when it is diagonal
 // (DIAG op: out-of-tile targets and controls are constants of the tile).
 // Tile coordinates: position p < L is qubit p; position L + h is high[h].
-constexpr int kPassThreads = 512;   // consumer threads (16 warps) + 1 producer warp
-constexpr int kPassLogThreads = 9;
+constexpr int kPassThreads = 256;  // threads per CTA, two CTAs per SM
+constexpr int kPassLogThreads = 8;
 constexpr int kPassMaxOps = 128;  // ops + RUN headers per pass
-constexpr int kPassMaxBlob = 56 * 1024;  // run offsets + op table + op data, staged in smem
+constexpr int kPassMaxBlob = 36 * 1024;  // run offsets + op table + op data, staged in smem
 constexpr int kPassPadBytes = 32;        // padding between runs in shared memory (bank spread)
 
-// Op kinds.  GEN ops mix 2^ks amplitudes (ks = mixed qubits, all tile
-// qubits) with one of 2^nb blocks selected by the block qubits
-// (tilesim::mixed_bits).  A RUN header precedes every maximal run of
-// consecutive diagonal ops; the run's ops are ordered by class (diagonal
-// gates commute), each class by where its in-tile bits sit relative to the
-// consumer's amplitude map x = tid + i * kPassThreads:
-//   DiagT  in-tile bits only on thread-id positions (or none): one factor per
-//          thread and tile
-//   DiagI  in-tile bits only on iteration positions: one factor per i,
-//          shared by all threads of the tile
-//   DiagX  both: a table lookup per amplitude
-//   Perm   a GEN op whose blocks are monomial (one nonzero per row: X, CX,
-//          SWAP, CCX, permutations with phases): a gather and one complex
-//          multiply per amplitude instead of a dense product
-enum PassOpKind : int32_t { kPassRun = 0, kPassDiagT = 1, kPassDiagI = 2, kPassDiagX = 3, kPassGen = 4, kPassPerm = 5 };
+// Register layouts.  Each consumer thread holds R = 2^r = 2^M / kPassThreads
+// amplitudes of the tile in registers: a LAYOUT op picks r "register" tile
+// positions P; thread tid holds x = deposit(tid over the other positions) |
+// deposit(i over P), i < R.  Ops run on those registers; only a layout
+// change or a wide op moves the tile through shared memory.
+//   Layout  store the registers (old layout), barrier, load the new layout
+//   Run     header of a run of diagonal ops, ordered by class w.r.t. the
+//           current layout (diagonal gates commute):
+//     DiagT  in-tile index bits only on thread positions: one factor per thread
+//     DiagI  only on register positions: one factor per register index i,
+//            shared through shared memory
+//     DiagX  both: a table lookup per amplitude
+//   RGen    sub-gate whose mixed qubits are register positions (rmask): in
+//           registers, one block (tilesim::mixed_bits) per sub-group
+//   RPerm   RGen whose blocks are monomial (one nonzero per row: X, CX, SWAP,
+//           permutations with phases): a select and one complex multiply
+//   SGen / SPerm  mixed qubits not all register positions (or more than r):
+//           through shared memory, one thread (or a row split) per group
+enum PassOpKind : int32_t {
+  kPassLayout = 0,
+  kPassRun = 1,
+  kPassDiagT = 2,
+  kPassDiagI = 3,
+  kPassDiagX = 4,
+  kPassRGen = 5,
+  kPassRPerm = 6,
+  kPassSGen = 7,
+  kPassSPerm = 8,
+};
 
 struct PassOp {  // 192 bytes, built on the host, read from shared memory
   int32_t kind;
-  int32_t ks;           // DIAG: table bits; GEN: mixed qubits; RUN: number of DiagT ops
+  int32_t ks;           // DIAG: table bits; GEN / PERM: mixed qubits; RUN: number of DiagT ops
   int32_t data_off;     // byte offset of the op's data in the blob
   int32_t n_out;        // table / block index bits taken from the tile base (out_gbit -> out_jbit)
-  int32_t log2_groups;  // GEN: groups per tile (when < kPassThreads, 2^log2_rsplit threads share a group)
-  int32_t run_i;        // RUN: number of DiagI ops
-  int32_t run_x;        // RUN: number of DiagX ops
-  int32_t aux_off;      // DiagT / DiagX: thread table offset; GEN: offset of the blocks
-  uint32_t ictl_mask, ictl_val;  // DIAG: controls on the iteration bits
-  int32_t log2_rsplit;  // GEN: the group's output rows are split over 2^log2_rsplit threads
-  uint32_t pad;
+  int32_t log2_groups;  // SGen / SPerm: groups per tile; RUN: number of DiagI ops
+  int32_t log2_rsplit;  // SGen / SPerm: rows of a group split over 2^log2_rsplit threads; RUN: number of DiagX ops
+  int32_t aux_off;      // DiagT / DiagX: thread table; GEN / PERM: blocks
+  int32_t rmask;        // RGen / RPerm: mixed bits among the register bits
+  uint32_t ictl_mask, ictl_val;  // controls on register bits (DIAG, RGen, RPerm)
+  uint32_t tctl_mask, tctl_val;  // RGen / RPerm: controls on thread positions (tile coordinates)
   uint64_t cout_mask, cout_val;  // controls outside the tile (global bits)
   uint8_t out_gbit[8], out_jbit[8];
-  uint32_t dep[8];  // DIAG: table-index bits set by iteration bit k
-  uint8_t reserved[80];
+  uint32_t dep[8];    // DIAG: table bits per register bit; RGen / RPerm: block bits per register bit;
+                      // LAYOUT: padded shared-memory offset of register position k
+  uint32_t xmask[6];  // LAYOUT: insertion masks, thread id -> thread positions (zeros at P; r + 1 <= 6)
+  uint8_t tb_pos[8], tb_jbit[8];  // RGen / RPerm: block bits on thread positions
+  int32_t n_tb;
+  int32_t n_xmask;
+  uint8_t reserved[32];
 };
 static_assert(sizeof(PassOp) == 192, "PassOp layout");
 
 // Blob: [run offsets: 2^(M-L) x u64][PassOp x n_ops][op data].  Op data:
-//   DIAG  table[2^ks + 1] {re, im} (state precision; the last entry is 1 and
-//         stands in for inactive controls); DiagT / DiagX also thr[512] u8 at
-//         aux_off: table-index bits on thread-id positions, 0xff when the
-//         controls on thread-id positions are inactive for that thread
-//   GEN   soff[2^ks] u32 (16-byte block), et[512] u32, ek[max(1, groups/512)] u32:
-//         group g = tid + 512 k sits at padded offset (et[tid] + ek[k]) & 0xffff
-//         and uses block ((et[tid] + ek[k]) >> 16) | (bits from the tile
-//         base); then at aux_off the 2^nb blocks, 2^ks x 2^ks {re, im}
-//         row-major each plus one padding entry (block stride 4^ks + 1)
-//   Perm  as GEN up to aux_off; there, per block: src[2^ks] u32 (padded
-//         offset of the source element of each row; 16-byte block) and
-//         val[2^ks] {re, im}
+//   DIAG   table[2^ks + 1] {re, im} (state precision; the last entry is 1 and
+//          stands in for inactive controls); DiagT / DiagX also thr[256] u8
+//          at aux_off: table-index bits on thread positions, 0xff when the
+//          controls on thread positions are inactive for that thread
+//   RGen   at aux_off the 2^nb blocks, 2^ks x 2^ks {re, im} row-major, one
+//          padding entry after each block (stride 4^ks + 1)
+//   RPerm  at aux_off per block: src[2^ks] u32 (element index of the source
+//          of row r; 16-byte block) and val[2^ks] {re, im}
+//   SGen   soff[2^ks] u32 (16-byte block), et[256] u32, ek[max(1, groups/256)] u32:
+//          group g = tid + 256 k sits at padded offset (et[tid] + ek[k]) & 0xffff
+//          and uses block ((et[tid] + ek[k]) >> 16) | (bits from the tile base);
+//          then the blocks as for RGen
+//   SPerm  as SGen up to aux_off; there, per block: src[2^ks] u32 (padded
+//          offset of the source element of each row; 16-byte block) and
+//          val[2^ks] {re, im}
 struct PassLaunch {
   int n = 0;          // state qubits
   int tile_log2 = 0;  // M

@@ -68,10 +68,10 @@ struct PassShape {
   static constexpr int kRunLen = 1 << L;
   static constexpr int kStride = kRunLen + kPassPadBytes / static_cast<int>(sizeof(Real));
   static constexpr int kStageElems = kRuns * kStride;
-  static constexpr int kIter = (1 << M) / kPassThreads;  // amplitudes per thread in RUN ops
+  static constexpr int kIter = (1 << M) / kPassThreads;  // amplitudes per thread (register layout)
   static constexpr int kIterBits = M - kPassLogThreads;
   static_assert(kIter >= 1 && kIterBits <= 8, "tile / thread geometry");
-  static constexpr size_t kFiBytes = 2 * kIter * 2 * sizeof(Real);       // DiagI factors, double-buffered by tile
+  static constexpr size_t kFiBytes = 2 * kIter * 2 * sizeof(Real);       // DiagI factors, double-buffered
   static constexpr size_t kTcBytes = 2 * kPassMaxOps * sizeof(uint32_t);  // per-tile op constants, double-buffered
   static constexpr size_t smem_bytes(int blob_bytes, int stages) {
     return ((static_cast<size_t>(blob_bytes) + 127) & ~size_t{127}) +
@@ -212,9 +212,9 @@ template <typename Real, int KS, int M, int L>
 __device__ __forceinline__ void pass_perm_split(const PassOp& op, const unsigned char* blob, uint32_t jo, Real* xr,
                                                 Real* xi, int tid) {
   constexpr int D = 1 << KS;
-  switch (op.log2_rsplit) {  // KS >= 4 always has a row split (see pass_gen_split)
+  switch (op.log2_rsplit) {  // see pass_gen_split
     case 0:
-      if constexpr (KS <= 3) pass_perm<Real, KS, M, L, 1>(op, blob, jo, xr, xi, tid);
+      if constexpr (KS <= 3 || (KS == 4 && sizeof(Real) == 4)) pass_perm<Real, KS, M, L, 1>(op, blob, jo, xr, xi, tid);
       break;
     case 1:
       if constexpr (D >= 2) pass_perm<Real, KS, M, L, 2>(op, blob, jo, xr, xi, tid);
@@ -232,10 +232,11 @@ template <typename Real, int KS, int M, int L>
 __device__ __forceinline__ void pass_gen_split(const PassOp& op, const unsigned char* blob, uint32_t jo, Real* xr,
                                                Real* xi, int tid) {
   constexpr int D = 1 << KS;
-  // tiles hold <= 2^12 amplitudes, so KS >= 4 always has < kPassThreads groups and a row split
+  // Without a row split only KS <= 3, or KS = 4 in complex64 (2^12-amplitude
+  // tiles: 256 groups for 256 threads); complex128 tiles (2^11) always split KS >= 4.
   switch (op.log2_rsplit) {
     case 0:
-      if constexpr (KS <= 3) pass_gen<Real, KS, M, L, 1>(op, blob, jo, xr, xi, tid);
+      if constexpr (KS <= 3 || (KS == 4 && sizeof(Real) == 4)) pass_gen<Real, KS, M, L, 1>(op, blob, jo, xr, xi, tid);
       break;
     case 1:
       if constexpr (D >= 2) pass_gen<Real, KS, M, L, 2>(op, blob, jo, xr, xi, tid);
@@ -252,7 +253,7 @@ __device__ __forceinline__ void pass_gen_split(const PassOp& op, const unsigned 
 template <typename Real, int M, int L>
 __device__ __forceinline__ void pass_gen_dispatch(const PassOp& op, const unsigned char* blob, uint32_t jo, Real* xr,
                                                   Real* xi, int tid) {
-  if (op.kind == kPassPerm) {
+  if (op.kind == kPassSPerm) {
     switch (op.ks) {
       case 1: pass_perm_split<Real, 1, M, L>(op, blob, jo, xr, xi, tid); break;
       case 2: pass_perm_split<Real, 2, M, L>(op, blob, jo, xr, xi, tid); break;
@@ -275,6 +276,97 @@ __device__ __forceinline__ void pass_gen_dispatch(const PassOp& op, const unsign
   }
 }
 
+// ---------------------------------------------------------- register ops
+// compile-time deposit of the bits of j into the set bits of mask
+__host__ __device__ constexpr int deposit_c(int j, int mask) {
+  int out = 0;
+  for (int b = 0, k = 0; b < 8; ++b)
+    if ((mask >> b) & 1) out |= ((j >> k++) & 1) << b;
+  return out;
+}
+
+// RGen / RPerm on the thread's R registers: the op mixes register bits RM;
+// sub-group s (register index with the RM bits clear) uses block
+// tc | thread-position block bits | register block bits of s.
+template <typename Real, int R, int RM, bool PERM>
+__device__ __forceinline__ void reg_gen(const PassOp& op, const unsigned char* blob, uint32_t tc, uint32_t xt,
+                                        Real (&ar)[R], Real (&ai)[R]) {
+  using R2 = typename Real2Of<Real>::T;
+  constexpr int KE = __builtin_popcount(RM);
+  constexpr int D = 1 << KE;
+  if ((xt & op.tctl_mask) != op.tctl_val) return;
+  uint32_t jt = tc;
+  for (int b = 0; b < op.n_tb; ++b) jt |= ((xt >> op.tb_pos[b]) & 1u) << op.tb_jbit[b];
+  const unsigned char* blocks = blob + op.aux_off;
+  constexpr int kSrcBytes = (4 * D + 15) & ~15;
+  constexpr int kBlockBytes = PERM ? kSrcBytes + D * static_cast<int>(sizeof(R2)) : (D * D + 1) * static_cast<int>(sizeof(R2));
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    if (s & RM) continue;  // compile time
+    if ((static_cast<uint32_t>(s) & op.ictl_mask) != op.ictl_val) continue;
+    uint32_t jb = jt;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if ((R >> k) > 1 && ((s >> k) & 1)) jb |= op.dep[k];
+    const unsigned char* blk = blocks + jb * kBlockBytes;
+    Real vr[D], vi[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      vr[j] = ar[s | deposit_c(j, RM)];
+      vi[j] = ai[s | deposit_c(j, RM)];
+    }
+    if constexpr (PERM) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(blk);
+      const R2* val = reinterpret_cast<const R2*>(blk + kSrcBytes);
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const uint32_t c = src[r];
+        Real xr = vr[0], xi = vi[0];
+#pragma unroll
+        for (int q = 1; q < D; ++q)
+          if (c == static_cast<uint32_t>(q)) {
+            xr = vr[q];
+            xi = vi[q];
+          }
+        const R2 m = val[r];
+        ar[s | deposit_c(r, RM)] = fma(-m.y, xi, m.x * xr);  // k_direct's order for one nonzero entry
+        ai[s | deposit_c(r, RM)] = fma(m.y, xr, m.x * xi);
+      }
+    } else {
+      const R2* mat = reinterpret_cast<const R2*>(blk);
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        Real yr = Real(0), yi = Real(0);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const R2 m = mat[r * D + c];
+          yr = fma(m.x, vr[c], yr);  // k_direct's order
+          yi = fma(m.x, vi[c], yi);
+          yr = fma(-m.y, vi[c], yr);
+          yi = fma(m.y, vr[c], yi);
+        }
+        ar[s | deposit_c(r, RM)] = yr;
+        ai[s | deposit_c(r, RM)] = yi;
+      }
+    }
+  }
+}
+
+// rmask: mixed bits among the r register bits (at most 3 of them)
+template <typename Real, int R, bool PERM, int RM = 1>
+__device__ __forceinline__ void reg_gen_dispatch(const PassOp& op, const unsigned char* blob, uint32_t tc, uint32_t xt,
+                                                 Real (&ar)[R], Real (&ai)[R]) {
+  if constexpr (RM < R) {
+    if constexpr (__builtin_popcount(RM) <= 3) {
+      if (op.rmask == RM) {
+        reg_gen<Real, R, RM, PERM>(op, blob, tc, xt, ar, ai);
+        return;
+      }
+    }
+    reg_gen_dispatch<Real, R, PERM, RM + 1>(op, blob, tc, xt, ar, ai);
+  }
+}
+
 // --------------------------------------------------------------------- RUN
 template <typename Real>
 __device__ __forceinline__ typename Real2Of<Real>::T diag_entry(const PassOp& op, const unsigned char* blob,
@@ -283,15 +375,13 @@ __device__ __forceinline__ typename Real2Of<Real>::T diag_entry(const PassOp& op
 }
 
 // The RUN header at ops[o] is followed by nT DiagT, nI DiagI and nX DiagX
-// ops.  Returns the index of the op after the run.
-template <typename Real, int M, int L>
+// ops (classes w.r.t. the current layout).  Returns the op after the run.
+template <typename Real, int R>
 __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const unsigned char* blob, const uint32_t* tcs,
-                                             int tid, Real (&ar)[PassShape<Real, M, L>::kIter],
-                                             Real (&ai)[PassShape<Real, M, L>::kIter],
-                                             typename Real2Of<Real>::T* fi_tab) {
-  using S = PassShape<Real, M, L>;
+                                             int tid, Real (&ar)[R], Real (&ai)[R], typename Real2Of<Real>::T* fi_tab) {
   using R2 = typename Real2Of<Real>::T;
-  const int nT = ops[o].ks, nI = ops[o].run_i, nX = ops[o].run_x;
+  constexpr int kBits = __builtin_ctz(R);
+  const int nT = ops[o].ks, nI = ops[o].log2_groups, nX = ops[o].log2_rsplit;
   ++o;
   // DiagT: one factor per thread (the loads of consecutive ops are independent)
   Real ftr = Real(1), fti = Real(0);
@@ -305,9 +395,9 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
     cmul_acc(ftr, fti, d.x, d.y);
   }
   o += nT;
-  // DiagI: factor of iteration i = tid, computed by threads tid < kIter
+  // DiagI: factor of register index i = tid, computed by threads tid < R
   if (nI > 0) {
-    if (tid < S::kIter) {
+    if (tid < R) {
       Real fir = Real(1), fii = Real(0);
 #pragma unroll 4
       for (int t = 0; t < nI; ++t) {
@@ -315,7 +405,7 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
         const uint32_t tc = tcs[o + t];
         uint32_t j = tc;
 #pragma unroll
-        for (int k = 0; k < S::kIterBits; ++k)
+        for (int k = 0; k < kBits; ++k)
           if ((tid >> k) & 1) j |= op.dep[k];
         const bool act = (static_cast<uint32_t>(tid) & op.ictl_mask) == op.ictl_val;
         const R2 d = diag_entry<Real>(op, blob, min(act ? j : ~0u, 1u << op.ks));
@@ -332,15 +422,15 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
     const uint32_t tv = blob[op.aux_off + tid];
     if ((tc >> 31) || tv == 0xffu) continue;
     const uint32_t jc = tc | tv;
-    uint32_t dep[S::kIterBits];
+    uint32_t dep[kBits > 0 ? kBits : 1];
 #pragma unroll
-    for (int k = 0; k < S::kIterBits; ++k) dep[k] = op.dep[k];
+    for (int k = 0; k < kBits; ++k) dep[k] = op.dep[k];
     const uint32_t im = op.ictl_mask, iv = op.ictl_val, one = 1u << op.ks;
 #pragma unroll
-    for (int i = 0; i < S::kIter; ++i) {
+    for (int i = 0; i < R; ++i) {
       uint32_t j = jc;
 #pragma unroll
-      for (int k = 0; k < S::kIterBits; ++k)
+      for (int k = 0; k < kBits; ++k)
         if ((i >> k) & 1) j |= dep[k];
       const R2 d = diag_entry<Real>(op, blob, (static_cast<uint32_t>(i) & im) == iv ? j : one);
       const Real r0 = ar[i], i0 = ai[i];
@@ -351,7 +441,7 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
   if (nI > 0) {  // uniform: every consumer thread read the same header
     consumer_bar();
 #pragma unroll
-    for (int i = 0; i < S::kIter; ++i) {
+    for (int i = 0; i < R; ++i) {
       const R2 f = fi_tab[i];
       Real gr = ftr, gi = fti;
       cmul_acc(gr, gi, f.x, f.y);
@@ -359,7 +449,7 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
     }
   } else if (nT > 0) {
 #pragma unroll
-    for (int i = 0; i < S::kIter; ++i) cmul_acc(ar[i], ai[i], ftr, fti);
+    for (int i = 0; i < R; ++i) cmul_acc(ar[i], ai[i], ftr, fti);
   }
   return o;
 }
@@ -389,7 +479,7 @@ struct PassCopy {
 };
 
 template <typename Real, int M, int L, int STAGES>
-__global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant__ PassParams p) {
+__global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant__ PassParams p) {
   using S = PassShape<Real, M, L>;
   using C = PassCopy<Real, M, L>;
   using R2 = typename Real2Of<Real>::T;
@@ -460,6 +550,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) prefetch(s);
 
+  constexpr int R = S::kIter;  // amplitudes per thread (register layout)
+  Real ar[R], ai[R];
+  uint32_t at[R];      // padded shared-memory offsets of the registers (current layout)
+  uint32_t xt = 0;     // tile coordinate of the thread part of the current layout
+  uint32_t irun = 0;   // runs with DiagI ops so far (fi_tab double-buffering)
   uint32_t j = 0;
   for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
     const int s = static_cast<int>(j % STAGES);
@@ -480,30 +575,84 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
     prefetch(static_cast<int>((j + STAGES - 1) % STAGES));
     Real* xr = buf + (2 * s) * S::kStageElems;
     Real* xi = xr + S::kStageElems;
-    int o = 0;
-    while (o < p.n_ops) {
-      if (o > 0) consumer_bar();  // the previous op's writes are visible to every consumer
+    // The op list starts with a LAYOUT op; registers hold the tile from then
+    // on.  `in_smem`: the registers have been stored (shared memory is current).
+    bool in_smem = true;
+    for (int o = 0; o < p.n_ops;) {
       const PassOp& op = ops[o];
-      if (op.kind == kPassRun) {
-        Real ar[S::kIter], ai[S::kIter];
+      const int kind = op.kind;
+      if (kind == kPassLayout) {
+        if (!in_smem) {
 #pragma unroll
-        for (int i = 0; i < S::kIter; ++i) {
-          const uint32_t a = pass_addr<L, S::kStride>(static_cast<uint32_t>(tid + i * kPassThreads));
+          for (int i = 0; i < R; ++i) {
+            xr[at[i]] = ar[i];
+            xi[at[i]] = ai[i];
+          }
+          consumer_bar();  // the tile is in shared memory in full
+        } else if (o > 0) {
+          consumer_bar();  // after shared-memory ops: their writes are visible
+        }
+        xt = 0;
+        for (int m = 0; m < op.n_xmask; ++m) xt += (static_cast<uint32_t>(tid) & op.xmask[m]) << m;
+        const uint32_t at0 = pass_addr<L, S::kStride>(xt);
+        constexpr int kBits = __builtin_ctz(R);
+        uint32_t pd[kBits];  // padded offset of each register position (additive over disjoint bits)
+#pragma unroll
+        for (int k = 0; k < kBits; ++k) pd[k] = op.dep[k];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          uint32_t a = at0;
+#pragma unroll
+          for (int k = 0; k < kBits; ++k)
+            if ((i >> k) & 1) a += pd[k];
+          at[i] = a;
           ar[i] = xr[a];
           ai[i] = xi[a];
         }
-        o = pass_diag_run<Real, M, L>(ops, o, blob, tcs, tid, ar, ai, fi_tab + (j & 1) * S::kIter);
-#pragma unroll
-        for (int i = 0; i < S::kIter; ++i) {
-          const uint32_t a = pass_addr<L, S::kStride>(static_cast<uint32_t>(tid + i * kPassThreads));
-          xr[a] = ar[i];
-          xi[a] = ai[i];
+        in_smem = false;
+        ++o;
+      } else if (kind == kPassRun) {
+        // DiagI factors alternate buffers run by run (each such run has a barrier)
+        const bool has_i = op.log2_groups > 0;
+        o = pass_diag_run<Real, R>(ops, o, blob, tcs, tid, ar, ai, fi_tab + (irun & 1) * R);
+        irun += has_i;
+      } else if (kind == kPassRGen || kind == kPassRPerm) {
+        const uint32_t tc = tcs[o];
+        if (!(tc >> 31)) {
+          if (kind == kPassRPerm) reg_gen_dispatch<Real, R, true>(op, blob, tc, xt, ar, ai);
+          else reg_gen_dispatch<Real, R, false>(op, blob, tc, xt, ar, ai);
         }
-      } else {
+        ++o;
+      } else {  // SGen / SPerm: through shared memory
+        if (!in_smem) {
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            xr[at[i]] = ar[i];
+            xi[at[i]] = ai[i];
+          }
+          in_smem = true;
+        }
+        consumer_bar();
         // the skip is tile-uniform, so a row-split op's internal barrier stays uniform
         const uint32_t tc = tcs[o];
         if (!(tc >> 31)) pass_gen_dispatch<Real, M, L>(op, blob, tc, xr, xi, tid);
         ++o;
+        if (o < p.n_ops && ops[o].kind != kPassSGen && ops[o].kind != kPassSPerm && ops[o].kind != kPassLayout) {
+          consumer_bar();  // back to the registers of the current layout
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            ar[i] = xr[at[i]];
+            ai[i] = xi[at[i]];
+          }
+          in_smem = false;
+        }
+      }
+    }
+    if (!in_smem) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        xr[at[i]] = ar[i];
+        xi[at[i]] = ai[i];
       }
     }
     consumer_bar();  // all ops done: write the tile back

@@ -1,7 +1,8 @@
 // Launchers of the tile-pass kernel (kernels_pass.cuh) for both precisions.
 //   complex128: tiles of 2^11 amplitudes, runs of 2^5  (32 KiB + 4 KiB pad per stage)
 //   complex64 : tiles of 2^12 amplitudes, runs of 2^6  (32 KiB + 4 KiB pad per stage)
-// Four stages per CTA keep three tiles (~110 KB) of loads in flight per SM.
+// Two CTAs of 256 threads per SM, two stages each: while one CTA's barriers
+// hold its warps, the other's compute or copy.
 #include <algorithm>
 #include <stdexcept>
 #include <string>
@@ -18,7 +19,7 @@ void pass_check(cudaError_t e, const char* what) {
 template <typename Real, int M, int L>
 int launch_pass_impl(const PassLaunch& pl, cudaStream_t s, int num_sms) {
   using S = PassShape<Real, M, L>;
-  constexpr int kStages = 4;
+  constexpr int kStages = 2;
   if (pl.tile_log2 != M || pl.run_log2 != L) throw std::runtime_error("pass geometry does not match the kernel");
   if (pl.n < M) throw std::runtime_error("state smaller than one pass tile");
   if (pl.blob_bytes % 16 != 0 || pl.blob_bytes > kPassMaxBlob) throw std::runtime_error("pass blob size");

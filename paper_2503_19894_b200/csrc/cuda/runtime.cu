@@ -533,100 +533,239 @@ void append_pod(std::vector<unsigned char>& v, const T& x) {
   v.insert(v.end(), b, b + sizeof(T));
 }
 
-// Tile-pass op record + data for one gate (layout: gate_launch.hpp).  `pos`
-// maps a qubit to its tile coordinate (-1 outside the tile); offsets in the
-// op are relative to the start of `data` and rebased by the caller.
+// Tile-pass op records (layout: gate_launch.hpp).  A pass is built by
+// walking its gates with the register layout the kernel will have: `pos`
+// maps a qubit to its tile coordinate (-1 outside the tile) and `P` lists the
+// r register positions (ascending) of the current layout; every other tile
+// position is a thread position (thread-id bit b = b-th of them, ascending).
+// Offsets are relative to the start of `data` and rebased by build_pass.
+struct PassGeom {
+  int M = 0, L = 0, r = 0;
+  std::vector<int> pos;  // qubit -> tile coordinate
+  std::vector<int> P;    // register positions of the current layout
+  int reg_bit(int p) const {
+    for (int k = 0; k < r; ++k)
+      if (P[k] == p) return k;
+    return -1;
+  }
+  int thread_bit(int p) const {  // index among the non-register positions
+    int b = 0;
+    for (int q = 0; q < p; ++q) b += reg_bit(q) < 0;
+    return b;
+  }
+};
+
 template <typename Real>
-tsg::PassOp build_pass_op(const LaunchStructure& ls, const std::vector<int>& pos, int M, int L,
-                          std::vector<unsigned char>& data) {
-  constexpr int T = tsg::kPassLogThreads;
+int padded_offset(uint32_t x, int L) {
   const int stride = (1 << L) + tsg::kPassPadBytes / static_cast<int>(sizeof(Real));
-  auto padded = [&](uint32_t x) { return (x >> L) * static_cast<uint32_t>(stride) + (x & ((1u << L) - 1)); };
+  return static_cast<int>((x >> L) * static_cast<uint32_t>(stride) + (x & ((1u << L) - 1)));
+}
+
+tsg::PassOp blank_op(int kind) {
   tsg::PassOp op;
   std::memset(&op, 0, sizeof op);
-  const int d = 1 << ls.ks;
-  pad16(data);
-  op.data_off = static_cast<int32_t>(data.size());
-  // controls outside the tile are shared by both op families
-  std::vector<std::pair<int, uint32_t>> cin;  // (tile position, value)
+  op.kind = kind;
+  return op;
+}
+
+template <typename Real>
+tsg::PassOp build_layout_op(const PassGeom& g) {
+  tsg::PassOp op = blank_op(tsg::kPassLayout);
+  std::vector<int> P = g.P;
+  uint64_t gm[16];
+  if (g.r + 1 > 6) throw SimError("pass: too many register positions");
+  op.n_xmask = tsg::insertion_masks(P.data(), g.r, g.M - g.r, gm);
+  for (int m = 0; m < op.n_xmask; ++m) op.xmask[m] = static_cast<uint32_t>(gm[m]);
+  for (int k = 0; k < g.r; ++k) op.dep[k] = static_cast<uint32_t>(padded_offset<Real>(1u << g.P[k], g.L));
+  return op;
+}
+
+// out-of-tile controls into cout, the rest returned as (tile position, value)
+std::vector<std::pair<int, uint32_t>> split_controls(const LaunchStructure& ls, const PassGeom& g, tsg::PassOp& op) {
+  std::vector<std::pair<int, uint32_t>> cin;
   for (int c : ls.controls) {
     const uint32_t v = static_cast<uint32_t>((ls.control_values >> c) & 1u);
-    if (pos[c] < 0) {
+    if (g.pos[c] < 0) {
       op.cout_mask |= uint64_t{1} << c;
       op.cout_val |= static_cast<uint64_t>(v) << c;
     } else {
-      cin.emplace_back(pos[c], v);
+      cin.emplace_back(g.pos[c], v);
     }
   }
-  if (ls.klass == KernelClass::Diagonal) {
-    if (ls.ks > 7) throw SimError("pass: diagonal op wider than 7 qubits");
-    op.ks = ls.ks;
-    uint32_t thr_ctl_mask = 0, thr_ctl_val = 0;
-    std::vector<std::pair<int, int>> thr_bits;  // (tile position < T, table bit)
-    bool on_thread = false, on_iter = false;
-    for (const auto& [p, v] : cin) {
-      if (p < T) {
-        thr_ctl_mask |= 1u << p;
-        thr_ctl_val |= v << p;
-        on_thread = true;
-      } else {
-        op.ictl_mask |= 1u << (p - T);
-        op.ictl_val |= v << (p - T);
-        on_iter = true;
-      }
+  return cin;
+}
+
+template <typename Real>
+tsg::PassOp build_diag_op(const LaunchStructure& ls, const PassGeom& g, std::vector<unsigned char>& data) {
+  if (ls.ks > 7) throw SimError("pass: diagonal op wider than 7 qubits");
+  tsg::PassOp op = blank_op(tsg::kPassDiagT);
+  const int d = 1 << ls.ks;
+  pad16(data);
+  op.data_off = static_cast<int32_t>(data.size());
+  op.ks = ls.ks;
+  uint32_t thr_ctl_mask = 0, thr_ctl_val = 0;
+  std::vector<std::pair<int, int>> thr_bits;  // (thread-id bit, table bit)
+  bool on_thread = false, on_reg = false;
+  for (const auto& [p, v] : split_controls(ls, g, op)) {
+    const int k = g.reg_bit(p);
+    if (k >= 0) {
+      op.ictl_mask |= 1u << k;
+      op.ictl_val |= v << k;
+      on_reg = true;
+    } else {
+      const int tb = g.thread_bit(p);
+      thr_ctl_mask |= 1u << tb;
+      thr_ctl_val |= v << tb;
+      on_thread = true;
     }
-    for (int b = 0; b < ls.ks; ++b) {
-      const int q = ls.sub_targets[b], p = pos[q];
-      if (p < 0) {
-        op.out_gbit[op.n_out] = static_cast<uint8_t>(q);
-        op.out_jbit[op.n_out++] = static_cast<uint8_t>(b);
-      } else if (p < T) {
-        thr_bits.emplace_back(p, b);
-        on_thread = true;
-      } else {
-        op.dep[p - T] |= 1u << b;
-        on_iter = true;
-      }
-    }
-    op.kind = on_thread && on_iter ? tsg::kPassDiagX : (on_iter ? tsg::kPassDiagI : tsg::kPassDiagT);
-    for (int j = 0; j < d; ++j) append_real2<Real>(data, ls.sub_re[j * d + j], ls.sub_im[j * d + j]);
-    append_real2<Real>(data, 1.0, 0.0);  // inactive controls
-    if (op.kind != tsg::kPassDiagI) {
-      pad16(data);
-      op.aux_off = static_cast<int32_t>(data.size());
-      for (int t = 0; t < tsg::kPassThreads; ++t) {
-        uint32_t v = 0;
-        for (const auto& [p, b] : thr_bits) v |= ((static_cast<uint32_t>(t) >> p) & 1u) << b;
-        if ((static_cast<uint32_t>(t) & thr_ctl_mask) != thr_ctl_val) v = 0xffu;
-        data.push_back(static_cast<unsigned char>(v));
-      }
-    }
-    return op;
   }
-  // GEN: mixed qubits E (tile qubits) and block qubits B (anywhere): the
-  // sub-gate is 2^|B| blocks of 2^|E| x 2^|E| (tilesim::mixed_bits)
-  op.kind = tsg::kPassGen;
-  const std::vector<int> ebits = mixed_bits(ls);
-  std::vector<int> bbits;
+  for (int b = 0; b < ls.ks; ++b) {
+    const int q = ls.sub_targets[b], p = g.pos[q];
+    if (p < 0) {
+      op.out_gbit[op.n_out] = static_cast<uint8_t>(q);
+      op.out_jbit[op.n_out++] = static_cast<uint8_t>(b);
+    } else if (g.reg_bit(p) >= 0) {
+      op.dep[g.reg_bit(p)] |= 1u << b;
+      on_reg = true;
+    } else {
+      thr_bits.emplace_back(g.thread_bit(p), b);
+      on_thread = true;
+    }
+  }
+  op.kind = on_thread && on_reg ? tsg::kPassDiagX : (on_reg ? tsg::kPassDiagI : tsg::kPassDiagT);
+  for (int j = 0; j < d; ++j) append_real2<Real>(data, ls.sub_re[j * d + j], ls.sub_im[j * d + j]);
+  append_real2<Real>(data, 1.0, 0.0);  // inactive controls
+  if (op.kind != tsg::kPassDiagI) {
+    pad16(data);
+    op.aux_off = static_cast<int32_t>(data.size());
+    for (int t = 0; t < tsg::kPassThreads; ++t) {
+      uint32_t v = 0;
+      for (const auto& [tb, b] : thr_bits) v |= ((static_cast<uint32_t>(t) >> tb) & 1u) << b;
+      if ((static_cast<uint32_t>(t) & thr_ctl_mask) != thr_ctl_val) v = 0xffu;
+      data.push_back(static_cast<unsigned char>(v));
+    }
+  }
+  return op;
+}
+
+// mixed (E) and block (B) bits of a non-diagonal sub-gate and the block matrices
+struct BlockForm {
+  std::vector<int> ebits, bbits;
+  int ke = 0, nb = 0, de = 1;
+  bool perm = false;
+  int full(const LaunchStructure& ls, int je, int jb) const {
+    int r = 0;
+    for (int b = 0; b < ke; ++b) r |= ((je >> b) & 1) << ebits[b];
+    for (int b = 0; b < nb; ++b) r |= ((jb >> b) & 1) << bbits[b];
+    return r;
+  }
+};
+
+BlockForm block_form(const LaunchStructure& ls) {
+  BlockForm f;
+  f.ebits = mixed_bits(ls);
   for (int b = 0; b < ls.ks; ++b)
-    if (std::find(ebits.begin(), ebits.end(), b) == ebits.end()) bbits.push_back(b);
-  const int ke = static_cast<int>(ebits.size()), nb = static_cast<int>(bbits.size());
-  const int de = 1 << ke;
-  op.ks = ke;
+    if (std::find(f.ebits.begin(), f.ebits.end(), b) == f.ebits.end()) f.bbits.push_back(b);
+  f.ke = static_cast<int>(f.ebits.size());
+  f.nb = static_cast<int>(f.bbits.size());
+  f.de = 1 << f.ke;
+  f.perm = monomial(ls);
+  return f;
+}
+
+// blocks at the current end of `data`: GEN (D*D + 1 entries each) or Perm
+// (src[D] element indices, 16-byte block, val[D]); perm_src_padded: Perm src
+// entries are padded smem offsets (SPerm) instead of element indices (RPerm)
+template <typename Real>
+void append_blocks(const LaunchStructure& ls, const BlockForm& f, std::vector<unsigned char>& data,
+                   const std::vector<uint32_t>* soffs) {
+  const int d = 1 << ls.ks, de = f.de;
+  for (int jb = 0; jb < (1 << f.nb); ++jb) {
+    if (f.perm) {
+      std::vector<int> col(de, 0);
+      for (int r = 0; r < de; ++r)
+        for (int c = 0; c < de; ++c) {
+          const int e = f.full(ls, r, jb) * d + f.full(ls, c, jb);
+          if (ls.sub_re[e] != 0.0 || ls.sub_im[e] != 0.0) col[r] = c;
+        }
+      for (int r = 0; r < de; ++r) append_pod(data, soffs ? (*soffs)[col[r]] : static_cast<uint32_t>(col[r]));
+      pad16(data);
+      for (int r = 0; r < de; ++r) {
+        const int e = f.full(ls, r, jb) * d + f.full(ls, col[r], jb);
+        append_real2<Real>(data, ls.sub_re[e], ls.sub_im[e]);
+      }
+    } else {
+      for (int r = 0; r < de; ++r)
+        for (int c = 0; c < de; ++c) {
+          const int e = f.full(ls, r, jb) * d + f.full(ls, c, jb);
+          append_real2<Real>(data, ls.sub_re[e], ls.sub_im[e]);
+        }
+      append_real2<Real>(data, 0.0, 0.0);  // bank padding between blocks
+    }
+  }
+}
+
+// RGen / RPerm: every mixed qubit is a register position of the layout
+template <typename Real>
+tsg::PassOp build_reg_op(const LaunchStructure& ls, const PassGeom& g, std::vector<unsigned char>& data) {
+  const BlockForm f = block_form(ls);
+  tsg::PassOp op = blank_op(f.perm ? tsg::kPassRPerm : tsg::kPassRGen);
+  op.ks = f.ke;
+  for (int b : f.ebits) {
+    const int k = g.reg_bit(g.pos[ls.sub_targets[b]]);
+    if (k < 0) throw SimError("pass: register op on a non-register qubit");
+    op.rmask |= 1 << k;
+  }
+  for (const auto& [p, v] : split_controls(ls, g, op)) {
+    const int k = g.reg_bit(p);
+    if (k >= 0) {
+      op.ictl_mask |= 1u << k;
+      op.ictl_val |= v << k;
+    } else {
+      op.tctl_mask |= 1u << p;
+      op.tctl_val |= v << p;
+    }
+  }
+  for (int i = 0; i < f.nb; ++i) {
+    const int q = ls.sub_targets[f.bbits[i]], p = g.pos[q];
+    if (p < 0) {
+      op.out_gbit[op.n_out] = static_cast<uint8_t>(q);
+      op.out_jbit[op.n_out++] = static_cast<uint8_t>(i);
+    } else if (g.reg_bit(p) >= 0) {
+      op.dep[g.reg_bit(p)] |= 1u << i;
+    } else {
+      op.tb_pos[op.n_tb] = static_cast<uint8_t>(p);
+      op.tb_jbit[op.n_tb++] = static_cast<uint8_t>(i);
+    }
+  }
+  pad16(data);
+  op.data_off = static_cast<int32_t>(data.size());
+  op.aux_off = op.data_off;
+  append_blocks<Real>(ls, f, data, nullptr);
+  return op;
+}
+
+// SGen / SPerm: through shared memory, one thread (or a row split) per group
+template <typename Real>
+tsg::PassOp build_smem_op(const LaunchStructure& ls, const PassGeom& g, std::vector<unsigned char>& data) {
+  const BlockForm f = block_form(ls);
+  tsg::PassOp op = blank_op(f.perm ? tsg::kPassSPerm : tsg::kPassSGen);
+  op.ks = f.ke;
+  const int de = f.de, M = g.M, L = g.L;
   std::vector<int> zpos;  // tile positions fixed within a group: mixed qubits + in-tile controls
   uint32_t cin_val = 0;
-  for (const auto& [p, v] : cin) {
+  for (const auto& [p, v] : split_controls(ls, g, op)) {
     zpos.push_back(p);
     cin_val |= v << p;
   }
-  for (int b : ebits) {
-    const int p = pos[ls.sub_targets[b]];
+  for (int b : f.ebits) {
+    const int p = g.pos[ls.sub_targets[b]];
     if (p < 0) throw SimError("pass: mixed qubit outside the tile");
     zpos.push_back(p);
   }
   std::vector<std::pair<int, int>> blk_in;  // (tile position, block bit)
-  for (int i = 0; i < nb; ++i) {
-    const int q = ls.sub_targets[bbits[i]], p = pos[q];
+  for (int i = 0; i < f.nb; ++i) {
+    const int q = ls.sub_targets[f.bbits[i]], p = g.pos[q];
     if (p < 0) {
       op.out_gbit[op.n_out] = static_cast<uint8_t>(q);
       op.out_jbit[op.n_out++] = static_cast<uint8_t>(i);
@@ -639,130 +778,157 @@ tsg::PassOp build_pass_op(const LaunchStructure& ls, const std::vector<int>& pos
   uint64_t gm[64];
   const int n_gm = tsg::insertion_masks(zpos.data(), count, M - count, gm);
   op.log2_groups = M - count;
-  auto deposit = [&](uint32_t g) {
+  auto deposit = [&](uint32_t v) {
     uint64_t x = 0;
-    for (int i = 0; i < n_gm; ++i) x += (g & gm[i]) << i;
+    for (int i = 0; i < n_gm; ++i) x += (v & gm[i]) << i;
     return static_cast<uint32_t>(x);
   };
   auto entry = [&](uint32_t x) {  // padded offset | block bits << 16 (additive over disjoint bits)
     uint32_t jb = 0;
     for (const auto& [p, i] : blk_in) jb |= ((x >> p) & 1u) << i;
-    return padded(x) | (jb << 16);
+    return static_cast<uint32_t>(padded_offset<Real>(x, L)) | (jb << 16);
   };
+  pad16(data);
+  op.data_off = static_cast<int32_t>(data.size());
+  std::vector<uint32_t> soffs(de);
   for (int j = 0; j < de; ++j) {
     uint32_t x = 0;
-    for (int b = 0; b < ke; ++b) x |= static_cast<uint32_t>((j >> b) & 1) << pos[ls.sub_targets[ebits[b]]];
-    append_pod(data, padded(x));
+    for (int b = 0; b < f.ke; ++b) x |= static_cast<uint32_t>((j >> b) & 1) << g.pos[ls.sub_targets[f.ebits[b]]];
+    soffs[j] = static_cast<uint32_t>(padded_offset<Real>(x, L));
+    append_pod(data, soffs[j]);
   }
   pad16(data);
   const uint32_t n_groups = 1u << op.log2_groups;
-  // fewer groups than threads: split each group's rows over 2^rsplit threads
-  int rsplit = 0;
+  int rsplit = 0;  // fewer groups than threads: split each group's rows over 2^rsplit threads
   while ((n_groups << (rsplit + 1)) <= static_cast<uint32_t>(tsg::kPassThreads) && (1 << (rsplit + 1)) <= std::min(de, 8))
     ++rsplit;
   op.log2_rsplit = rsplit;
-  if (ke >= 4 && rsplit == 0) throw SimError("pass: an op of >= 4 mixed qubits needs a row split");
+  if (rsplit == 0 && (f.ke >= 5 || (f.ke == 4 && sizeof(Real) == 8)))
+    throw SimError("pass: this op needs a row split");  // no kernel instance without one (pass_gen_split)
   for (uint32_t t = 0; t < static_cast<uint32_t>(tsg::kPassThreads); ++t) {
-    const uint32_t g = t & (n_groups - 1);
-    append_pod(data, (t < (n_groups << rsplit)) ? entry(deposit(g) | cin_val) : 0u);
+    const uint32_t gi = t & (n_groups - 1);
+    append_pod(data, (t < (n_groups << rsplit)) ? entry(deposit(gi) | cin_val) : 0u);
   }
   const uint32_t n_k = std::max<uint32_t>(1, n_groups / tsg::kPassThreads);
   for (uint32_t k = 0; k < n_k; ++k) append_pod(data, k == 0 ? 0u : entry(deposit(k * tsg::kPassThreads)));
   pad16(data);
   op.aux_off = static_cast<int32_t>(data.size());
-  auto full_index = [&](int je, int jb) {
-    int r = 0;
-    for (int b = 0; b < ke; ++b) r |= ((je >> b) & 1) << ebits[b];
-    for (int b = 0; b < nb; ++b) r |= ((jb >> b) & 1) << bbits[b];
-    return r;
-  };
-  if (monomial(ls)) {  // Perm: per block src[de] then val[de]
-    op.kind = tsg::kPassPerm;
-    std::vector<uint32_t> soffs(de);
-    for (int j = 0; j < de; ++j) {
-      uint32_t x = 0;
-      for (int b = 0; b < ke; ++b) x |= static_cast<uint32_t>((j >> b) & 1) << pos[ls.sub_targets[ebits[b]]];
-      soffs[j] = padded(x);
-    }
-    for (int jb = 0; jb < (1 << nb); ++jb) {
-      std::vector<int> col(de, 0);
-      for (int r = 0; r < de; ++r)
-        for (int c = 0; c < de; ++c) {
-          const int e = full_index(r, jb) * d + full_index(c, jb);
-          if (ls.sub_re[e] != 0.0 || ls.sub_im[e] != 0.0) col[r] = c;
-        }
-      for (int r = 0; r < de; ++r) append_pod(data, soffs[col[r]]);
-      pad16(data);
-      for (int r = 0; r < de; ++r) {
-        const int e = full_index(r, jb) * d + full_index(col[r], jb);
-        append_real2<Real>(data, ls.sub_re[e], ls.sub_im[e]);
-      }
-    }
-    return op;
-  }
-  for (int jb = 0; jb < (1 << nb); ++jb) {
-    for (int r = 0; r < de; ++r)
-      for (int c = 0; c < de; ++c) {
-        const int e = full_index(r, jb) * d + full_index(c, jb);
-        append_real2<Real>(data, ls.sub_re[e], ls.sub_im[e]);
-      }
-    append_real2<Real>(data, 0.0, 0.0);  // bank padding between blocks
-  }
+  append_blocks<Real>(ls, f, data, f.perm ? &soffs : nullptr);
   return op;
 }
 
-// Device blob of one tile pass (layout: gate_launch.hpp).  Runs of
-// consecutive diagonal gates get a RUN header and are ordered by class
-// (DiagT, DiagI, DiagX; program order within a class -- diagonal gates
-// commute).
+// Register positions for a layout that holds `need` (tile positions):
+// then the next ops' needs while they fit, then high positions.
+std::vector<int> choose_layout(const std::vector<int>& need, const std::vector<std::vector<int>>& upcoming, int r,
+                               int M, int L) {
+  std::vector<int> P = need;
+  for (const auto& e : upcoming) {
+    std::vector<int> u = P;
+    for (int p : e)
+      if (std::find(u.begin(), u.end(), p) == u.end()) u.push_back(p);
+    if (static_cast<int>(u.size()) > r) break;
+    P = u;
+  }
+  for (int p = M - 1; p >= L && static_cast<int>(P.size()) < r; --p)
+    if (std::find(P.begin(), P.end(), p) == P.end()) P.push_back(p);
+  for (int p = L - 1; p >= 0 && static_cast<int>(P.size()) < r; --p)
+    if (std::find(P.begin(), P.end(), p) == P.end()) P.push_back(p);
+  std::sort(P.begin(), P.end());
+  return P;
+}
+
+// Device blob of one tile pass: LAYOUT, then the gates in program order --
+// register ops when the mixed qubits fit the register positions (a new
+// LAYOUT when they are not the current ones), shared-memory ops otherwise,
+// and RUN headers before runs of diagonal gates ordered by class (diagonal
+// gates commute).
 template <typename Real>
 ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const PassConfig& cfg,
                        std::vector<unsigned char>& arena) {
   const int n = prog->n, L = cfg.run_log2, M = cfg.tile_log2;
   const int nh = M - L;
   if (static_cast<int>(step.high.size()) != nh) throw SimError("pass: high tile qubit count");
-  std::vector<int> pos(n, -1);
-  for (int q = 0; q < L; ++q) pos[q] = q;
-  for (int h = 0; h < nh; ++h) pos[step.high[h]] = L + h;
+  PassGeom g;
+  g.M = M;
+  g.L = L;
+  g.r = M - tsg::kPassLogThreads;
+  g.pos.assign(n, -1);
+  for (int q = 0; q < L; ++q) g.pos[q] = q;
+  for (int h = 0; h < nh; ++h) g.pos[step.high[h]] = L + h;
+
+  // mixed tile positions of every register-capable gate (in order)
+  const size_t ng = step.gates.size();
+  std::vector<std::vector<int>> mixed(ng);
+  std::vector<bool> reg_ok(ng, false);
+  for (size_t i = 0; i < ng; ++i) {
+    const LaunchStructure& ls = prog->gates[step.gates[i]].ls;
+    if (ls.klass == KernelClass::Diagonal) continue;
+    for (int b : mixed_bits(ls)) mixed[i].push_back(g.pos[ls.sub_targets[b]]);
+    reg_ok[i] = static_cast<int>(mixed[i].size()) <= std::min(g.r, 3);
+  }
+  auto upcoming = [&](size_t from) {
+    std::vector<std::vector<int>> u;
+    for (size_t i = from; i < ng; ++i)
+      if (reg_ok[i]) u.push_back(mixed[i]);
+    return u;
+  };
 
   std::vector<tsg::PassOp> ops;
   std::vector<unsigned char> data;
-  size_t i = 0;
-  while (i < step.gates.size()) {
+  {
+    size_t first = 0;
+    while (first < ng && !reg_ok[first]) ++first;
+    g.P = first < ng ? choose_layout(mixed[first], upcoming(first + 1), g.r, M, L)
+                     : choose_layout({}, {}, g.r, M, L);
+    ops.push_back(build_layout_op<Real>(g));
+  }
+  std::vector<tsg::PassOp> cls[3];  // the open run of diagonal ops, by class
+  auto flush_run = [&]() {
+    if (cls[0].empty() && cls[1].empty() && cls[2].empty()) return;
+    tsg::PassOp hdr = blank_op(tsg::kPassRun);
+    hdr.ks = static_cast<int32_t>(cls[0].size());
+    hdr.log2_groups = static_cast<int32_t>(cls[1].size());
+    hdr.log2_rsplit = static_cast<int32_t>(cls[2].size());
+    ops.push_back(hdr);
+    for (auto& c : cls) {
+      ops.insert(ops.end(), c.begin(), c.end());
+      c.clear();
+    }
+  };
+  for (size_t i = 0; i < ng; ++i) {
     const LaunchStructure& ls = prog->gates[step.gates[i]].ls;
-    if (ls.klass != KernelClass::Diagonal) {
-      ops.push_back(build_pass_op<Real>(ls, pos, M, L, data));
-      ++i;
+    if (ls.klass == KernelClass::Diagonal) {
+      tsg::PassOp op = build_diag_op<Real>(ls, g, data);
+      cls[op.kind - tsg::kPassDiagT].push_back(op);
       continue;
     }
-    std::vector<tsg::PassOp> cls[3];
-    for (; i < step.gates.size() && prog->gates[step.gates[i]].ls.klass == KernelClass::Diagonal; ++i) {
-      tsg::PassOp op = build_pass_op<Real>(prog->gates[step.gates[i]].ls, pos, M, L, data);
-      cls[op.kind - tsg::kPassDiagT].push_back(op);
+    flush_run();
+    if (reg_ok[i]) {
+      bool fits = true;
+      for (int p : mixed[i]) fits = fits && g.reg_bit(p) >= 0;
+      if (!fits) {
+        g.P = choose_layout(mixed[i], upcoming(i + 1), g.r, M, L);
+        ops.push_back(build_layout_op<Real>(g));
+      }
+      ops.push_back(build_reg_op<Real>(ls, g, data));
+    } else {
+      ops.push_back(build_smem_op<Real>(ls, g, data));
     }
-    tsg::PassOp hdr;
-    std::memset(&hdr, 0, sizeof hdr);
-    hdr.kind = tsg::kPassRun;
-    hdr.ks = static_cast<int32_t>(cls[0].size());
-    hdr.run_i = static_cast<int32_t>(cls[1].size());
-    hdr.run_x = static_cast<int32_t>(cls[2].size());
-    ops.push_back(hdr);
-    for (auto& c : cls) ops.insert(ops.end(), c.begin(), c.end());
   }
+  flush_run();
+
   if (ops.size() > static_cast<size_t>(tsg::kPassMaxOps)) throw SimError("pass: too many ops");
   if (std::getenv("TSG_PASS_DEBUG")) {
-    int cnt[5] = {0, 0, 0, 0, 0};
+    int cnt[9] = {0};
     for (const tsg::PassOp& op : ops) ++cnt[op.kind];
     std::fprintf(stderr, "pass gates %zu high", step.gates.size());
     for (int h : step.high) std::fprintf(stderr, " %d", h);
-    std::fprintf(stderr, ": runs %d diagT %d diagI %d diagX %d gen %d (ks:", cnt[0], cnt[1], cnt[2], cnt[3], cnt[4]);
-    for (const tsg::PassOp& op : ops)
-      if (op.kind == tsg::kPassGen) std::fprintf(stderr, " %d/%d", op.ks, op.log2_rsplit);
-    std::fprintf(stderr, ")\n");
+    std::fprintf(stderr, ": layouts %d runs %d diagT %d diagI %d diagX %d rgen %d rperm %d sgen %d sperm %d\n", cnt[0],
+                 cnt[1], cnt[2], cnt[3], cnt[4], cnt[5], cnt[6], cnt[7], cnt[8]);
   }
   const size_t data_base = (size_t{8} << nh) + ops.size() * sizeof(tsg::PassOp);
   for (tsg::PassOp& op : ops) {
-    if (op.kind == tsg::kPassRun) continue;
+    if (op.kind == tsg::kPassLayout || op.kind == tsg::kPassRun) continue;
     op.data_off += static_cast<int32_t>(data_base);
     if (op.kind != tsg::kPassDiagI) op.aux_off += static_cast<int32_t>(data_base);
   }

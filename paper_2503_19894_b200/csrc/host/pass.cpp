@@ -15,11 +15,13 @@ PassConfig pass_config(int precision_bits) {
     c.run_log2 = 5;    // 256-byte runs per array
     c.max_gen_ks = 4;  // dense ks = 5 complex128 is FP64-bound: own DMMA kernel
     c.amp_real_bytes = 8;
+    c.reg_bits = 3;
   } else {
     c.tile_log2 = 12;
     c.run_log2 = 6;
     c.max_gen_ks = 5;
     c.amp_real_bytes = 4;
+    c.reg_bits = 3;  // of 4: register ops mix at most 3 qubits
   }
   const char* f = std::getenv("TSG_PASS_FORCE");
   c.force = f && f[0] == '1';
@@ -29,7 +31,7 @@ PassConfig pass_config(int precision_bits) {
 namespace {
 
 constexpr int kPassOpRecord = 192;  // sizeof(tsg::PassOp)
-constexpr int kThreads = 512;       // tsg::kPassThreads (consumer threads of k_pass)
+constexpr int kThreads = 256;       // tsg::kPassThreads (threads of a k_pass CTA)
 
 }  // namespace
 
@@ -144,8 +146,9 @@ int pass_op_bytes(const LaunchStructure& ls, const PassConfig& cfg) {
 
 double pass_op_sweeps(const LaunchStructure& ls, const PassConfig& cfg) {
   if (ls.klass == KernelClass::Diagonal) return cfg.diag_sweeps;
-  if (monomial(ls)) return cfg.perm_sweeps * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
   const int ke = static_cast<int>(mixed_bits(ls).size());
+  if (ke <= cfg.reg_bits) return cfg.reg_gen_sweeps;  // register op (controls do not shrink its cost)
+  if (monomial(ls)) return cfg.perm_sweeps * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
   return cfg.gen_sweeps[std::min(ke, 5)] * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
 }
 

@@ -26,7 +26,16 @@ def case(name, gates):
     else:
         c = ts.Circuit(N)
         for q, kind in gates:
-            c.add_matrix(sorted(q), random_gate_matrix(len(q), sum(q) * 7 + len(name), kind))
+            if kind == "blockdiag2":  # 4-qubit gate mixing its two low qubits, blocks chosen by the two high ones
+                rng = np.random.default_rng(sum(q))
+                m = np.zeros((16, 16), complex)
+                for b in range(4):
+                    u = random_gate_matrix(2, int(rng.integers(1000)), "dense")
+                    idx = [b * 4 + j for j in range(4)]
+                    m[np.ix_(idx, idx)] = u
+                c.add_matrix(sorted(q), m)
+            else:
+                c.add_matrix(sorted(q), random_gate_matrix(len(q), sum(q) * 7 + len(name), kind))
     out = []
     for no_pass in (False, True):
         if no_pass:
@@ -62,6 +71,10 @@ cases = {
     "ks5 dense 20-24": [([20, 21, 22, 23, 24], "dense")],
     "ks5 diag-ish 7-11": [([7, 8, 9, 10, 11], "controlled")],
     "ks5 rqc-like": "rqc",
+    "4x gen ks2 blk out": [([6, 7, 20, 21], "blockdiag2"), ([8, 9, 22, 23], "blockdiag2"), ([6, 7, 24, 25], "blockdiag2"), ([8, 9, 26, 27], "blockdiag2")],
+    "4x gen ks2 blk thr": [([0, 1, 6, 7], "blockdiag2"), ([2, 3, 6, 7], "blockdiag2"), ([0, 1, 8, 9], "blockdiag2"), ([2, 3, 8, 9], "blockdiag2")],
+    "4x gen ks2 blk iter": [([6, 7, 9, 10], "blockdiag2"), ([0, 1, 9, 10], "blockdiag2"), ([2, 3, 9, 10], "blockdiag2"), ([7, 8, 9, 10], "blockdiag2")],
+    "4x gen ks2 noblk": [([6, 7], "dense"), ([8, 9], "dense"), ([6, 7], "dense"), ([8, 9], "dense")],
     "4x perm ks2": [([6, 7], "perm"), ([8, 9], "perm"), ([1, 7], "perm"), ([2, 9], "perm")],
     "4x perm ks4": [([0, 1, 9, 10], "perm"), ([2, 3, 7, 8], "perm"), ([0, 2, 9, 7], "perm"), ([5, 6, 7, 8], "perm")],
 }

@@ -49,3 +49,25 @@ def random_gate_matrix(k: int, seed: int, kind: str = "dense") -> np.ndarray:
         m[h:, h:] = ob.random_unitary(k - 1, seed) if k > 1 else np.exp(1j * 0.3)
         return m
     raise ValueError(kind)
+
+
+def block_gate(mixed, block, seed: int):
+    """A gate on sorted(mixed + block) that is block-diagonal in the `block`
+    qubits, with an independent dense unitary on the `mixed` qubits per block
+    (the structure tilesim::mixed_bits / split_blocks detect)."""
+    targets = sorted(mixed + block)
+    k = len(targets)
+    rng = np.random.default_rng(seed)
+    m = np.zeros((1 << k, 1 << k), complex)
+    for jb in range(1 << len(block)):
+        u = ob.random_unitary(len(mixed), int(rng.integers(1000)))
+        idx = []
+        for je in range(1 << len(mixed)):
+            f = 0
+            for b, q in enumerate(mixed):
+                f |= ((je >> b) & 1) << targets.index(q)
+            for b, q in enumerate(block):
+                f |= ((jb >> b) & 1) << targets.index(q)
+            idx.append(f)
+        m[np.ix_(idx, idx)] = u
+    return targets, m

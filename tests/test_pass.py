@@ -12,7 +12,7 @@ import pytest
 
 import paper_2503_19894_b200 as ts
 from oracle import binding as ob
-from tests._util import random_gate_matrix, to_oracle
+from tests._util import block_gate, random_gate_matrix, to_oracle
 
 PREC = {64: "f64", 32: "f32"}
 BAR = {64: 1e-10, 32: 1e-5}
@@ -170,3 +170,33 @@ def test_pass_qft_analytic_basis_state():
     y = np.arange(1 << n)
     want = np.exp(2j * np.pi * ((x * y) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
     assert np.abs(sv.amplitudes() - want).max() <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("mixed,block", [
+    ([3, 11, 15], [9, 13]), ([3, 11, 15], []), ([11, 15], [9]), ([3], [9, 13]), ([2, 4], []), ([7, 8, 9], [12]),
+    ([0, 1], [5, 14]), ([6], []), ([5, 6, 7, 8], []), ([1, 2, 3, 4], [10]), ([4, 5, 6, 7, 8], []),
+])
+def test_forced_single_op_pass(prec, mixed, block):
+    """One block-structured gate (+ a phase) forced into a tile pass -- register
+    or shared-memory op depending on its width and the layout -- against the
+    same gate without passes and against the oracle."""
+    n = 16
+    targets, m = block_gate(mixed, block, sum(mixed) * 31 + len(block))
+    c = ts.Circuit(n)
+    c.add_matrix(targets, m)
+    c.add_matrix([0], np.diag([1, np.exp(0.3j)]))
+    rng = np.random.default_rng(1)
+    re0, im0 = rng.standard_normal(1 << n), rng.standard_normal(1 << n)
+    s = np.sqrt((re0 ** 2 + im0 ** 2).sum())
+    dt = np.float64 if prec == 64 else np.float32
+    re0, im0 = (re0 / s).astype(dt).astype(np.float64), (im0 / s).astype(dt).astype(np.float64)
+    sv, prog = _run_program(c, prec, re0, im0, force=True)
+    in_pass = len(mixed) <= GEOM[prec][2]  # wider sub-gates always run on their own kernel
+    assert (prog.steps()[0]["kind"] == "pass") == in_pass
+    ref, _ = _run_program(c, prec, re0, im0, no_pass=True)
+    assert ts.compare_states(sv, ref) <= (1e-12 if prec == 64 else 2e-6)
+    ore, oim = re0.astype(dt), im0.astype(dt)
+    ob.run_circuit(to_oracle(c), ore, oim)
+    assert ts.compare_states(sv, (ore.astype(np.float64), oim.astype(np.float64))) <= BAR[prec]
