@@ -29,15 +29,16 @@ struct PassConfig {
   // B200 cost model of a pass, in units of one state sweep (2 * 2^n * B_amp
   // bytes at HBM speed), measured with scripts/pass_bench.py at n = 28
   // (profiles/r01/pass_bench.txt): the pass itself, each diagonal op, each
-  // GEN op by mixed-qubit count; a standalone launch costs its sweep
-  // (touched share for controlled gates).
-  double base_sweeps = 1.3;
-  double diag_sweeps = 0.08;
-  double gen_sweeps[6] = {0.0, 0.45, 0.55, 0.8, 1.4, 2.0};  // through shared memory
-  double perm_sweeps = 0.45;
-  int reg_bits = 3;             // register positions a register op may mix (2^M / 256 amplitudes per thread)
-  double reg_gen_sweeps = 0.3;  // an op on register positions, with its share of layout changes
+  // GEN op by mixed-qubit count (register ops up to reg_bits mixed qubits,
+  // shared-memory ops above; layout changes included), monomial ops; a
+  // standalone launch costs its sweep (touched share for controlled gates).
+  double base_sweeps = 1.07;
+  double diag_sweeps = 0.04;
+  double gen_sweeps[6] = {0.0, 0.2, 0.45, 0.6, 1.2, 2.0};
+  double perm_sweeps_reg = 0.4;
+  double perm_sweeps_smem = 0.5;
   double standalone_sweeps = 1.08;
+  int reg_bits = 3;  // register positions a register op may mix (2^M / 256 amplitudes per thread)
   // testing: every eligible gate joins (no cost test, single-gate passes allowed);
   // pass_config() sets it when the environment has TSG_PASS_FORCE=1
   bool force = false;

@@ -22,6 +22,13 @@ PassConfig pass_config(int precision_bits) {
     c.max_gen_ks = 5;
     c.amp_real_bytes = 4;
     c.reg_bits = 3;  // of 4: register ops mix at most 3 qubits
+    c.base_sweeps = 1.28;
+    c.diag_sweeps = 0.05;
+    const double gen32[6] = {0.0, 0.25, 0.4, 0.7, 1.6, 2.5};
+    std::copy(gen32, gen32 + 6, c.gen_sweeps);
+    c.perm_sweeps_reg = 0.45;
+    c.perm_sweeps_smem = 0.6;
+    c.standalone_sweeps = 1.1;
   }
   const char* f = std::getenv("TSG_PASS_FORCE");
   c.force = f && f[0] == '1';
@@ -147,9 +154,8 @@ int pass_op_bytes(const LaunchStructure& ls, const PassConfig& cfg) {
 double pass_op_sweeps(const LaunchStructure& ls, const PassConfig& cfg) {
   if (ls.klass == KernelClass::Diagonal) return cfg.diag_sweeps;
   const int ke = static_cast<int>(mixed_bits(ls).size());
-  if (ke <= cfg.reg_bits) return cfg.reg_gen_sweeps;  // register op (controls do not shrink its cost)
-  if (monomial(ls)) return cfg.perm_sweeps * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
-  return cfg.gen_sweeps[std::min(ke, 5)] * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
+  if (monomial(ls)) return ke <= cfg.reg_bits ? cfg.perm_sweeps_reg : cfg.perm_sweeps_smem;
+  return cfg.gen_sweeps[std::min(ke, 5)];
 }
 
 double standalone_sweeps(const LaunchStructure& ls, const PassConfig& cfg) {

@@ -75,6 +75,10 @@ cases = {
     "4x gen ks2 blk thr": [([0, 1, 6, 7], "blockdiag2"), ([2, 3, 6, 7], "blockdiag2"), ([0, 1, 8, 9], "blockdiag2"), ([2, 3, 8, 9], "blockdiag2")],
     "4x gen ks2 blk iter": [([6, 7, 9, 10], "blockdiag2"), ([0, 1, 9, 10], "blockdiag2"), ([2, 3, 9, 10], "blockdiag2"), ([7, 8, 9, 10], "blockdiag2")],
     "4x gen ks2 noblk": [([6, 7], "dense"), ([8, 9], "dense"), ([6, 7], "dense"), ([8, 9], "dense")],
+    "4x gen ks3 same": [([6, 7, 8], "dense")] * 4,
+    "4x gen ks3 diff": [([6, 7, 8], "dense"), ([9, 10, 11], "dense"), ([6, 7, 8], "dense"), ([9, 10, 11], "dense")],
+    "4x gen ks1 same-layout": [([6], "dense"), ([7], "dense"), ([8], "dense"), ([6], "dense")],
+    "4x gen ks4 smem": [([5, 6, 7, 8], "dense"), ([7, 8, 9, 10], "dense"), ([5, 6, 9, 10], "dense"), ([6, 7, 8, 9], "dense")],
     "4x perm ks2": [([6, 7], "perm"), ([8, 9], "perm"), ([1, 7], "perm"), ([2, 9], "perm")],
     "4x perm ks4": [([0, 1, 9, 10], "perm"), ([2, 3, 7, 8], "perm"), ([0, 2, 9, 7], "perm"), ([5, 6, 7, 8], "perm")],
 }
