@@ -1028,6 +1028,61 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
   }
 }
 
+// run_circuit's planning: plan every gate, group the launches into steps
+// (tile passes, block splits), upload matrices and pass blobs once.
+std::unique_ptr<tsg_program> build_program(tsg_ctx* ctx, const Circuit& fused, double zero_tol, double one_tol,
+                                           int precision_bits) {
+  use_device(ctx);
+  const auto t0 = std::chrono::steady_clock::now();
+  auto prog = std::make_unique<tsg_program>();
+  prog->ctx = ctx;
+  prog->n = fused.n_qubits;
+  prog->prec = precision_bits;
+  std::vector<unsigned char> arena;
+  const uint64_t amp = precision_bits == 64 ? 16 : 8;
+  for (const Gate& g : fused.gates) {
+    ProgramGate pg;
+    pg.plan = plan_kernel(g, prog->n, 0, zero_tol, one_tol, false);
+    pg.ls = precision_bits == 64 ? pg.plan.launch : derive_launch(pg.plan, nullptr, precision_bits);
+    pg.launch = make_launch(pg.plan, pg.ls);
+    if (needs_tile_matrix(pg.launch, precision_bits)) {
+      const auto bytes = tile_matrix_bytes(pg.ls, pg.launch);
+      pg.mat_offset = (arena.size() + 255) & ~size_t{255};
+      arena.resize(pg.mat_offset + bytes.size());
+      std::copy(bytes.begin(), bytes.end(), arena.begin() + pg.mat_offset);
+      pg.has_mat = true;
+    }
+    prog->total_ops += pg.plan.profile.op_count;
+    prog->gates.push_back(std::move(pg));
+  }
+  plan_steps(prog.get(), arena);
+  for (const ProgramStep& step : prog->steps) {  // one launch per step (block splits: one per part)
+    const ProgramGate& pg = prog->gates[step.gate];
+    const bool split = step.kind == kStepGate && !pg.subs.empty();
+    prog->launches += split ? pg.subs.size() : 1;
+    prog->bytes += 2 * (uint64_t{1} << prog->n) * amp;
+    double frac = step.kind != kStepGate ? 1.0 : touched_fraction(pg.ls);
+    if (split) {
+      frac = 0.0;
+      for (const LaunchStructure& sl : pg.sub_ls) frac += touched_fraction(sl);
+    }
+    prog->touched_bytes += static_cast<uint64_t>(2.0 * std::ldexp(1.0, prog->n) * amp * frac);
+  }
+  if (!arena.empty()) {
+    ck(cudaMalloc(&prog->arena, arena.size()), "cudaMalloc program arena");
+    ck(cudaMemcpy(prog->arena, arena.data(), arena.size(), cudaMemcpyHostToDevice), "program arena upload");
+  }
+  // the host snapped matrices referenced by launch.m_re/m_im must follow the moved vectors
+  for (ProgramGate& pg : prog->gates) {
+    pg.launch.m_re = pg.ls.sub_re.data();
+    pg.launch.m_im = pg.ls.sub_im.data();
+  }
+  ck(cudaEventCreate(&prog->ev0), "event");
+  ck(cudaEventCreate(&prog->ev1), "event");
+  prog->planning_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return prog;
+}
+
 }  // namespace
 
 // ================================================================ C ABI ===
@@ -1408,55 +1463,7 @@ int tsg_program_create(tsg_ctx* ctx, const tsc_circuit* fused, double zero_tol, 
   TSG_TRY({
     require(ctx && fused && out, "null argument");
     require(precision_bits == 64 || precision_bits == 32, "precision_bits must be 64 or 32");
-    use_device(ctx);
-    const auto t0 = std::chrono::steady_clock::now();
-    auto prog = std::make_unique<tsg_program>();
-    prog->ctx = ctx;
-    prog->n = fused->c.n_qubits;
-    prog->prec = precision_bits;
-    std::vector<unsigned char> arena;
-    const uint64_t amp = precision_bits == 64 ? 16 : 8;
-    for (const Gate& g : fused->c.gates) {
-      ProgramGate pg;
-      pg.plan = plan_kernel(g, prog->n, 0, zero_tol, one_tol, false);
-      pg.ls = precision_bits == 64 ? pg.plan.launch : derive_launch(pg.plan, nullptr, precision_bits);
-      pg.launch = make_launch(pg.plan, pg.ls);
-      if (needs_tile_matrix(pg.launch, precision_bits)) {
-        const auto bytes = tile_matrix_bytes(pg.ls, pg.launch);
-        pg.mat_offset = (arena.size() + 255) & ~size_t{255};
-        arena.resize(pg.mat_offset + bytes.size());
-        std::copy(bytes.begin(), bytes.end(), arena.begin() + pg.mat_offset);
-        pg.has_mat = true;
-      }
-      prog->total_ops += pg.plan.profile.op_count;
-      prog->gates.push_back(std::move(pg));
-    }
-    plan_steps(prog.get(), arena);
-    for (const ProgramStep& step : prog->steps) {  // one launch per step (block splits: one per part)
-      const ProgramGate& pg = prog->gates[step.gate];
-      const bool split = step.kind == kStepGate && !pg.subs.empty();
-      prog->launches += split ? pg.subs.size() : 1;
-      prog->bytes += 2 * (uint64_t{1} << prog->n) * amp;
-      double frac = step.kind != kStepGate ? 1.0 : touched_fraction(pg.ls);
-      if (split) {
-        frac = 0.0;
-        for (const LaunchStructure& sl : pg.sub_ls) frac += touched_fraction(sl);
-      }
-      prog->touched_bytes += static_cast<uint64_t>(2.0 * std::ldexp(1.0, prog->n) * amp * frac);
-    }
-    if (!arena.empty()) {
-      ck(cudaMalloc(&prog->arena, arena.size()), "cudaMalloc program arena");
-      ck(cudaMemcpy(prog->arena, arena.data(), arena.size(), cudaMemcpyHostToDevice), "program arena upload");
-    }
-    // the host snapped matrices referenced by launch.m_re/m_im must follow the moved vectors
-    for (ProgramGate& pg : prog->gates) {
-      pg.launch.m_re = pg.ls.sub_re.data();
-      pg.launch.m_im = pg.ls.sub_im.data();
-    }
-    ck(cudaEventCreate(&prog->ev0), "event");
-    ck(cudaEventCreate(&prog->ev1), "event");
-    prog->planning_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    *out = prog.release();
+    *out = build_program(ctx, fused->c, zero_tol, one_tol, precision_bits).release();
   })
 }
 

@@ -53,6 +53,10 @@ __global__ void k_swap_halves(Real* __restrict__ a, Real* __restrict__ c, uint64
 struct PreparedOp {
   bool swap = false;
   bool skip = false;
+  // local gates run as programs (tile passes, block splits): the first op of
+  // a run of local gates holds the run's program, the others are in_seg
+  tsg_program* prog = nullptr;
+  bool in_seg = false;
   std::vector<std::pair<int, int>> swaps;
   KernelPlan plan;
   LaunchStructure ls;
@@ -66,16 +70,27 @@ struct PreparedRank {
   void* arena = nullptr;
   ~PreparedRank() {
     if (arena) cudaFree(arena);
+    for (PreparedOp& po : ops)
+      if (po.prog) tsg_program_destroy(po.prog);
   }
 };
 
-std::unique_ptr<PreparedRank> prepare_rank(const ShardPlan& plan, uint64_t rank, int prec, int device) {
+std::unique_ptr<PreparedRank> prepare_rank(const ShardPlan& plan, uint64_t rank, int prec, tsg_ctx* ctx) {
   auto pr = std::make_unique<PreparedRank>();
   std::vector<unsigned char> arena;
   const int nl = plan.n_local;
+  Circuit seg;  // the open run of local gates (this rank's sub-gates)
+  seg.n_qubits = nl;
+  size_t seg_first = 0;
+  auto close_segment = [&]() {
+    if (seg.gates.empty()) return;
+    pr->ops[seg_first].prog = build_program(ctx, seg, 1e-8, 1e-8, prec).release();
+    seg.gates.clear();
+  };
   for (const ShardOp& op : plan.ops) {
     PreparedOp po;
     if (op.kind == ShardOp::Kind::Swap) {
+      close_segment();
       po.swap = true;
       po.swaps = op.swaps;
       pr->ops.push_back(std::move(po));
@@ -83,6 +98,7 @@ std::unique_ptr<PreparedRank> prepare_rank(const ShardPlan& plan, uint64_t rank,
     }
     const Gate g = op.kind == ShardOp::Kind::Local ? op.gate : rank_subgate(op, nl, rank);
     if (g.k() == 0) {  // every target global: a rank-wide phase
+      close_segment();
       const cplx v = g.matrix.at(0, 0);
       if (v == cplx(1.0, 0.0)) {
         po.skip = true;
@@ -99,39 +115,42 @@ std::unique_ptr<PreparedRank> prepare_rank(const ShardPlan& plan, uint64_t rank,
       pr->ops.push_back(std::move(po));
       continue;
     }
-    po.plan = plan_kernel(g, nl, 0, 1e-8, 1e-8, false);
-    po.ls = derive_launch(po.plan, nullptr, prec);
-    po.launch = make_launch(po.plan, po.ls);
-    po.skip = po.ls.klass == KernelClass::Identity;
-    if (!po.skip && needs_tile_matrix(po.launch, prec)) {
-      const auto bytes = tile_matrix_bytes(po.ls, po.launch);
-      po.mat_off = (arena.size() + 255) & ~size_t{255};
-      arena.resize(po.mat_off + bytes.size());
-      std::copy(bytes.begin(), bytes.end(), arena.begin() + po.mat_off);
-      po.has_mat = true;
-    }
+    if (seg.gates.empty()) seg_first = pr->ops.size();
+    else po.in_seg = true;
+    seg.gates.push_back(g);
     pr->ops.push_back(std::move(po));
   }
+  close_segment();
   for (PreparedOp& po : pr->ops) {  // pointers into the (now stable) vectors
     po.launch.m_re = po.ls.sub_re.data();
     po.launch.m_im = po.ls.sub_im.data();
   }
   if (!arena.empty()) {
-    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     ck(cudaMalloc(&pr->arena, arena.size()), "cudaMalloc shard arena");
     ck(cudaMemcpy(pr->arena, arena.data(), arena.size(), cudaMemcpyHostToDevice), "shard arena upload");
   }
   return pr;
 }
 
-void apply_prepared(const PreparedOp& po, const PreparedRank& pr, void* re, void* im, int prec, cudaStream_t s,
-                    int num_sms) {
-  if (po.skip || po.swap) return;
+// returns the kernels launched
+uint64_t apply_prepared(const PreparedOp& po, const PreparedRank& pr, tsg_state* st) {
+  if (po.skip || po.swap || po.in_seg) return 0;
+  if (po.prog) {
+    run_program(st, po.prog, nullptr);
+    return po.prog->launches;
+  }
+  const int prec = st->prec;
+  cudaStream_t s = st->stream;
+  const int num_sms = st->ctx->num_sms;
+  void* re = st->re;
+  void* im = st->im;
   tsg::GateLaunch g = po.launch;
   g.re = re;
   g.im = im;
   if (po.has_mat) g.dev_mat = static_cast<unsigned char*>(pr.arena) + po.mat_off;
   prec == 64 ? tsg::launch_gate_f64(g, s, num_sms) : tsg::launch_gate_f32(g, s, num_sms);
+  return 1;
 }
 
 // ------------------------------------------------------------ NCCL loader
@@ -248,9 +267,23 @@ int tsg_vshard_run(tsg_ctx* ctx, const tsc_shard_plan* plan, int precision_bits,
       if (tsg_state_create(ctx, nl, precision_bits, &st)) throw SimError(tsg_last_error());
       shards.emplace_back(st, tsg_state_destroy);
       if (tsg_state_upload(st, re_in + s * local, im_in + s * local)) throw SimError(tsg_last_error());
-      prep.push_back(prepare_rank(sp, s, precision_bits, ctx->device));
+      prep.push_back(prepare_rank(sp, s, precision_bits, ctx));
     }
+    // one stream orders every shard's launches and the swaps (the shards'
+    // own streams are restored before they are destroyed)
     cudaStream_t stream = shards[0]->stream;
+    std::vector<cudaStream_t> own(S);
+    for (uint64_t s = 0; s < S; ++s) {
+      own[s] = shards[s]->stream;
+      shards[s]->stream = stream;
+    }
+    struct Restore {
+      std::vector<std::unique_ptr<tsg_state, int (*)(tsg_state*)>>& sh;
+      std::vector<cudaStream_t>& own;
+      ~Restore() {
+        for (size_t s = 0; s < sh.size(); ++s) sh[s]->stream = own[s];
+      }
+    } restore{shards, own};
     cudaEvent_t e0, e1;
     ck(cudaEventCreate(&e0), "event");
     ck(cudaEventCreate(&e1), "event");
@@ -280,11 +313,7 @@ int tsg_vshard_run(tsg_ctx* ctx, const tsc_shard_plan* plan, int precision_bits,
         }
         continue;
       }
-      for (uint64_t s = 0; s < S; ++s) {
-        apply_prepared(prep[s]->ops[i], *prep[s], shards[s]->re, shards[s]->im, precision_bits, stream,
-                       ctx->num_sms);
-        launches += !prep[s]->ops[i].skip;
-      }
+      for (uint64_t s = 0; s < S; ++s) launches += apply_prepared(prep[s]->ops[i], *prep[s], shards[s].get());
     }
     ck(cudaEventRecord(e1, stream), "event");
     ck(cudaEventSynchronize(e1), "vshard sync");
@@ -387,7 +416,7 @@ int tsg_dist_run(tsg_dist* d, const tsc_shard_plan* plan, tsg_run_report* report
     use_device(d->ctx);
     auto it = d->prepared.find(plan);
     if (it == d->prepared.end())
-      it = d->prepared.emplace(plan, prepare_rank(sp, d->rank, d->st->prec, d->ctx->device)).first;
+      it = d->prepared.emplace(plan, prepare_rank(sp, d->rank, d->st->prec, d->ctx)).first;
     const PreparedRank& pr = *it->second;
     const int nl = sp.n_local;
     cudaStream_t s = d->st->stream;
@@ -397,8 +426,7 @@ int tsg_dist_run(tsg_dist* d, const tsc_shard_plan* plan, tsg_run_report* report
     for (size_t i = 0; i < sp.ops.size(); ++i) {
       const PreparedOp& po = pr.ops[i];
       if (!po.swap) {
-        apply_prepared(po, pr, d->st->re, d->st->im, d->st->prec, s, d->ctx->num_sms);
-        launches += !po.skip;
+        launches += apply_prepared(po, pr, d->st);
         continue;
       }
       ck(cudaEventRecord(d->x0, s), "event");

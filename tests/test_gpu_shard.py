@@ -33,6 +33,22 @@ def test_vshard_matches_unsharded(kind, n, depth, kmax, prec, g):
         assert rep["exchanged_bytes"] > 0
 
 
+@pytest.mark.parametrize("kind,n,depth,kmax,prec,g", [("qft", 16, 1, 5, "f64", 2), ("rqc", 16, 6, 3, "f64", 1),
+                                                      ("qaoa", 18, 3, 4, "f32", 2), ("hes", 16, 3, 5, "f32", 3)])
+def test_vshard_forced_passes(kind, n, depth, kmax, prec, g, monkeypatch):
+    """Every local run of a shard executes as a tile-pass program (forced)."""
+    monkeypatch.setenv("TSG_PASS_FORCE", "1")
+    c = ts.gen_benchmark(kind, n, depth, 7)
+    fused, _ = ts.run_fusion(c, ts.FusionConfig(k_max=kmax))
+    re, im = random_state(n, 4)
+    got_re, got_im, _ = ts.vshard_run(ts.ShardPlan(fused, g), re, im, prec)
+    monkeypatch.delenv("TSG_PASS_FORCE")
+    monkeypatch.setenv("TSG_NO_PASS", "1")
+    sv = ts.Statevector(n, prec).upload(re, im)
+    ts.run_circuit(fused, sv)
+    assert ts.compare_states(sv, (got_re, got_im)) <= (1e-10 if prec == "f64" else 1e-5)
+
+
 def test_qft_sharded_analytic():
     n, g, x = 18, 3, 0x2A5A5
     fused, _ = ts.run_fusion(ts.gen_benchmark("qft", n), ts.FusionConfig(k_max=5))
