@@ -22,13 +22,18 @@
 // k-rows of a B fragment (different runs when the targets are high) in four
 // distinct bank quarters, so each LDS.64 costs the minimum two wavefronts.
 //
-// Warp roles: warp W (the last) is the producer -- one lane issues every bulk
-// load (full[s] mbarrier, complete_tx) and bulk store (after empty[s]); warps
-// 0..W-1 only wait on full[s], run the DMMA product, synchronise among
-// themselves with a named barrier and arrive on empty[s].
+// Warp roles: warp W (the last) is the producer -- its lanes issue the bulk
+// loads of a stage (full[s] mbarrier, complete_tx) and, for ks <= 4, the bulk
+// stores of its results once empty[s] says every consumer warp is done with
+// it; warps 0..W-1 wait on full[s] and run the DMMA product.  For ks = 5 the
+// consumers arrive on empty[s] as soon as they have read the stage and store
+// their results straight from the accumulator fragments to global memory
+// (the FP64-bound case: a stage is free for the next load sooner); for
+// ks <= 4 they write the results into the stage (in place) for the bulk store.
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels_stream.cuh"
 
@@ -117,6 +122,13 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
     k_stream_dmma(const __grid_constant__ DmmaParams<Real, KS> p) {
   using S = DShape<Real, KS>;
   constexpr bool MREG = dmma_m_in_regs<KS>();
+  // ks = 5 (FP64-bound): results leave from registers so a stage frees as soon
+  // as it is read; ks <= 4 (HBM-bound): in-place smem write-back + bulk stores
+  // (full 256-byte+ runs) measured faster
+#ifndef TSG_DMMA_DIRECT_OUT_MIN_KS
+#define TSG_DMMA_DIRECT_OUT_MIN_KS 5
+#endif
+  constexpr bool kDirectOut = KS >= TSG_DMMA_DIRECT_OUT_MIN_KS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t run_len = 1u << p.L;
   const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
@@ -176,23 +188,29 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
     uint32_t j = 0;
     for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
       const int s = static_cast<int>(j % STAGES);
-      mbar_wait(&empty[s], (j / STAGES) & 1u);  // consumers wrote tile j's results
-      const uint64_t base = tile_base(tile);
-      const Real* sr = buf + (2 * s) * stage_elems;
-      const Real* si = sr + stage_elems;
-      for (int r = lane; r < p.n_runs; r += 32) {
-        bulk_s2g(p.re + base + p.roff[r], sr + r * p.run_stride, run_bytes);
-        bulk_s2g(p.im + base + p.roff[r], si + r * p.run_stride, run_bytes);
-      }
-      bulk_commit();
       const uint64_t next = tile + STAGES * step;
-      if (next < p.n_tiles) {
-        bulk_wait_read_all();  // this lane's stores have read the stage
-        __syncwarp();
+      if constexpr (kDirectOut) {
+        if (next >= p.n_tiles) break;
+        mbar_wait(&empty[s], (j / STAGES) & 1u);  // the consumers have read tile j
         load(next, s);
+      } else {
+        mbar_wait(&empty[s], (j / STAGES) & 1u);  // the consumers wrote tile j's results
+        const uint64_t base = tile_base(tile);
+        const Real* sr = buf + (2 * s) * stage_elems;
+        const Real* si = sr + stage_elems;
+        for (int r = lane; r < p.n_runs; r += 32) {
+          bulk_s2g(p.re + base + p.roff[r], sr + r * p.run_stride, run_bytes);
+          bulk_s2g(p.im + base + p.roff[r], si + r * p.run_stride, run_bytes);
+        }
+        bulk_commit();
+        if (next < p.n_tiles) {
+          bulk_wait_read_all();  // this lane's stores have read the stage
+          __syncwarp();
+          load(next, s);
+        }
       }
     }
-    bulk_wait_all();
+    if constexpr (!kDirectOut) bulk_wait_all();
     return;
   }
 
@@ -214,7 +232,12 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
   uint32_t offb[S::KST], lbb[S::NR], lbc[S::NR][2];
 #pragma unroll
   for (int k = 0; k < S::KST; ++k) offb[k] = p.soff[4 * k + lc];
+  // results go straight from the accumulator fragments to global memory:
+  // output row 8 rb + lr sits in run `run` at in-run offset `low` (smem
+  // offset run * run_stride + low), i.e. at tile base + roff[run] + low +
+  // the group's in-run base
   const uint32_t offc = p.soff[8 * rb + lr];
+  const uint64_t goffc = p.roff[offc / p.run_stride] + offc % p.run_stride;
 #pragma unroll
   for (int nb = 0; nb < S::NR; ++nb) {
     const uint32_t g0 = wg * S::GW + nb * 8;
@@ -222,6 +245,8 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
     lbc[nb][0] = dmma_group_base(p, g0 + 2 * lc);
     lbc[nb][1] = dmma_group_base(p, g0 + 2 * lc + 1);
   }
+  // no target on bit 0: groups 2c, 2c+1 are adjacent, even-aligned amplitudes
+  const bool pair_store = lbc[0][1] == lbc[0][0] + 1 && (lbc[0][0] & 1u) == 0 && (goffc & 1u) == 0;
 
   uint32_t j = 0;
   for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
@@ -259,19 +284,46 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
         if (use_s) dmma(t3[nb], fs, br + bi);
       }
     }
-    // all consumer warps have read the stage before anyone overwrites it
-    asm volatile("bar.sync 1, %0;" ::"r"(S::kThreads) : "memory");
+    if constexpr (!kDirectOut) {
+      // all consumer warps have read the stage before anyone overwrites it
+      asm volatile("bar.sync 1, %0;" ::"r"(S::kThreads) : "memory");
 #pragma unroll
-    for (int nb = 0; nb < S::NR; ++nb)
+      for (int nb = 0; nb < S::NR; ++nb)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const uint32_t a = lbc[nb][i] + offc;
-        xr[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
-        xi[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
-      }
-    fence_async_smem();  // generic-proxy writes -> async-proxy bulk store
+        for (int i = 0; i < 2; ++i) {
+          const uint32_t a = lbc[nb][i] + offc;
+          xr[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
+          xi[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
+        }
+      fence_async_smem();  // generic-proxy writes -> async-proxy bulk store
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+      continue;
+    }
+    // this warp has read the stage: release it to the producer, then write
+    // the results from registers (the stage is not written back)
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+    const uint64_t tb = tile_base(tile) + goffc;
+    if (pair_store) {  // the lane's two groups are adjacent amplitudes: one 2-element store per array
+#pragma unroll
+      for (int nb = 0; nb < S::NR; ++nb) {
+        const uint64_t a = tb + lbc[nb][0];
+        using V2 = std::conditional_t<sizeof(Real) == 8, double2, float2>;
+        *reinterpret_cast<V2*>(p.re + a) = V2{static_cast<Real>(t1[nb][0] - t2[nb][0]), static_cast<Real>(t1[nb][1] - t2[nb][1])};
+        *reinterpret_cast<V2*>(p.im + a) = V2{static_cast<Real>(t3[nb][0] - t1[nb][0] - t2[nb][0]),
+                                              static_cast<Real>(t3[nb][1] - t1[nb][1] - t2[nb][1])};
+      }
+    } else {
+#pragma unroll
+      for (int nb = 0; nb < S::NR; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const uint64_t a = tb + lbc[nb][i];
+          p.re[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
+          p.im[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
+        }
+    }
   }
 }
 

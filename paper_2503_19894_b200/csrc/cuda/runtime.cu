@@ -959,6 +959,37 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
   return pp;
 }
 
+// Contiguous region L of the DMMA stream kernel's tiles (dmma_geometry): the
+// low bits holding 2^log2g groups plus every target or control below them.
+int dmma_region(std::vector<int> qubits, int log2g) {
+  int L = log2g;
+  for (;;) {
+    int below = 0;
+    for (int q : qubits) below += q < L;
+    if (log2g + below == L) return L;
+    L = log2g + below;
+  }
+}
+
+// A block split pays (measured on RQC-30, scripts/pass_bench.py) for a 5-6
+// qubit sub-gate with ONE block qubit -- two half-sweep launches of a one
+// qubit smaller sub-gate -- unless that qubit falls inside the part's
+// contiguous tile region, where the half launches run double-size tiles.
+// Four quarter launches (two block qubits) measured slower than the DMMA
+// kernel's own zero-tile skipping.
+bool split_pays(const LaunchStructure& ls, const std::vector<LaunchStructure>& parts, int prec) {
+  if (parts.size() != 2 || parts[0].ks != ls.ks - 1) return false;
+  const int amps_log2 = prec == 64 ? 11 : 12;  // DShape tile of the DMMA kernel
+  for (const LaunchStructure& p : parts) {
+    std::vector<int> q = p.sub_targets;
+    q.insert(q.end(), p.controls.begin(), p.controls.end());
+    const int L = dmma_region(q, amps_log2 - p.ks);
+    for (int c : p.controls)
+      if (std::find(ls.controls.begin(), ls.controls.end(), c) == ls.controls.end() && c < L) return false;
+  }
+  return true;
+}
+
 // Steps of a program: tile passes (tilesim/pass.hpp) when the state holds at
 // least one tile, else per-gate launches with diagonal batches.
 void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
@@ -992,7 +1023,7 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
         ProgramGate& pg = prog->gates[step.gate];
         if (pg.ls.ks < 5) continue;
         std::vector<LaunchStructure> parts = split_blocks(pg.ls, prog->prec);
-        if (parts.size() == 1 && parts[0].ks == pg.ls.ks) continue;
+        if (!split_pays(pg.ls, parts, prog->prec)) continue;
         pg.sub_ls = std::move(parts);
         for (const LaunchStructure& sl : pg.sub_ls) {
           tsg::GateLaunch g = make_launch(pg.plan, sl);

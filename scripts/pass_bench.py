@@ -17,11 +17,11 @@ PREC = os.environ.get("PB_PREC", "f64")
 
 
 def case(name, gates):
-    if gates == "rqc":  # the 5-qubit fused gates of RQC-n (k <= 5)
+    if gates in ("rqc", "rqc4"):  # the 5- (4-) qubit fused gates of RQC-n (k <= 5)
         fused, _ = ts.run_fusion(ts.gen_benchmark("rqc", N, 20, 42), ts.FusionConfig(k_max=5))
         c = ts.Circuit(N)
         for g in fused.gates():
-            if g.k == 5:
+            if g.k == (5 if gates == "rqc" else 4):
                 c.add_matrix(g.targets, g.matrix)
     else:
         c = ts.Circuit(N)
@@ -71,6 +71,7 @@ cases = {
     "ks5 dense 20-24": [([20, 21, 22, 23, 24], "dense")],
     "ks5 diag-ish 7-11": [([7, 8, 9, 10, 11], "controlled")],
     "ks5 rqc-like": "rqc",
+    "ks4 rqc-like": "rqc4",
     "4x gen ks2 blk out": [([6, 7, 20, 21], "blockdiag2"), ([8, 9, 22, 23], "blockdiag2"), ([6, 7, 24, 25], "blockdiag2"), ([8, 9, 26, 27], "blockdiag2")],
     "4x gen ks2 blk thr": [([0, 1, 6, 7], "blockdiag2"), ([2, 3, 6, 7], "blockdiag2"), ([0, 1, 8, 9], "blockdiag2"), ([2, 3, 8, 9], "blockdiag2")],
     "4x gen ks2 blk iter": [([6, 7, 9, 10], "blockdiag2"), ([0, 1, 9, 10], "blockdiag2"), ([2, 3, 9, 10], "blockdiag2"), ([7, 8, 9, 10], "blockdiag2")],
