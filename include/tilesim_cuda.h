@@ -72,6 +72,11 @@ int tsg_state_upload(tsg_state* st, const double* re, const double* im);
 int tsg_state_download(tsg_state* st, double* re, double* im);
 int tsg_state_download_range(tsg_state* st, uint64_t begin, uint64_t count, double* re, double* im);
 int tsg_state_copy(tsg_state* dst, const tsg_state* src);
+/* QSV1 amplitude dump / load: header "QSV1", u8 precision bits
+ * (32 | 64), u8 n, 10 zero bytes; then re[2^n], im[2^n] little-endian in the
+ * state's precision.  Load requires matching precision and n. */
+int tsg_state_dump(tsg_state* st, const char* path);
+int tsg_state_load(tsg_state* st, const char* path);
 int tsg_synchronize(tsg_state* st);
 /* CUDA events on the state's stream bracketing any sequence of calls;
  * tsg_timer_end synchronizes and returns the device seconds in between. */

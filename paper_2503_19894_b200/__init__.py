@@ -127,6 +127,8 @@ _sig("tsg_state_upload", [_vp, _dp, _dp])
 _sig("tsg_state_download", [_vp, _dp, _dp])
 _sig("tsg_state_download_range", [_vp, _u64, _u64, _dp, _dp])
 _sig("tsg_state_copy", [_vp, _vp])
+_sig("tsg_state_dump", [_vp, C.c_char_p])
+_sig("tsg_state_load", [_vp, C.c_char_p])
 _sig("tsg_synchronize", [_vp])
 _sig("tsg_timer_begin", [_vp])
 _sig("tsg_timer_end", [_vp, _dp])
@@ -441,6 +443,16 @@ class Statevector:
     def amplitudes(self) -> np.ndarray:
         re, im = self.download()
         return re + 1j * im
+
+    def dump(self, path: str):
+        """QSV1 amplitude dump."""
+        _check(_lib.tsg_state_dump(self._h, os.fsencode(path)))
+        return self
+
+    def load(self, path: str):
+        """Load a QSV1 dump of the same precision and qubit count."""
+        _check(_lib.tsg_state_load(self._h, os.fsencode(path)))
+        return self
 
     def synchronize(self):
         _check(_lib.tsg_synchronize(self._h))
