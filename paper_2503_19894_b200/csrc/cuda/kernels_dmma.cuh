@@ -160,20 +160,30 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
   }
   __syncthreads();
 
-  auto tile_base = [&](uint64_t tile) {
+  auto raw_base = [&](uint64_t tile) {
     uint64_t b = 0;
 #pragma unroll
     for (int i = 0; i < kMaxMasks; ++i)
       if (i < p.n_tmask) b += (tile & p.tmask[i]) << i;
-    return (b << p.L) | p.ctrl_hi;
+    return b << p.L;
   };
+  // Tile bases in the persistent order first, first + step, ...: stepped in
+  // the masked domain (non-tile bits forced to 1 so the carry crosses them).
+  struct TileStream {
+    uint64_t raw, mask, dstep, ctrl;
+    __device__ uint64_t base() const { return raw | ctrl; }
+    __device__ void advance() { raw = ((raw | ~mask) + dstep) & mask; }
+  };
+  const TileStream stream0{raw_base(first), raw_base(p.n_tiles - 1), raw_base(step), p.ctrl_hi};
 
   if (warp == S::W) {
     // ---------------- producer warp: TMA bulk loads and stores ------------
     // Copies are spread over the 32 lanes (lane l owns runs l, l+32, ...);
     // bulk groups are per thread, so every lane waits for its own stores.
+    TileStream lstream = stream0, sstream = stream0;  // next tile to load / to store
     auto load = [&](uint64_t tile, int s) {
-      const uint64_t base = tile_base(tile);
+      const uint64_t base = lstream.base();
+      lstream.advance();
       Real* dr = buf + (2 * s) * stage_elems;
       Real* di = dr + stage_elems;
       if (lane == 0) mbar_expect_tx(&full[s], 2u * run_bytes * static_cast<uint32_t>(p.n_runs));
@@ -195,7 +205,8 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
         load(next, s);
       } else {
         mbar_wait(&empty[s], (j / STAGES) & 1u);  // the consumers wrote tile j's results
-        const uint64_t base = tile_base(tile);
+        const uint64_t base = sstream.base();
+        sstream.advance();
         const Real* sr = buf + (2 * s) * stage_elems;
         const Real* si = sr + stage_elems;
         for (int r = lane; r < p.n_runs; r += 32) {
@@ -248,6 +259,7 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
   // no target on bit 0: groups 2c, 2c+1 are adjacent, even-aligned amplitudes
   const bool pair_store = lbc[0][1] == lbc[0][0] + 1 && (lbc[0][0] & 1u) == 0 && (goffc & 1u) == 0;
 
+  TileStream cstream = stream0;  // output addresses (ks = 5)
   uint32_t j = 0;
   for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
     const int s = static_cast<int>(j % STAGES);
@@ -304,7 +316,8 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
     // the results from registers (the stage is not written back)
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
-    const uint64_t tb = tile_base(tile) + goffc;
+    const uint64_t tb = cstream.base() + goffc;
+    cstream.advance();
     if (pair_store) {  // the lane's two groups are adjacent amplitudes: one 2-element store per array
 #pragma unroll
       for (int nb = 0; nb < S::NR; ++nb) {
