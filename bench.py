@@ -143,6 +143,11 @@ def measured_peaks():
         return FALLBACK_HBM_GBS, "fallback"
 
 
+def fp64_peak_tflops(clock_info):
+    mhz = (clock_info or {}).get("sm_mhz") or 1965.0
+    return 63.6 * 148 * 2 * mhz * 1e6 / 1e12
+
+
 def build_circuits(ts, n, kmax):
     t0 = time.perf_counter()
     qft = ts.gen_benchmark("qft", n)
@@ -164,10 +169,21 @@ def breakdown(ts, progs, sv, n):
             s = float(secs[st["first_gate"]])  # a step's gates after its first one have zero-length marks
             info = prog.gate_info(st["first_gate"])
             key = st["kernel"]
-            g = groups.setdefault(key, {"seconds": 0.0, "launches": 0, "bytes": 0, "touched": 0, "gates": 0})
+            g = groups.setdefault(key, {"seconds": 0.0, "launches": 0, "bytes": 0, "touched": 0, "gates": 0,
+                                        "flops": 0})
             g["seconds"] += s
             g["launches"] += 1
             g["gates"] += st["n_gates"]
+            # algorithmic flops: 2 * op_count * 2^(n-k) per gate of the step
+            gi = st["first_gate"]
+            done = 0
+            while done < st["n_gates"]:
+                ginfo = prog.gate_info(gi)
+                gi += 1
+                if ginfo["kernel"] == "identity":
+                    continue
+                g["flops"] += 2 * ginfo["op_count"] * ginfo["loop_count"]
+                done += 1
             g["bytes"] += 2 * (1 << n) * amp
             frac = info["touched_fraction"] if st["kind"] == "gate" else 1.0
             g["touched"] += int(2 * (1 << n) * amp * frac)
@@ -351,9 +367,17 @@ def run_ours(args):
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": dom_name, "peak_source": peak_kind,
-                     "per_launch_bytes": 2 * (1 << n) * 16},
+                     "per_launch_bytes": 2 * (1 << n) * 16,
+                     # the same kernel against the FP64 tensor (DMMA) roof: SPEC op_count flops
+                     # (2 * op_count * 2^(n-k) per gate) / time vs the measured DMMA peak
+                     # (63.6 MAC/clk/SM, profiles/r01/microbench.log) at the run's SM clock
+                     "fp64": {"achieved_tflops": dom["flops"] / dom["seconds"] / 1e12,
+                              "peak_tflops": fp64_peak_tflops(clock_info),
+                              "frac": dom["flops"] / dom["seconds"] / 1e12 / fp64_peak_tflops(clock_info),
+                              "peak_source": "measured DMMA.8x8x4 rate x 148 SMs x sampled SM clock"}},
         "kernels": {k: {"seconds_per_step": v["seconds"], "launches": v["launches"], "gates": v["gates"],
                         "GBps_algorithmic": v["bytes"] / v["seconds"] / 1e9,
+                        "TFLOPs_algorithmic": v["flops"] / v["seconds"] / 1e12,
                         "GBps_touched": v["touched"] / v["seconds"] / 1e9} for k, v in groups.items()},
         "parity": {"qft30_analytic_maxdiff_64_samples": maxdiff, "qft30_norm": qft_norm},
         "clocks": clock_info,
