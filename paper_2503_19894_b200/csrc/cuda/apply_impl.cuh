@@ -304,7 +304,6 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   p.n_tiles = uint64_t{1} << tile_bits;
   p.L = L;
   p.n_runs = 1 << n_run;
-  p.run_stride = (1u << L) + kRunPadBytes / sizeof(Real);
   const uint64_t low_mask = (uint64_t{1} << L) - 1;
   p.ctrl_hi = g.fixed_or & ~low_mask;
   p.ctrl_lo = static_cast<uint32_t>(g.fixed_or & low_mask);
@@ -318,6 +317,7 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
     for (int b = 0; b < n_run; ++b) o |= static_cast<uint64_t>((r >> b) & 1) << run_pos[b];
     p.roff[r] = o;
   }
+  uint32_t low_of[1 << KS], run_of[1 << KS];
   for (int j = 0; j < (1 << KS); ++j) {
     uint32_t low = 0, run = 0;
     int hb = 0;
@@ -326,7 +326,49 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
       if (st[b] < L) low |= bit << st[b];
       else run |= bit << hb++;
     }
-    p.soff[j] = run * p.run_stride + low;
+    low_of[j] = low;
+    run_of[j] = run;
+    p.goff[j] = p.roff[run] + low;
+  }
+  // Shared-memory layout: runs padded by kRunPadBytes; a long run whose B
+  // fragments (8 groups x 4 elements per warp load) would pile onto few
+  // banks is cut into padded 256-byte chunks instead (e.g. targets 0..4: all
+  // groups 256 bytes apart).  Pick the layout with fewer wavefronts.
+  const uint32_t pad = kRunPadBytes / sizeof(Real);
+  auto layout = [&](int chunk_log2, uint32_t* chunk_stride, uint32_t* run_stride) {
+    *chunk_stride = (1u << chunk_log2) + pad;
+    *run_stride = chunk_log2 == L ? *chunk_stride : (1u << (L - chunk_log2)) * *chunk_stride;
+  };
+  auto wavefronts = [&](int chunk_log2) {  // B-fragment load of warp 0, k-step 0
+    uint32_t cs, rs;
+    layout(chunk_log2, &cs, &rs);
+    auto padw = [&](uint32_t w) { return (w >> chunk_log2) * cs + (w & ((1u << chunk_log2) - 1)); };
+    int worst = 0;
+    for (int k = 0; k < (1 << KS) / 4; ++k) {
+      int words[32] = {0};
+      for (int lane = 0; lane < 32; ++lane) {
+        const int lr = lane >> 2, lc = lane & 3;
+        uint32_t gpos = 0;
+        for (int i = 0; i < p.n_gmask; ++i) gpos += (static_cast<uint32_t>(lr) & p.gmask[i]) << i;
+        gpos |= p.ctrl_lo;
+        const int j = 4 * k + lc;
+        const uint32_t a = run_of[j] * rs + padw(low_of[j]) + padw(gpos);  // element offset (Real units)
+        const uint32_t w = a * (sizeof(Real) / 4);
+        for (uint32_t b = 0; b < sizeof(Real) / 4; ++b) ++words[(w + b) % 32];
+      }
+      for (int b = 0; b < 32; ++b) worst = std::max(worst, words[b]);
+    }
+    return worst;
+  };
+  p.chunk_log2 = L;
+  const int chunk = sizeof(Real) == 8 ? 5 : 6;  // 256-byte chunks
+  // only for ks = 5, whose stages are loaded and never bulk-stored: more,
+  // smaller bulk copies measured slower for the HBM-bound ks <= 4 kernels
+  if (KS >= 5 && L > chunk && wavefronts(chunk) < wavefronts(L)) p.chunk_log2 = chunk;
+  layout(p.chunk_log2, &p.chunk_stride, &p.run_stride);
+  for (int j = 0; j < (1 << KS); ++j) {
+    const uint32_t w = low_of[j];
+    p.soff[j] = run_of[j] * p.run_stride + (w >> p.chunk_log2) * p.chunk_stride + (w & ((1u << p.chunk_log2) - 1));
   }
   // Two CTAs per SM beat deeper pipelines (measured): 3 stages when two CTAs
   // still fit in shared memory, else 2.

@@ -82,11 +82,17 @@ struct DmmaParams {
   int n_tmask;
   int L;
   int n_runs;
-  uint32_t run_stride;  // 2^L + kRunPadBytes / sizeof(Real)
+  uint32_t run_stride;  // shared-memory elements per run (padded)
+  // A run is stored as 2^(L - chunk_log2) chunks of 2^chunk_log2 amplitudes,
+  // chunk_stride elements apart (chunk_log2 = L: one padded chunk per run).
+  // Chunking spreads runs whose groups would all start on the same bank.
+  int chunk_log2;
+  uint32_t chunk_stride;
   uint32_t gmask[kMaxMasks];
   int n_gmask;
   uint64_t roff[1 << KS];  // global offset of run r
-  uint32_t soff[1 << KS];  // shared offset of element j (padded runs)
+  uint32_t soff[1 << KS];  // shared offset of element j (padded runs and chunks)
+  uint64_t goff[1 << KS];  // global offset of element j from the tile base
   uint32_t nzblk[3];       // bit (rb * KST + ks): block of Mr / Mi / Ms is nonzero
 };
 
@@ -96,13 +102,20 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// in-run position of group g (low targets zero, low controls at their value)
 template <typename Real, int KS>
-__device__ __forceinline__ uint32_t dmma_group_base(const DmmaParams<Real, KS>& p, uint32_t g) {
+__device__ __forceinline__ uint32_t dmma_group_pos(const DmmaParams<Real, KS>& p, uint32_t g) {
   uint32_t b = 0;
 #pragma unroll
   for (int i = 0; i < kMaxMasks; ++i)
     if (i < p.n_gmask) b += (g & p.gmask[i]) << i;
   return b | p.ctrl_lo;
+}
+
+// shared-memory offset of an in-run position (chunk padding; additive over disjoint bits)
+template <typename Real, int KS>
+__device__ __forceinline__ uint32_t dmma_pad(const DmmaParams<Real, KS>& p, uint32_t w) {
+  return (w >> p.chunk_log2) * p.chunk_stride + (w & ((1u << p.chunk_log2) - 1));
 }
 
 // M fragments live in registers for ks <= 4; for ks = 5 they are staged in
@@ -130,7 +143,6 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
 #endif
   constexpr bool kDirectOut = KS >= TSG_DMMA_DIRECT_OUT_MIN_KS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const uint32_t run_len = 1u << p.L;
   const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
   double* mfrag = reinterpret_cast<double*>(smem_raw);  // [3][KST][RB][32] when !MREG
   Real* buf = reinterpret_cast<Real*>(smem_raw + dmma_m_smem_bytes<KS>());  // [STAGES][2][stage_elems]
@@ -140,7 +152,9 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const uint32_t run_bytes = run_len * sizeof(Real);
+  const int chunk_shift = p.L - p.chunk_log2;  // chunks per run = 2^chunk_shift
+  const int n_chunks = p.n_runs << chunk_shift;
+  const uint32_t chunk_bytes = (1u << p.chunk_log2) * sizeof(Real);
   const uint64_t first = blockIdx.x, step = gridDim.x;
 
   if (tid == 0) {
@@ -186,11 +200,14 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
       lstream.advance();
       Real* dr = buf + (2 * s) * stage_elems;
       Real* di = dr + stage_elems;
-      if (lane == 0) mbar_expect_tx(&full[s], 2u * run_bytes * static_cast<uint32_t>(p.n_runs));
+      if (lane == 0) mbar_expect_tx(&full[s], 2u * chunk_bytes * static_cast<uint32_t>(n_chunks));
       __syncwarp();
-      for (int r = lane; r < p.n_runs; r += 32) {
-        bulk_g2s(dr + r * p.run_stride, p.re + base + p.roff[r], run_bytes, &full[s]);
-        bulk_g2s(di + r * p.run_stride, p.im + base + p.roff[r], run_bytes, &full[s]);
+      for (int c = lane; c < n_chunks; c += 32) {
+        const int r = c >> chunk_shift, q = c & ((1 << chunk_shift) - 1);
+        const uint32_t so = r * p.run_stride + q * p.chunk_stride;
+        const uint64_t go = base + p.roff[r] + (static_cast<uint64_t>(q) << p.chunk_log2);
+        bulk_g2s(dr + so, p.re + go, chunk_bytes, &full[s]);
+        bulk_g2s(di + so, p.im + go, chunk_bytes, &full[s]);
       }
     };
     for (int s = 0; s < STAGES; ++s)
@@ -209,9 +226,12 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
         sstream.advance();
         const Real* sr = buf + (2 * s) * stage_elems;
         const Real* si = sr + stage_elems;
-        for (int r = lane; r < p.n_runs; r += 32) {
-          bulk_s2g(p.re + base + p.roff[r], sr + r * p.run_stride, run_bytes);
-          bulk_s2g(p.im + base + p.roff[r], si + r * p.run_stride, run_bytes);
+        for (int c = lane; c < n_chunks; c += 32) {
+          const int r = c >> chunk_shift, q = c & ((1 << chunk_shift) - 1);
+          const uint32_t so = r * p.run_stride + q * p.chunk_stride;
+          const uint64_t go = base + p.roff[r] + (static_cast<uint64_t>(q) << p.chunk_log2);
+          bulk_s2g(p.re + go, sr + so, chunk_bytes);
+          bulk_s2g(p.im + go, si + so, chunk_bytes);
         }
         bulk_commit();
         if (next < p.n_tiles) {
@@ -243,21 +263,24 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
   uint32_t offb[S::KST], lbb[S::NR], lbc[S::NR][2];
 #pragma unroll
   for (int k = 0; k < S::KST; ++k) offb[k] = p.soff[4 * k + lc];
-  // results go straight from the accumulator fragments to global memory:
-  // output row 8 rb + lr sits in run `run` at in-run offset `low` (smem
-  // offset run * run_stride + low), i.e. at tile base + roff[run] + low +
-  // the group's in-run base
+  // output row 8 rb + lr: shared offset offc (ks <= 4 write-back) and global
+  // offset goffc from the tile base (ks = 5 stores from registers); a
+  // group's base is padded for shared memory (lbb, lbc) and raw for global
+  // memory (gbc)
   const uint32_t offc = p.soff[8 * rb + lr];
-  const uint64_t goffc = p.roff[offc / p.run_stride] + offc % p.run_stride;
+  const uint64_t goffc = p.goff[8 * rb + lr];
+  uint32_t gbc[S::NR][2];
 #pragma unroll
   for (int nb = 0; nb < S::NR; ++nb) {
     const uint32_t g0 = wg * S::GW + nb * 8;
-    lbb[nb] = dmma_group_base(p, g0 + lr);
-    lbc[nb][0] = dmma_group_base(p, g0 + 2 * lc);
-    lbc[nb][1] = dmma_group_base(p, g0 + 2 * lc + 1);
+    lbb[nb] = dmma_pad(p, dmma_group_pos(p, g0 + lr));
+    gbc[nb][0] = dmma_group_pos(p, g0 + 2 * lc);
+    gbc[nb][1] = dmma_group_pos(p, g0 + 2 * lc + 1);
+    lbc[nb][0] = dmma_pad(p, gbc[nb][0]);
+    lbc[nb][1] = dmma_pad(p, gbc[nb][1]);
   }
   // no target on bit 0: groups 2c, 2c+1 are adjacent, even-aligned amplitudes
-  const bool pair_store = lbc[0][1] == lbc[0][0] + 1 && (lbc[0][0] & 1u) == 0 && (goffc & 1u) == 0;
+  const bool pair_store = gbc[0][1] == gbc[0][0] + 1 && (gbc[0][0] & 1u) == 0 && (goffc & 1u) == 0;
 
   TileStream cstream = stream0;  // output addresses (ks = 5)
   uint32_t j = 0;
@@ -321,7 +344,7 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
     if (pair_store) {  // the lane's two groups are adjacent amplitudes: one 2-element store per array
 #pragma unroll
       for (int nb = 0; nb < S::NR; ++nb) {
-        const uint64_t a = tb + lbc[nb][0];
+        const uint64_t a = tb + gbc[nb][0];
         using V2 = std::conditional_t<sizeof(Real) == 8, double2, float2>;
         *reinterpret_cast<V2*>(p.re + a) = V2{static_cast<Real>(t1[nb][0] - t2[nb][0]), static_cast<Real>(t1[nb][1] - t2[nb][1])};
         *reinterpret_cast<V2*>(p.im + a) = V2{static_cast<Real>(t3[nb][0] - t1[nb][0] - t2[nb][0]),
@@ -332,7 +355,7 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
       for (int nb = 0; nb < S::NR; ++nb)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const uint64_t a = tb + lbc[nb][i];
+          const uint64_t a = tb + gbc[nb][i];
           p.re[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
           p.im[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
         }
