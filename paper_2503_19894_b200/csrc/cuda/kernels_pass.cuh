@@ -384,16 +384,24 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
   const int nT = ops[o].ks, nI = ops[o].log2_groups, nX = ops[o].log2_rsplit;
   ++o;
   // DiagT: one factor per thread (the loads of consecutive ops are independent)
-  Real ftr = Real(1), fti = Real(0);
-#pragma unroll 4
-  for (int t = 0; t < nT; ++t) {
-    const PassOp& op = ops[o + t];
-    const uint32_t tc = tcs[o + t];
-    const uint32_t tv = blob[op.aux_off + tid];
+  // two interleaved partial products halve the dependent multiply chain
+  Real ftr = Real(1), fti = Real(0), f2r = Real(1), f2i = Real(0);
+  int t = 0;
+  for (; t + 1 < nT; t += 2) {
+    const PassOp& op0 = ops[o + t];
+    const PassOp& op1 = ops[o + t + 1];
     // inactive (tc = ~0 or tv = 0xff) selects the identity entry 2^ks (<= 128)
-    const R2 d = diag_entry<Real>(op, blob, min(tc | tv, 1u << op.ks));
+    const R2 d0 = diag_entry<Real>(op0, blob, min(tcs[o + t] | blob[op0.aux_off + tid], 1u << op0.ks));
+    const R2 d1 = diag_entry<Real>(op1, blob, min(tcs[o + t + 1] | blob[op1.aux_off + tid], 1u << op1.ks));
+    cmul_acc(ftr, fti, d0.x, d0.y);
+    cmul_acc(f2r, f2i, d1.x, d1.y);
+  }
+  if (t < nT) {
+    const PassOp& op = ops[o + t];
+    const R2 d = diag_entry<Real>(op, blob, min(tcs[o + t] | blob[op.aux_off + tid], 1u << op.ks));
     cmul_acc(ftr, fti, d.x, d.y);
   }
+  if (nT > 1) cmul_acc(ftr, fti, f2r, f2i);
   o += nT;
   // DiagI: factor of register index i = tid, computed by threads tid < R
   if (nI > 0) {
@@ -592,8 +600,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
         } else if (o > 0) {
           consumer_bar();  // after shared-memory ops: their writes are visible
         }
-        xt = 0;
-        for (int m = 0; m < op.n_xmask; ++m) xt += (static_cast<uint32_t>(tid) & op.xmask[m]) << m;
+        xt = reinterpret_cast<const uint32_t*>(blob + op.aux_off)[tid];  // host-built per-thread coordinate
         const uint32_t at0 = pass_addr<L, S::kStride>(xt);
         constexpr int kBits = __builtin_ctz(R);
         uint32_t pd[kBits];  // padded offset of each register position (additive over disjoint bits)

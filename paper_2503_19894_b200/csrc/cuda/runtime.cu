@@ -569,13 +569,22 @@ tsg::PassOp blank_op(int kind) {
 }
 
 template <typename Real>
-tsg::PassOp build_layout_op(const PassGeom& g) {
+tsg::PassOp build_layout_op(const PassGeom& g, std::vector<unsigned char>& data) {
   tsg::PassOp op = blank_op(tsg::kPassLayout);
   std::vector<int> P = g.P;
   uint64_t gm[16];
   if (g.r + 1 > 6) throw SimError("pass: too many register positions");
   op.n_xmask = tsg::insertion_masks(P.data(), g.r, g.M - g.r, gm);
   for (int m = 0; m < op.n_xmask; ++m) op.xmask[m] = static_cast<uint32_t>(gm[m]);
+  // per-thread tile coordinate of the thread part (deposit of tid over the
+  // non-register positions), looked up instead of recomputed every tile
+  pad16(data);
+  op.aux_off = static_cast<int32_t>(data.size());
+  for (uint32_t t = 0; t < static_cast<uint32_t>(tsg::kPassThreads); ++t) {
+    uint64_t x = 0;
+    for (int m = 0; m < op.n_xmask; ++m) x += (t & gm[m]) << m;
+    append_pod(data, static_cast<uint32_t>(x));
+  }
   for (int k = 0; k < g.r; ++k) op.dep[k] = static_cast<uint32_t>(padded_offset<Real>(1u << g.P[k], g.L));
   return op;
 }
@@ -880,7 +889,7 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
     while (first < ng && !reg_ok[first]) ++first;
     g.P = first < ng ? choose_layout(mixed[first], upcoming(first + 1), g.r, M, L)
                      : choose_layout({}, {}, g.r, M, L);
-    ops.push_back(build_layout_op<Real>(g));
+    ops.push_back(build_layout_op<Real>(g, data));
   }
   std::vector<tsg::PassOp> cls[3];  // the open run of diagonal ops, by class
   auto flush_run = [&]() {
@@ -908,7 +917,7 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
       for (int p : mixed[i]) fits = fits && g.reg_bit(p) >= 0;
       if (!fits) {
         g.P = choose_layout(mixed[i], upcoming(i + 1), g.r, M, L);
-        ops.push_back(build_layout_op<Real>(g));
+        ops.push_back(build_layout_op<Real>(g, data));
       }
       ops.push_back(build_reg_op<Real>(ls, g, data));
     } else {
@@ -928,7 +937,11 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
   }
   const size_t data_base = (size_t{8} << nh) + ops.size() * sizeof(tsg::PassOp);
   for (tsg::PassOp& op : ops) {
-    if (op.kind == tsg::kPassLayout || op.kind == tsg::kPassRun) continue;
+    if (op.kind == tsg::kPassRun) continue;
+    if (op.kind == tsg::kPassLayout) {
+      op.aux_off += static_cast<int32_t>(data_base);
+      continue;
+    }
     op.data_off += static_cast<int32_t>(data_base);
     if (op.kind != tsg::kPassDiagI) op.aux_off += static_cast<int32_t>(data_base);
   }

@@ -171,7 +171,7 @@ std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int
 
   std::vector<int> cur;      // gates of the open pass
   std::vector<int> cur_high; // mixed qubits >= L of the open pass
-  int cur_bytes = run_table;
+  int cur_bytes = run_table + 4 * 1024;  // room for a few LAYOUT records + per-thread tables (1 KiB each)
 
   auto emit_standalone = [&](int g) {
     PassStep s;
@@ -200,7 +200,7 @@ std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int
     }
     cur.clear();
     cur_high.clear();
-    cur_bytes = run_table;
+    cur_bytes = run_table + 4 * 1024;
   };
 
   for (int i = 0; i < static_cast<int>(gates.size()); ++i) {
