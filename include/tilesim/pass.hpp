@@ -24,7 +24,7 @@ struct PassConfig {
   int run_log2 = 5;      // L: contiguous run length = 2^L (>= 256 bytes per array)
   int max_ops = 96;      // ops per pass
   int max_gen_ks = 4;    // widest non-diagonal sub-gate inside a pass
-  int max_blob = 36 * 1024;  // bytes of run offsets + op table + op data
+  int max_blob = 32 * 1024;  // bytes of run offsets + op table + op data
   int amp_real_bytes = 8;    // sizeof(Real) of the state
   // B200 cost model of a pass, in units of one state sweep (2 * 2^n * B_amp
   // bytes at HBM speed), measured with scripts/pass_bench.py at n = 28

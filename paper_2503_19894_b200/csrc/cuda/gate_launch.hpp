@@ -94,7 +94,9 @@ std::string kernel_name(const GateLaunch& g, int precision_bits);
 constexpr int kPassThreads = 256;  // threads per CTA, two CTAs per SM
 constexpr int kPassLogThreads = 8;
 constexpr int kPassMaxOps = 128;  // ops + RUN headers per pass
-constexpr int kPassMaxBlob = 36 * 1024;  // run offsets + op table + op data, staged in smem
+constexpr int kPassMaxBlob = 32 * 1024;  // run offsets + op table + op data, staged in smem
+constexpr int kPassMaxGEntries = 128;    // combined diagonal-group entries per run (smem scratch)
+constexpr int kPassMaxSig = 6;           // signature bits of a diagonal group
 constexpr int kPassPadBytes = 32;        // padding between runs in shared memory (bank spread)
 
 // Register layouts.  Each consumer thread holds R = 2^r = 2^M / kPassThreads
@@ -103,8 +105,13 @@ constexpr int kPassPadBytes = 32;        // padding between runs in shared memor
 // deposit(i over P), i < R.  Ops run on those registers; only a layout
 // change or a wide op moves the tile through shared memory.
 //   Layout  store the registers (old layout), barrier, load the new layout
-//   Run     header of a run of diagonal ops, ordered by class w.r.t. the
-//           current layout (diagonal gates commute):
+//   Run     header of a run of diagonal ops (diagonal gates commute).  Ops
+//           are grouped by signature -- the in-tile positions their targets
+//           and controls touch (at most 6): per tile, the CTA builds each
+//           group's combined table over its signature once (out-of-tile
+//           bits and controls are tile constants), then every amplitude
+//           takes one lookup per group.  Ops with wider signatures follow
+//           as per-op classes w.r.t. the current layout:
 //     DiagT  in-tile index bits only on thread positions: one factor per thread
 //     DiagI  only on register positions: one factor per register index i,
 //            shared through shared memory
@@ -125,6 +132,8 @@ enum PassOpKind : int32_t {
   kPassRPerm = 6,
   kPassSGen = 7,
   kPassSPerm = 8,
+  kPassDGroup = 9,   // RUN group header: diagonal ops sharing an in-tile signature
+  kPassDMember = 10, // member of the preceding DGroup
 };
 
 struct PassOp {  // 192 bytes, built on the host, read from shared memory

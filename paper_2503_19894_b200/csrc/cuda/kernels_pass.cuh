@@ -71,7 +71,7 @@ struct PassShape {
   static constexpr int kIter = (1 << M) / kPassThreads;  // amplitudes per thread (register layout)
   static constexpr int kIterBits = M - kPassLogThreads;
   static_assert(kIter >= 1 && kIterBits <= 8, "tile / thread geometry");
-  static constexpr size_t kFiBytes = 2 * kIter * 2 * sizeof(Real);       // DiagI factors, double-buffered
+  static constexpr size_t kFiBytes = 2 * kPassMaxGEntries * 2 * sizeof(Real);  // group tables, double-buffered
   static constexpr size_t kTcBytes = 2 * kPassMaxOps * sizeof(uint32_t);  // per-tile op constants, double-buffered
   static constexpr size_t smem_bytes(int blob_bytes, int stages) {
     return ((static_cast<size_t>(blob_bytes) + 127) & ~size_t{127}) +
@@ -374,17 +374,69 @@ __device__ __forceinline__ typename Real2Of<Real>::T diag_entry(const PassOp& op
   return reinterpret_cast<const typename Real2Of<Real>::T*>(blob + op.data_off)[j];
 }
 
-// The RUN header at ops[o] is followed by nT DiagT, nI DiagI and nX DiagX
-// ops (classes w.r.t. the current layout).  Returns the op after the run.
+// The RUN header at ops[o] (ks = groups, log2_groups = per-op DiagT count,
+// log2_rsplit = per-op DiagX count) is followed by its groups (a DGroup
+// header and its DMember ops each), then the per-op DiagT and DiagX ops.
+// Groups: every thread builds some entries of the groups' combined tables
+// (product of the members' factors at that signature index), a barrier,
+// then every amplitude multiplies one entry per group.  Returns the op after
+// the run.  gtab: this run's table scratch (kPassMaxGEntries entries).
 template <typename Real, int R>
 __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const unsigned char* blob, const uint32_t* tcs,
-                                             int tid, Real (&ar)[R], Real (&ai)[R], typename Real2Of<Real>::T* fi_tab) {
+                                             int tid, Real (&ar)[R], Real (&ai)[R], typename Real2Of<Real>::T* gtab) {
   using R2 = typename Real2Of<Real>::T;
   constexpr int kBits = __builtin_ctz(R);
-  const int nT = ops[o].ks, nI = ops[o].log2_groups, nX = ops[o].log2_rsplit;
+  const int n_groups = ops[o].ks, nT = ops[o].log2_groups, nX = ops[o].log2_rsplit;
   ++o;
-  // DiagT: one factor per thread (the loads of consecutive ops are independent)
-  // two interleaved partial products halve the dependent multiply chain
+  if (n_groups > 0) {
+    // build: entry e of group g = product over members (inactive controls skip)
+    int og = o;
+    for (int g = 0; g < n_groups; ++g) {
+      const PassOp& gh = ops[og];
+      const int sbits = gh.ks, m = gh.log2_groups;
+      for (int e = tid; e < (1 << sbits); e += kPassThreads) {
+        // two interleaved partial products halve the dependent multiply chain
+        Real fr[2] = {Real(1), Real(1)}, fi[2] = {Real(0), Real(0)};
+        for (int t = 1; t <= m; ++t) {
+          const PassOp& mo = ops[og + t];
+          const uint32_t tc = tcs[og + t];
+          if (tc == ~0u || (static_cast<uint32_t>(e) & mo.ictl_mask) != mo.ictl_val) continue;
+          uint32_t jj = tc;
+#pragma unroll
+          for (int k = 0; k < kPassMaxSig; ++k)
+            if (((e >> k) & 1) && k < sbits) jj |= mo.dep[k];
+          const R2 d = diag_entry<Real>(mo, blob, jj);
+          cmul_acc(fr[t & 1], fi[t & 1], d.x, d.y);
+        }
+        cmul_acc(fr[0], fi[0], fr[1], fi[1]);
+        gtab[gh.data_off + e] = R2{fr[0], fi[0]};
+      }
+      og += 1 + m;
+    }
+    consumer_bar();
+    // apply: one entry per group and amplitude
+    og = o;
+    for (int g = 0; g < n_groups; ++g) {
+      const PassOp& gh = ops[og];
+      const uint32_t tv = blob[gh.aux_off + tid];
+      uint32_t dep[kBits > 0 ? kBits : 1];
+#pragma unroll
+      for (int k = 0; k < kBits; ++k) dep[k] = gh.dep[k];
+      const R2* gt = gtab + gh.data_off;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        uint32_t idx = tv;
+#pragma unroll
+        for (int k = 0; k < kBits; ++k)
+          if ((i >> k) & 1) idx |= dep[k];
+        const R2 f = gt[idx];
+        cmul_acc(ar[i], ai[i], f.x, f.y);
+      }
+      og += 1 + gh.log2_groups;
+    }
+    o = og;
+  }
+  // DiagT: one factor per thread (two interleaved partial products)
   Real ftr = Real(1), fti = Real(0), f2r = Real(1), f2i = Real(0);
   int t = 0;
   for (; t + 1 < nT; t += 2) {
@@ -401,30 +453,14 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
     const R2 d = diag_entry<Real>(op, blob, min(tcs[o + t] | blob[op.aux_off + tid], 1u << op.ks));
     cmul_acc(ftr, fti, d.x, d.y);
   }
-  if (nT > 1) cmul_acc(ftr, fti, f2r, f2i);
-  o += nT;
-  // DiagI: factor of register index i = tid, computed by threads tid < R
-  if (nI > 0) {
-    if (tid < R) {
-      Real fir = Real(1), fii = Real(0);
-#pragma unroll 4
-      for (int t = 0; t < nI; ++t) {
-        const PassOp& op = ops[o + t];
-        const uint32_t tc = tcs[o + t];
-        uint32_t j = tc;
+  if (nT > 0) {
+    if (nT > 1) cmul_acc(ftr, fti, f2r, f2i);
 #pragma unroll
-        for (int k = 0; k < kBits; ++k)
-          if ((tid >> k) & 1) j |= op.dep[k];
-        const bool act = (static_cast<uint32_t>(tid) & op.ictl_mask) == op.ictl_val;
-        const R2 d = diag_entry<Real>(op, blob, min(act ? j : ~0u, 1u << op.ks));
-        cmul_acc(fir, fii, d.x, d.y);
-      }
-      fi_tab[tid] = R2{fir, fii};
-    }
-    o += nI;
+    for (int i = 0; i < R; ++i) cmul_acc(ar[i], ai[i], ftr, fti);
   }
+  o += nT;
   // DiagX: amplitude by amplitude, k_diag's update
-  for (int t = 0; t < nX; ++t, ++o) {
+  for (int x = 0; x < nX; ++x, ++o) {
     const PassOp& op = ops[o];
     const uint32_t tc = tcs[o];
     const uint32_t tv = blob[op.aux_off + tid];
@@ -445,19 +481,6 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
       ar[i] = fma(d.x, r0, -d.y * i0);
       ai[i] = fma(d.x, i0, d.y * r0);
     }
-  }
-  if (nI > 0) {  // uniform: every consumer thread read the same header
-    consumer_bar();
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const R2 f = fi_tab[i];
-      Real gr = ftr, gi = fti;
-      cmul_acc(gr, gi, f.x, f.y);
-      cmul_acc(ar[i], ai[i], gr, gi);
-    }
-  } else if (nT > 0) {
-#pragma unroll
-    for (int i = 0; i < R; ++i) cmul_acc(ar[i], ai[i], ftr, fti);
   }
   return o;
 }
@@ -562,7 +585,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
   Real ar[R], ai[R];
   uint32_t at[R];      // padded shared-memory offsets of the registers (current layout)
   uint32_t xt = 0;     // tile coordinate of the thread part of the current layout
-  uint32_t irun = 0;   // runs with DiagI ops so far (fi_tab double-buffering)
+  uint32_t irun = 0;   // runs with diagonal groups so far (table double-buffering)
   uint32_t j = 0;
   for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
     const int s = static_cast<int>(j % STAGES);
@@ -619,10 +642,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
         in_smem = false;
         ++o;
       } else if (kind == kPassRun) {
-        // DiagI factors alternate buffers run by run (each such run has a barrier)
-        const bool has_i = op.log2_groups > 0;
-        o = pass_diag_run<Real, R>(ops, o, blob, tcs, tid, ar, ai, fi_tab + (irun & 1) * R);
-        irun += has_i;
+        // group tables alternate buffers run by run (each such run has a barrier)
+        const bool has_groups = op.ks > 0;
+        o = pass_diag_run<Real, R>(ops, o, blob, tcs, tid, ar, ai, fi_tab + (irun & 1) * kPassMaxGEntries);
+        irun += has_groups;
       } else if (kind == kPassRGen || kind == kPassRPerm) {
         const uint32_t tc = tcs[o];
         if (!(tc >> 31)) {

@@ -657,6 +657,69 @@ tsg::PassOp build_diag_op(const LaunchStructure& ls, const PassGeom& g, std::vec
   return op;
 }
 
+// in-tile positions a diagonal sub-gate reads (targets and controls), ascending
+std::vector<int> diag_signature(const LaunchStructure& ls, const PassGeom& g) {
+  std::vector<int> sig;
+  for (int q : ls.sub_targets)
+    if (g.pos[q] >= 0) sig.push_back(g.pos[q]);
+  for (int c : ls.controls)
+    if (g.pos[c] >= 0) sig.push_back(g.pos[c]);
+  std::sort(sig.begin(), sig.end());
+  return sig;
+}
+
+// member of a diagonal group over signature `sig`: table index bits from the
+// tile base (out bits, tc) and from the signature index e (dep[k] per bit k)
+template <typename Real>
+tsg::PassOp build_member_op(const LaunchStructure& ls, const PassGeom& g, const std::vector<int>& sig,
+                            std::vector<unsigned char>& data) {
+  tsg::PassOp op = blank_op(tsg::kPassDMember);
+  const int d = 1 << ls.ks;
+  pad16(data);
+  op.data_off = static_cast<int32_t>(data.size());
+  op.ks = ls.ks;
+  auto sig_bit = [&](int p) { return static_cast<int>(std::find(sig.begin(), sig.end(), p) - sig.begin()); };
+  for (const auto& [p, v] : split_controls(ls, g, op)) {
+    op.ictl_mask |= 1u << sig_bit(p);
+    op.ictl_val |= v << sig_bit(p);
+  }
+  for (int b = 0; b < ls.ks; ++b) {
+    const int q = ls.sub_targets[b], p = g.pos[q];
+    if (p < 0) {
+      op.out_gbit[op.n_out] = static_cast<uint8_t>(q);
+      op.out_jbit[op.n_out++] = static_cast<uint8_t>(b);
+    } else {
+      op.dep[sig_bit(p)] |= 1u << b;
+    }
+  }
+  for (int j = 0; j < d; ++j) append_real2<Real>(data, ls.sub_re[j * d + j], ls.sub_im[j * d + j]);
+  return op;
+}
+
+// group header: thread table (signature-index bits from thread positions),
+// dep[k] = signature-index bits of register bit k, data_off = table entry offset
+tsg::PassOp build_group_op(const PassGeom& g, const std::vector<int>& sig, int members, int entry_off,
+                           std::vector<unsigned char>& data) {
+  tsg::PassOp op = blank_op(tsg::kPassDGroup);
+  op.ks = static_cast<int32_t>(sig.size());
+  op.log2_groups = members;
+  op.data_off = entry_off;
+  std::vector<std::pair<int, int>> thr;  // (thread-id bit, signature bit)
+  for (int k = 0; k < static_cast<int>(sig.size()); ++k) {
+    const int rb = g.reg_bit(sig[k]);
+    if (rb >= 0) op.dep[rb] |= 1u << k;
+    else thr.emplace_back(g.thread_bit(sig[k]), k);
+  }
+  pad16(data);
+  op.aux_off = static_cast<int32_t>(data.size());
+  for (int t = 0; t < tsg::kPassThreads; ++t) {
+    uint32_t v = 0;
+    for (const auto& [tb, k] : thr) v |= ((static_cast<uint32_t>(t) >> tb) & 1u) << k;
+    data.push_back(static_cast<unsigned char>(v));
+  }
+  return op;
+}
+
 // mixed (E) and block (B) bits of a non-diagonal sub-gate and the block matrices
 struct BlockForm {
   std::vector<int> ebits, bbits;
@@ -891,24 +954,82 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
                      : choose_layout({}, {}, g.r, M, L);
     ops.push_back(build_layout_op<Real>(g, data));
   }
-  std::vector<tsg::PassOp> cls[3];  // the open run of diagonal ops, by class
+  std::vector<const LaunchStructure*> run;  // the open run of diagonal gates
   auto flush_run = [&]() {
-    if (cls[0].empty() && cls[1].empty() && cls[2].empty()) return;
-    tsg::PassOp hdr = blank_op(tsg::kPassRun);
-    hdr.ks = static_cast<int32_t>(cls[0].size());
-    hdr.log2_groups = static_cast<int32_t>(cls[1].size());
-    hdr.log2_rsplit = static_cast<int32_t>(cls[2].size());
-    ops.push_back(hdr);
-    for (auto& c : cls) {
-      ops.insert(ops.end(), c.begin(), c.end());
-      c.clear();
+    if (run.empty()) return;
+    // groups: largest signatures first, each op into the first group whose
+    // signature stays <= kPassMaxSig bits with it (entries within budget)
+    std::vector<std::pair<std::vector<int>, const LaunchStructure*>> items;
+    for (const LaunchStructure* ls : run) items.emplace_back(diag_signature(*ls, g), ls);
+    std::stable_sort(items.begin(), items.end(),
+                     [](const auto& a, const auto& b) { return a.first.size() > b.first.size(); });
+    std::vector<std::vector<int>> gsig;
+    std::vector<std::vector<const LaunchStructure*>> gmem;
+    std::vector<const LaunchStructure*> rest;
+    int entries = 0;
+    for (const auto& [sig, ls] : items) {
+      // thread-position-only ops keep the per-thread DiagT path (no barrier,
+      // all threads in parallel); groups take the rest
+      bool on_reg = false;
+      for (int p : sig) on_reg = on_reg || g.reg_bit(p) >= 0;
+      if (static_cast<int>(sig.size()) > tsg::kPassMaxSig || !on_reg) {
+        rest.push_back(ls);
+        continue;
+      }
+      int best = -1, best_growth = 1 << 30;
+      for (size_t q = 0; q < gsig.size(); ++q) {
+        std::vector<int> u = gsig[q];
+        for (int p : sig)
+          if (std::find(u.begin(), u.end(), p) == u.end()) u.push_back(p);
+        const int growth = (1 << u.size()) - (1 << gsig[q].size());
+        if (static_cast<int>(u.size()) <= tsg::kPassMaxSig && entries + growth <= tsg::kPassMaxGEntries &&
+            growth < best_growth) {
+          best = static_cast<int>(q);
+          best_growth = growth;
+        }
+      }
+      if (best < 0) {
+        if (entries + (1 << sig.size()) > tsg::kPassMaxGEntries) {
+          rest.push_back(ls);
+          continue;
+        }
+        gsig.push_back(sig);
+        gmem.push_back({});
+        entries += 1 << sig.size();
+        best = static_cast<int>(gsig.size()) - 1;
+      } else {
+        for (int p : sig)
+          if (std::find(gsig[best].begin(), gsig[best].end(), p) == gsig[best].end()) gsig[best].push_back(p);
+        std::sort(gsig[best].begin(), gsig[best].end());
+        entries += best_growth;
+      }
+      gmem[best].push_back(ls);
     }
+    std::vector<tsg::PassOp> tops, xops;  // per-op classes for the rest
+    for (const LaunchStructure* ls : rest) {
+      tsg::PassOp op = build_diag_op<Real>(*ls, g, data);
+      (op.kind == tsg::kPassDiagT ? tops : xops).push_back(op);  // DiagI ops always fit a group (<= 4 bits)
+      if (op.kind == tsg::kPassDiagI) throw SimError("pass: register-only diagonal op outside a group");
+    }
+    tsg::PassOp hdr = blank_op(tsg::kPassRun);
+    hdr.ks = static_cast<int32_t>(gsig.size());
+    hdr.log2_groups = static_cast<int32_t>(tops.size());
+    hdr.log2_rsplit = static_cast<int32_t>(xops.size());
+    ops.push_back(hdr);
+    int entry_off = 0;
+    for (size_t q = 0; q < gsig.size(); ++q) {
+      ops.push_back(build_group_op(g, gsig[q], static_cast<int>(gmem[q].size()), entry_off, data));
+      entry_off += 1 << gsig[q].size();
+      for (const LaunchStructure* ls : gmem[q]) ops.push_back(build_member_op<Real>(*ls, g, gsig[q], data));
+    }
+    ops.insert(ops.end(), tops.begin(), tops.end());
+    ops.insert(ops.end(), xops.begin(), xops.end());
+    run.clear();
   };
   for (size_t i = 0; i < ng; ++i) {
     const LaunchStructure& ls = prog->gates[step.gates[i]].ls;
     if (ls.klass == KernelClass::Diagonal) {
-      tsg::PassOp op = build_diag_op<Real>(ls, g, data);
-      cls[op.kind - tsg::kPassDiagT].push_back(op);
+      run.push_back(&ls);
       continue;
     }
     flush_run();
@@ -928,22 +1049,23 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
 
   if (ops.size() > static_cast<size_t>(tsg::kPassMaxOps)) throw SimError("pass: too many ops");
   if (std::getenv("TSG_PASS_DEBUG")) {
-    int cnt[9] = {0};
+    int cnt[11] = {0};
     for (const tsg::PassOp& op : ops) ++cnt[op.kind];
     std::fprintf(stderr, "pass gates %zu high", step.gates.size());
     for (int h : step.high) std::fprintf(stderr, " %d", h);
-    std::fprintf(stderr, ": layouts %d runs %d diagT %d diagI %d diagX %d rgen %d rperm %d sgen %d sperm %d\n", cnt[0],
-                 cnt[1], cnt[2], cnt[3], cnt[4], cnt[5], cnt[6], cnt[7], cnt[8]);
+    std::fprintf(stderr,
+                 ": layouts %d runs %d groups %d (members %d) diagT %d diagX %d rgen %d rperm %d sgen %d sperm %d\n",
+                 cnt[0], cnt[1], cnt[9], cnt[10], cnt[2], cnt[4], cnt[5], cnt[6], cnt[7], cnt[8]);
   }
   const size_t data_base = (size_t{8} << nh) + ops.size() * sizeof(tsg::PassOp);
   for (tsg::PassOp& op : ops) {
     if (op.kind == tsg::kPassRun) continue;
-    if (op.kind == tsg::kPassLayout) {
+    if (op.kind == tsg::kPassLayout || op.kind == tsg::kPassDGroup) {
       op.aux_off += static_cast<int32_t>(data_base);
       continue;
     }
     op.data_off += static_cast<int32_t>(data_base);
-    if (op.kind != tsg::kPassDiagI) op.aux_off += static_cast<int32_t>(data_base);
+    if (op.kind != tsg::kPassDiagI && op.kind != tsg::kPassDMember) op.aux_off += static_cast<int32_t>(data_base);
   }
   std::vector<unsigned char> blob;
   for (int r = 0; r < (1 << nh); ++r) {
