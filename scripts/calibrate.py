@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--n", type=int, default=30)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default="profiles/r01")
+    ap.add_argument("--tag", default="", help="suffix of the sweep file (fusion_sweep<tag>.json)")
     args = ap.parse_args()
     os.makedirs(args.out, exist_ok=True)
     models = {}
@@ -70,13 +71,15 @@ def main():
             prog.run(sv)
             runs = [prog.run(sv)["execution_s"] for _ in range(2)]
             pred = predicted(cm, fused, n)
+            steps = prog.steps()
             row = {"circuit": f"{kind}-{n}", "precision": prec, "fusion": name, "gates": st["fused_block_count"],
                    "original": st["original_gate_count"], "total_op_count": st["total_op_count"],
-                   "fusion_s": st["fusion_wall_time"], "predicted_s": pred, "measured_s": min(runs)}
+                   "fusion_s": st["fusion_wall_time"], "predicted_s": pred, "measured_s": min(runs),
+                   "launch_steps": len(steps), "tile_passes": sum(s["kind"] == "pass" for s in steps)}
             rows.append(row)
             print(json.dumps(row), flush=True)
             del prog
-    with open(os.path.join(args.out, "fusion_sweep.json"), "w") as f:
+    with open(os.path.join(args.out, f"fusion_sweep{args.tag}.json"), "w") as f:
         json.dump(rows, f, indent=1)
 
 
