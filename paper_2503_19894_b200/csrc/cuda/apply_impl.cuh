@@ -270,7 +270,7 @@ bool try_stream(const GateLaunch& g, cudaStream_t s, int num_sms) {
 
 // ------------------------------------------------------------ stream_dmma
 template <typename Real, int KS>
-bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, int* stages) {
+bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, int* stages, bool simt) {
   using S = DShape<Real, KS>;
   int tg[24], nt = 0;  // all targets (controls + sub-targets), ascending
   {
@@ -364,7 +364,7 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   const int chunk = sizeof(Real) == 8 ? 5 : 6;  // 256-byte chunks
   // only for ks = 5, whose stages are loaded and never bulk-stored: more,
   // smaller bulk copies measured slower for the HBM-bound ks <= 4 kernels
-  if (KS >= 5 && L > chunk && wavefronts(chunk) < wavefronts(L)) p.chunk_log2 = chunk;
+  if (KS >= 5 && !simt && L > chunk && wavefronts(chunk) < wavefronts(L)) p.chunk_log2 = chunk;
   layout(p.chunk_log2, &p.chunk_stride, &p.run_stride);
   for (int j = 0; j < (1 << KS); ++j) {
     const uint32_t w = low_of[j];
@@ -373,16 +373,16 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   // Two CTAs per SM beat deeper pipelines (measured): 3 stages when two CTAs
   // still fit in shared memory, else 2.
   const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(Real);
-  const size_t fixed = dmma_m_smem_bytes<KS>() + 128;
+  const size_t fixed = (simt ? dmma_m_smem_bytes<Real, KS, true>() : dmma_m_smem_bytes<Real, KS>()) + 128;
   const size_t per_cta = 110 * 1024;
   *stages = 3 * stage + fixed <= per_cta ? 3 : 2;
   *smem = *stages * stage + fixed;
   return *smem <= 220 * 1024;
 }
 
-template <typename Real, int KS, int STAGES, bool SP>
+template <typename Real, int KS, int STAGES, bool SP, bool SIMT>
 void launch_dmma(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int num_sms) {
-  auto kern = k_stream_dmma<Real, KS, STAGES, SP>;
+  auto kern = k_stream_dmma<Real, KS, STAGES, SP, SIMT>;
   static size_t configured_smem = 0;
   if (configured_smem < smem) {
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "dmma smem");
@@ -396,6 +396,14 @@ void launch_dmma(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int
   cuda_check(cudaGetLastError(), "k_stream_dmma launch");
 }
 
+template <typename Real, int KS, int STAGES, bool SP>
+void launch_dmma_pick(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int num_sms, bool simt) {
+  if constexpr (sizeof(Real) == 4 && KS <= 3) {
+    if (simt) return launch_dmma<Real, KS, STAGES, false, true>(p, smem, s, num_sms);  // SIMT evaluates densely
+  }
+  launch_dmma<Real, KS, STAGES, SP, false>(p, smem, s, num_sms);
+}
+
 template <typename Real, int KS>
 bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   using S = DShape<Real, KS>;
@@ -404,7 +412,14 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   std::memset(&p, 0, sizeof p);
   size_t smem = 0;
   int stages = 3;
-  if (!dmma_geometry<Real, KS>(g, p, &smem, &stages)) return false;
+  // complex64, 3 qubits, every target and control at bit 5 or above: FP32
+  // SIMT consumer (measured faster there; slower than the FP64-widened DMMA
+  // product for 4-5 qubits and for low targets -- scripts/pass_bench.py)
+  int lowest = 64;
+  for (int b = 0; b < g.ks; ++b) lowest = std::min(lowest, g.sub_targets[b]);
+  for (int c = 0; c < g.n_ctrl; ++c) lowest = std::min(lowest, g.ctrl[c]);
+  const bool simt = sizeof(Real) == 4 && KS <= 3 && lowest >= 5;
+  if (!dmma_geometry<Real, KS>(g, p, &smem, &stages, simt)) return false;
   p.re = static_cast<Real*>(g.re);
   p.im = static_cast<Real*>(g.im);
   p.mat = static_cast<const double*>(g.dev_mat);
@@ -426,10 +441,14 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
     }
   const bool sparse = (p.nzblk[0] & p.nzblk[1] & p.nzblk[2]) != (S::RB * S::KST >= 32 ? ~0u : ((1u << (S::RB * S::KST)) - 1));
   switch (stages) {
-    case 5: sparse ? launch_dmma<Real, KS, 5, true>(p, smem, s, num_sms) : launch_dmma<Real, KS, 5, false>(p, smem, s, num_sms); break;
-    case 4: sparse ? launch_dmma<Real, KS, 4, true>(p, smem, s, num_sms) : launch_dmma<Real, KS, 4, false>(p, smem, s, num_sms); break;
-    case 3: sparse ? launch_dmma<Real, KS, 3, true>(p, smem, s, num_sms) : launch_dmma<Real, KS, 3, false>(p, smem, s, num_sms); break;
-    default: sparse ? launch_dmma<Real, KS, 2, true>(p, smem, s, num_sms) : launch_dmma<Real, KS, 2, false>(p, smem, s, num_sms); break;
+    case 3:
+      sparse ? launch_dmma_pick<Real, KS, 3, true>(p, smem, s, num_sms, simt)
+             : launch_dmma_pick<Real, KS, 3, false>(p, smem, s, num_sms, simt);
+      break;
+    default:
+      sparse ? launch_dmma_pick<Real, KS, 2, true>(p, smem, s, num_sms, simt)
+             : launch_dmma_pick<Real, KS, 2, false>(p, smem, s, num_sms, simt);
+      break;
   }
   return true;
 }

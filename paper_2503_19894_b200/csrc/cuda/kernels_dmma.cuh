@@ -125,12 +125,18 @@ template <int KS>
 __host__ __device__ constexpr bool dmma_m_in_regs() {
   return KS <= 4;
 }
-template <int KS>
+// shared memory ahead of the stages: M fragments (FP64 DMMA, ks = 5) or the
+// sub-matrix as {re, im} FP32 pairs (SIMT: complex64 3-qubit sub-gates with
+// every target and control at bit 5 or above -- FP32 FMA at twice the FP64
+// rate, lanes on contiguous groups; measured faster than the FP64-widened
+// DMMA product there, slower for 4-5 qubits and low targets)
+template <typename Real, int KS, bool SIMT = false>
 __host__ __device__ constexpr size_t dmma_m_smem_bytes() {
+  if (SIMT) return size_t{8} << (2 * KS);
   return dmma_m_in_regs<KS>() ? 0 : size_t{3} * DmmaShape<KS>::KST * DmmaShape<KS>::RB * 32 * sizeof(double);
 }
 
-template <typename Real, int KS, int STAGES, bool SPARSE>
+template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT = false>
 __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, KS>::W >= 16 ? 1 : 2)
     k_stream_dmma(const __grid_constant__ DmmaParams<Real, KS> p) {
   using S = DShape<Real, KS>;
@@ -141,11 +147,12 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
 #ifndef TSG_DMMA_DIRECT_OUT_MIN_KS
 #define TSG_DMMA_DIRECT_OUT_MIN_KS 5
 #endif
-  constexpr bool kDirectOut = KS >= TSG_DMMA_DIRECT_OUT_MIN_KS;
+  constexpr bool kSimt = SIMT;
+  constexpr bool kDirectOut = KS >= TSG_DMMA_DIRECT_OUT_MIN_KS && !kSimt;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
   double* mfrag = reinterpret_cast<double*>(smem_raw);  // [3][KST][RB][32] when !MREG
-  Real* buf = reinterpret_cast<Real*>(smem_raw + dmma_m_smem_bytes<KS>());  // [STAGES][2][stage_elems]
+  Real* buf = reinterpret_cast<Real*>(smem_raw + dmma_m_smem_bytes<Real, KS, SIMT>());  // [STAGES][2][stage_elems]
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(buf) +
                                                sizeof(Real) * 2 * STAGES * stage_elems);
   uint64_t* empty = full + STAGES;
@@ -164,7 +171,11 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
     }
     mbar_fence_init();
   }
-  if constexpr (!MREG) {
+  if constexpr (kSimt) {
+    constexpr int DD = S::D * S::D;
+    float2* smat = reinterpret_cast<float2*>(smem_raw);
+    for (int i = tid; i < DD; i += blockDim.x) smat[i] = float2{static_cast<float>(p.mat[i]), static_cast<float>(p.mat[DD + i])};
+  } else if constexpr (!MREG) {
     constexpr int DD = S::D * S::D;
     constexpr int NF = 3 * S::KST * S::RB * 32;
     for (int f = tid; f < NF; f += blockDim.x) {
@@ -242,6 +253,66 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
       }
     }
     if constexpr (!kDirectOut) bulk_wait_all();
+    return;
+  }
+
+  if constexpr (kSimt) {
+    // ---------------- consumer warps, complex64: FP32 SIMT product ---------
+    // Thread t owns GP groups (t, t + T, ...) when the tile has more groups
+    // than threads, else group t % G and rows [RS (t / G), RS (t / G) + RS).
+    // Lanes take consecutive groups: every element load of a warp is one
+    // contiguous run of the stage; matrix entries are warp-uniform broadcasts.
+    constexpr int T = S::kThreads, G = S::G, D = S::D;
+    constexpr int GP = G >= T ? G / T : 1;
+    constexpr int RS = G >= T ? D : D * G / T;
+    const float2* smat = reinterpret_cast<const float2*>(smem_raw);
+    const int r0 = G >= T ? 0 : (tid / G) * RS;
+    uint32_t gb[GP];
+#pragma unroll
+    for (int q = 0; q < GP; ++q) gb[q] = dmma_pad(p, dmma_group_pos(p, (G >= T ? tid : tid % G) + q * T));
+    uint32_t jt = 0;
+    for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++jt) {
+      const int s = static_cast<int>(jt % STAGES);
+      mbar_wait(&full[s], (jt / STAGES) & 1u);
+      Real* xr = buf + (2 * s) * stage_elems;
+      Real* xi = xr + stage_elems;
+      float yr[GP][RS], yi[GP][RS];
+#pragma unroll
+      for (int q = 0; q < GP; ++q) {
+        float vr[D], vi[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          vr[j] = xr[gb[q] + p.soff[j]];
+          vi[j] = xi[gb[q] + p.soff[j]];
+        }
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+          float ar = 0.f, ai = 0.f;
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const float2 m = smat[(r0 + r) * D + c];
+            ar = fmaf(m.x, vr[c], ar);
+            ai = fmaf(m.x, vi[c], ai);
+            ar = fmaf(-m.y, vi[c], ar);
+            ai = fmaf(m.y, vr[c], ai);
+          }
+          yr[q][r] = ar;
+          yi[q][r] = ai;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");  // every consumer has read the stage
+#pragma unroll
+      for (int q = 0; q < GP; ++q)
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+          const uint32_t a = gb[q] + p.soff[r0 + r];
+          xr[a] = yr[q][r];
+          xi[a] = yi[q][r];
+        }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+    }
     return;
   }
 
