@@ -364,7 +364,8 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   const int chunk = sizeof(Real) == 8 ? 5 : 6;  // 256-byte chunks
   // only for ks = 5, whose stages are loaded and never bulk-stored: more,
   // smaller bulk copies measured slower for the HBM-bound ks <= 4 kernels
-  if (KS >= 5 && !simt && L > chunk && wavefronts(chunk) < wavefronts(L)) p.chunk_log2 = chunk;
+  const bool direct_out = KS >= 5 || (sizeof(Real) == 4 && KS >= 4);  // k_stream_dmma kDirectOut
+  if (direct_out && !simt && L > chunk && wavefronts(chunk) < wavefronts(L)) p.chunk_log2 = chunk;
   layout(p.chunk_log2, &p.chunk_stride, &p.run_stride);
   for (int j = 0; j < (1 << KS); ++j) {
     const uint32_t w = low_of[j];

@@ -148,7 +148,12 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
 #define TSG_DMMA_DIRECT_OUT_MIN_KS 5
 #endif
   constexpr bool kSimt = SIMT;
-  constexpr bool kDirectOut = KS >= TSG_DMMA_DIRECT_OUT_MIN_KS && !kSimt;
+#ifndef TSG_DMMA_DIRECT_OUT_MIN_KS_F32
+#define TSG_DMMA_DIRECT_OUT_MIN_KS_F32 4
+#endif
+  // (complex64 4-qubit products are FP64-bound too: widened to the DMMA pipe)
+  constexpr bool kDirectOut =
+      KS >= (sizeof(Real) == 4 ? TSG_DMMA_DIRECT_OUT_MIN_KS_F32 : TSG_DMMA_DIRECT_OUT_MIN_KS) && !kSimt;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
   double* mfrag = reinterpret_cast<double*>(smem_raw);  // [3][KST][RB][32] when !MREG
