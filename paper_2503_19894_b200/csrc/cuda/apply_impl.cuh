@@ -12,6 +12,11 @@
 #include "kernels.cuh"
 #include "kernels_dmma.cuh"
 #include "kernels_stream.cuh"
+#include "kernels_umma.cuh"
+
+#ifndef TSG_UMMA_DEFAULT_KS
+#define TSG_UMMA_DEFAULT_KS 0x30u  // ks 4, 5
+#endif
 
 namespace tsg {
 
@@ -454,6 +459,73 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   return true;
 }
 
+// ---------------------------------------------------------- stream_umma
+// complex64 4- and 5-qubit sub-gates on the INT8 tensor cores
+// (kernels_umma.cuh).  TSG_UMMA=0 disables it (the FP64-widened DMMA product
+// runs instead); TSG_UMMA_KS=<bitmask of ks> overrides which sizes take it.
+inline uint32_t umma_ks_mask() {
+  static uint32_t mask = [] {
+    const char* e = std::getenv("TSG_UMMA");
+    if (e && std::string(e) == "0") return 0u;
+    const char* m = std::getenv("TSG_UMMA_KS");
+    return (m ? static_cast<uint32_t>(std::strtoul(m, nullptr, 0)) : TSG_UMMA_DEFAULT_KS) & 0x30u;
+  }();
+  return mask;
+}
+
+template <int KS, int STAGES>
+void launch_umma(const DmmaParams<float, KS>& p, size_t smem, cudaStream_t s, int num_sms) {
+  using U = UmmaShape<KS>;
+  auto kern = k_stream_umma<KS, STAGES>;
+  static size_t configured_smem = 0;
+  if (configured_smem < smem) {
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "umma smem");
+    configured_smem = smem;
+  }
+  const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * 2);
+  kern<<<static_cast<unsigned>(blocks), U::T + 32, smem, s>>>(p);
+  cuda_check(cudaGetLastError(), "k_stream_umma launch");
+}
+
+// Lanes own consecutive groups: a target or control on bit 0 spreads a
+// warp's stage reads over many banks and its global stores over twice the
+// sectors (measured 3-4x slower there than the DMMA product).
+inline bool umma_takes(const GateLaunch& g) {
+  if (!g.dev_mat || !g.full_range || !((umma_ks_mask() >> g.ks) & 1u)) return false;
+  for (int b = 0; b < g.ks; ++b)
+    if (g.sub_targets[b] == 0) return false;
+  for (int c = 0; c < g.n_ctrl; ++c)
+    if (g.ctrl[c] == 0) return false;
+  return true;
+}
+
+template <int KS>
+bool try_umma(const GateLaunch& g, cudaStream_t s, int num_sms) {
+  if (!umma_takes(g)) return false;
+  DmmaParams<float, KS> p;
+  std::memset(&p, 0, sizeof p);
+  size_t dsmem = 0;
+  int dstages = 0;
+  // geometry without chunked runs (the simt layout): one bulk copy per run
+  if (!dmma_geometry<float, KS>(g, p, &dsmem, &dstages, /*simt=*/true)) return false;
+  if (p.chunk_log2 != p.L) return false;
+  p.re = static_cast<float*>(g.re);
+  p.im = static_cast<float*>(g.im);
+  p.mat = static_cast<const double*>(g.dev_mat);
+  // two CTAs per SM (256 TMEM columns each), two stages each; at least 80 KB
+  // so that a third CTA never lands on an SM (tcgen05.alloc would wait)
+  const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(float);
+  const size_t fixed = umma_fixed_smem<KS>() + 256;
+  static const int max_stages = std::getenv("TSG_UMMA_STAGES") ? std::atoi(std::getenv("TSG_UMMA_STAGES")) : 3;
+  if (max_stages >= 3 && fixed + 3 * stage <= 113 * 1024) {
+    launch_umma<KS, 3>(p, std::max(fixed + 3 * stage, size_t{80} * 1024), s, num_sms);
+    return true;
+  }
+  if (fixed + 2 * stage > 113 * 1024) return false;
+  launch_umma<KS, 2>(p, std::max(fixed + 2 * stage, size_t{80} * 1024), s, num_sms);
+  return true;
+}
+
 // ---------------------------------------------------------- dmma_direct
 template <int KS>
 bool try_dmma_direct(const GateLaunch& g, cudaStream_t s, int num_sms) {
@@ -521,10 +593,10 @@ bool launch_stream_if(const GateLaunch& g, cudaStream_t s, int num_sms) {
       default: return false;
     }
   } else {
-    switch (g.ks) {  // complex64: widened to FP64 on the DMMA pipe
+    switch (g.ks) {  // complex64: INT8 slices on tcgen05 (ks 4, 5), else widened to FP64 on the DMMA pipe
       case 3: return try_dmma<float, 3>(g, s, num_sms);
-      case 4: return try_dmma<float, 4>(g, s, num_sms);
-      case 5: return try_dmma<float, 5>(g, s, num_sms);
+      case 4: return try_umma<4>(g, s, num_sms) || try_dmma<float, 4>(g, s, num_sms);
+      case 5: return try_umma<5>(g, s, num_sms) || try_dmma<float, 5>(g, s, num_sms);
       default: return false;
     }
   }
@@ -594,6 +666,7 @@ std::string kernel_name_impl(const GateLaunch& g) {
   const std::string ks = "<ks=" + std::to_string(g.ks);
   int klass = g.klass;
   if (klass == 0) return "none";
+  if ((klass == 2 || klass == 3) && sizeof(Real) == 4 && umma_takes(g)) return "k_stream_umma" + ks + ">";
   if (g.full_range && (klass == 2 || klass == 3) && g.ks >= 3 && g.ks <= 5 && g.dev_mat)
     return (dmma_mode() == 1 && sizeof(Real) == 8 ? "k_dmma_direct" : "k_stream_dmma") + ks + ">";
   if (klass == 1 && !g.full_range) klass = g.ks <= DM ? 2 : 3;

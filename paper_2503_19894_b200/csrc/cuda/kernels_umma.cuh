@@ -1,0 +1,375 @@
+// k_stream_umma: complex64 sub-gates of 4 and 5 qubits on the 5th-generation
+// tensor cores, in exact integer arithmetic (tcgen05.mma.kind::i8, INT32
+// accumulators in TMEM).
+//
+// Same tile stream as k_stream_dmma (runs of 2^L amplitudes, bulk copies into
+// mbarrier stages, persistent CTAs, producer warp) and the same host geometry
+// (dmma_geometry: element order, run offsets, control folding).  Per tile of
+// G groups x D elements the complex product Y = M X is one real product
+//
+//   [Yr | Yi] (G x 2D) = [Xr | Xi] (G x 2D) . B^T,   B = | Mr  -Mi |
+//                                                         | Mi   Mr |
+//
+// (MMA M = 128 groups, N = K = 2D).  Operands are split into signed 8-bit
+// slices (the Ozaki scheme): every group row x is scaled by a power of two
+// s with |x| / s < 1 and written as x = s (a1 2^-7 + a2 2^-14 + a3 2^-21 + r)
+// with integer slices |a_i| <= 127 (round to nearest: |r| <= 2^-22); every
+// row of B likewise with its own power of two t and slices b_j.  Slice
+// products are integers and their K-sums stay far below 2^31, so the tensor
+// core computes them EXACTLY; three INT32 accumulators collect the levels
+// i + j = 2, 3, 4:
+//     acc2 = a1 b1,  acc3 = a1 b2 + a2 b1,  acc4 = a1 b3 + a2 b2 + a3 b1
+// and the epilogue forms y = s t 2^-28 (2^14 acc2 + 2^7 acc3 + acc4) with
+// round-to-nearest FP32 operations.  The dropped levels (>= 5) and the slice
+// residuals are ~2^-21 of the row scale and have no preferred sign: unlike a
+// TF32 split, whose FP32 tensor-core accumulation truncates (measured: the
+// norm fell by ~2e-7 per gate), the result carries no bias.
+//
+// Tensor memory per 128-group M block (KS = 4: two blocks, KS = 5: one):
+//   [acc2 | acc3 | acc4] 2D INT32 columns each, then the three A slices of
+//   the block's rows, 2D / 4 columns each (4 INT8 per 32-bit column).
+// 256 consumer threads: thread t owns group g = t mod G = TMEM lane g mod 128
+// of block g / 128 (KS = 5: two threads per group, each half of the row's
+// columns): it reads its group's 2D values from the stage, slices them and
+// writes its own TMEM row (tcgen05.st) -- no shared-memory staging of A.  B's slices sit in
+// shared memory in the canonical K-major no-swizzle layout (core matrices of
+// 8 rows x 16 bytes, rows 16 bytes apart; 8-row groups 128 bytes apart; the
+// next 16 K-bytes N x 16 bytes further).  Thread 0 issues 6 MMAs per K step
+// (K = 32 INT8) and commits to an mbarrier; the threads then read their
+// row's accumulators and store Yr, Yi straight to global memory (lanes own
+// consecutive groups: coalesced rows).  256 TMEM columns and < 113 KB of
+// shared memory per CTA: two CTAs per SM overlap one's MMAs and epilogue with
+// the other's loads.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#include "kernels_dmma.cuh"
+
+namespace tsg {
+
+template <int KS>
+struct UmmaShape {
+  static_assert(KS == 4 || KS == 5, "k_stream_umma: 4- and 5-qubit sub-gates");
+  static constexpr int D = 1 << KS;
+  static constexpr int LOG2G = 12 - KS;  // 4096-amplitude tiles (DShape<float, KS>)
+  static constexpr int G = 1 << LOG2G;   // groups per tile
+  static constexpr int T = 256;          // consumer threads
+  static constexpr int TPG = T / G;      // threads per group (KS = 5: two, each half the columns)
+  static constexpr int W = T / 32;       // consumer warps
+  static constexpr int N = 2 * D;        // [Yr | Yi]
+  static constexpr int K = 2 * D;        // [Xr | Xi]
+  static constexpr int MB = G / 128;     // 128-group M blocks
+  static constexpr int KSTEPS = K / 32;  // INT8 MMA K = 32
+  static constexpr int ACOLS = K / 4;    // TMEM columns of one A slice row
+  static constexpr int kTmemCols = 256;
+  static constexpr int BLK = kTmemCols / MB;  // TMEM columns per M block
+  static_assert(3 * N + 3 * ACOLS <= BLK, "tensor-memory budget");
+  static constexpr uint32_t kBBytes = uint32_t(N) * K;  // one slice of B (INT8)
+  // instruction descriptor (kind::i8): D S32 (bits 4-5 = 2), A / B signed
+  // (bits 7-9, 10-12 = 1), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+  static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+};
+
+__device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // start >> 4 (bits 0-13), LBO >> 4 (16-29), SBO >> 4 (32-45), version 1
+  // (bit 46), base offset 0, SWIZZLE_NONE (bits 61-63 = 0)
+  return uint64_t((saddr >> 4) & 0x3fffu) | (uint64_t((lbo >> 4) & 0x3fffu) << 16) |
+         (uint64_t((sbo >> 4) & 0x3fffu) << 32) | (uint64_t{1} << 46);
+}
+// D[tmem] (+)= A[tmem] . B[smem]^T, INT8 x INT8 -> INT32
+__device__ __forceinline__ void umma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// the loaded registers are valid after tcgen05.wait::ld; the empty asm
+// statements tie every later use to the wait
+template <int NV>
+__device__ __forceinline__ void tmem_wait_ld(uint32_t* v) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < NV; ++i) asm volatile("" : "+r"(v[i]));
+}
+
+// Smallest power of two s with m (1 + 2^-7) <= s (1 for m == 0): slices of
+// x / s * 128 then round to at most 127 in magnitude.
+__device__ __forceinline__ float slice_scale(float m) {
+  m = m + m * (1.0f / 128.0f);
+  if (!(m > 0.0f)) return 1.0f;
+  return __uint_as_float((__float_as_uint(m) + 0x007fffffu) & 0xff800000u);
+}
+// Slices of u = x / s * 128 (|u| <= 127): a1, a2, a3 as the low byte of the
+// magic-number rounding (round to nearest even, two's complement)
+__device__ __forceinline__ void slice3(float u, uint32_t& b1, uint32_t& b2, uint32_t& b3) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  float t = u + kMagic;
+  float a = t - kMagic;
+  b1 = __float_as_uint(t);
+  u = (u - a) * 128.0f;
+  t = u + kMagic;
+  a = t - kMagic;
+  b2 = __float_as_uint(t);
+  u = (u - a) * 128.0f;
+  b3 = __float_as_uint(u + kMagic);
+}
+// int32 (|v| < 2^22) to float, exactly
+__device__ __forceinline__ float small_i2f(uint32_t v) { return __uint_as_float(v + 0x4B400000u) - 12582912.0f; }
+
+template <int KS>
+__host__ __device__ constexpr size_t umma_fixed_smem() {
+  using U = UmmaShape<KS>;
+  return 3 * size_t{U::kBBytes} + U::N * sizeof(float);  // B slices, B row scales
+}
+// registers for two CTAs per SM (multiple of 8)
+template <int KS>
+constexpr int umma_max_regs() {
+  return (65536 / (2 * (UmmaShape<KS>::T + 32))) / 8 * 8;  // 112
+}
+
+template <int KS, int STAGES>
+__global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_constant__ DmmaParams<float, KS> p) {
+  using U = UmmaShape<KS>;
+  constexpr int D = U::D;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* b_ops = smem_raw;                                       // [b1 | b2 | b3]
+  float* b_scale = reinterpret_cast<float*>(smem_raw + 3 * U::kBBytes);  // t_n 2^-28
+  const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
+  float* buf = reinterpret_cast<float*>(smem_raw + umma_fixed_smem<KS>());  // [STAGES][2][stage_elems]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(buf) + sizeof(float) * 2 * STAGES * stage_elems);
+  uint64_t* empty = full + STAGES;
+  uint64_t* mma_bar = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t run_bytes = (1u << p.L) * sizeof(float);
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], U::W);
+    }
+    mbar_init(mma_bar, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) {  // tensor memory (warp-wide), released at the end by the same warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                 "r"(U::kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // B row n (output column): n < D -> Yr row n: [Mr | -Mi]; n >= D -> Yi
+  // row n - D: [Mi | Mr].  One thread per row: its scale and slices.
+  auto bval = [&](int n, int k) {
+    constexpr int DD = D * D;
+    const int r = n % D, c = k % D;
+    const double mr = p.mat[r * D + c], mi = p.mat[DD + r * D + c];
+    return n < D ? (k < D ? mr : -mi) : (k < D ? mi : mr);
+  };
+  for (int n = tid; n < U::N; n += blockDim.x) {
+    float m = 0.0f;
+    for (int k = 0; k < U::K; ++k) m = fmaxf(m, fabsf(static_cast<float>(bval(n, k))));
+    const float t = slice_scale(m);
+    b_scale[n] = t * 0x1p-28f;
+    const double inv = 128.0 / static_cast<double>(t);
+    for (int k = 0; k < U::K; ++k) {
+      double u = bval(n, k) * inv;  // |u| <= 127 (+ the float rounding of the max: still rounds to <= 127)
+      const uint32_t off = (k >> 4) * (U::N * 16) + n * 16 + (k & 15);
+      for (int jj = 0; jj < 3; ++jj) {
+        const double a = rint(u);
+        b_ops[jj * U::kBBytes + off] = static_cast<unsigned char>(static_cast<int>(a) & 0xff);
+        u = (u - a) * 128.0;
+      }
+    }
+  }
+  fence_async_smem();  // B (generic writes) -> tensor-core reads
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto raw_base = [&](uint64_t tile) {
+    uint64_t b = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxMasks; ++i)
+      if (i < p.n_tmask) b += (tile & p.tmask[i]) << i;
+    return b << p.L;
+  };
+  struct TileStream {
+    uint64_t raw, mask, dstep, ctrl;
+    __device__ uint64_t base() const { return raw | ctrl; }
+    __device__ void advance() { raw = ((raw | ~mask) + dstep) & mask; }
+  };
+  const TileStream stream0{raw_base(first), raw_base(p.n_tiles - 1), raw_base(step), p.ctrl_hi};
+
+  if (warp == U::W) {
+    // ---------------- producer warp: bulk loads of whole runs --------------
+    TileStream lstream = stream0;
+    auto load = [&](int s) {
+      const uint64_t base = lstream.base();
+      lstream.advance();
+      float* dr = buf + (2 * s) * stage_elems;
+      float* di = dr + stage_elems;
+      if (lane == 0) mbar_expect_tx(&full[s], 2u * run_bytes * static_cast<uint32_t>(p.n_runs));
+      __syncwarp();
+      for (int r = lane; r < p.n_runs; r += 32) {
+        const uint32_t so = r * p.run_stride;
+        const uint64_t go = base + p.roff[r];
+        bulk_g2s(dr + so, p.re + go, run_bytes, &full[s]);
+        bulk_g2s(di + so, p.im + go, run_bytes, &full[s]);
+      }
+    };
+    for (int s = 0; s < STAGES; ++s)
+      if (first + s * step < p.n_tiles) load(s);
+    uint32_t j = 0;
+    for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
+      const int s = static_cast<int>(j % STAGES);
+      if (tile + STAGES * step >= p.n_tiles) break;
+      mbar_wait(&empty[s], (j / STAGES) & 1u);  // the consumers have read tile j
+      load(s);
+    }
+    return;
+  }
+
+  // ---------------- consumer threads ----------------------------------------
+  // thread t: group t mod G (TMEM lane (t mod G) mod 128 of M block
+  // (t mod G) / 128), part t / G of the row's columns (warp-uniform)
+  const int grp = tid % U::G, part = U::TPG > 1 ? tid / U::G : 0;  // (compile-time 0 for KS = 4: column indices stay static)
+  const uint32_t gpos = dmma_group_pos(p, static_cast<uint32_t>(grp));  // raw in-run position
+  const uint32_t row = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                       static_cast<uint32_t>((grp >> 7) * U::BLK);  // this group's TMEM lane, its block
+  const uint32_t b_addr = smem_addr(b_ops);
+  constexpr uint32_t kLboB = U::N * 16;
+  constexpr int kAc = U::ACOLS / U::TPG;  // A columns this thread writes
+  constexpr int kNc = U::N / U::TPG;      // output columns this thread stores
+
+  TileStream cstream = stream0;
+  uint32_t j = 0;
+  for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
+    const int s = static_cast<int>(j % STAGES);
+    mbar_wait(&full[s], (j / STAGES) & 1u);
+    const float* xr = buf + (2 * s) * stage_elems;
+    const float* xi = xr + stage_elems;
+    float v[U::K];
+    float m = 0.0f;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      v[c] = xr[p.soff[c] + gpos];
+      v[D + c] = xi[p.soff[c] + gpos];
+      m = fmaxf(m, fmaxf(fabsf(v[c]), fabsf(v[D + c])));
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+    const float sg = slice_scale(m);
+    const float inv = __uint_as_float(0x82800000u - __float_as_uint(sg));  // 128 / sg (powers of two: (134 - E) << 23)
+    // this thread's part of the group's row of the three A slices, straight
+    // into the group's TMEM lane
+#pragma unroll
+    for (int cc = 0; cc < kAc; cc += 8) {
+      const int c = part * kAc + cc;  // 32-bit column
+      uint32_t w1[8], w2[8], w3[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint32_t e1[4], e2[4], e3[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float x = v[4 * (cc + q) + e];
+          if constexpr (U::TPG > 1) x = part ? v[kAc * 4 + 4 * (cc + q) + e] : x;
+          slice3(x * inv, e1[e], e2[e], e3[e]);
+        }
+        w1[q] = __byte_perm(__byte_perm(e1[0], e1[1], 0x0040), __byte_perm(e1[2], e1[3], 0x0040), 0x5410);
+        w2[q] = __byte_perm(__byte_perm(e2[0], e2[1], 0x0040), __byte_perm(e2[2], e2[3], 0x0040), 0x5410);
+        w3[q] = __byte_perm(__byte_perm(e3[0], e3[1], 0x0040), __byte_perm(e3[2], e3[3], 0x0040), 0x5410);
+      }
+      tmem_st8(row + 3 * U::N + 0 * U::ACOLS + c, w1);
+      tmem_st8(row + 3 * U::N + 1 * U::ACOLS + c, w2);
+      tmem_st8(row + 3 * U::N + 2 * U::ACOLS + c, w3);
+    }
+    tmem_wait_st();
+    tc_fence_before();  // A written / previous tile's tcgen05.ld done before the MMAs
+    asm volatile("bar.sync 1, %0;" ::"r"(U::T) : "memory");
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int mb = 0; mb < U::MB; ++mb)
+#pragma unroll
+        for (int ks = 0; ks < U::KSTEPS; ++ks) {
+          const uint32_t blk = tmem_base + mb * U::BLK;
+          const uint32_t a1 = blk + 3 * U::N + 8 * ks, a2 = a1 + U::ACOLS, a3 = a2 + U::ACOLS;
+          const uint32_t bo = b_addr + ks * 2 * kLboB;
+          const uint64_t b1 = umma_smem_desc(bo, kLboB, 128), b2 = umma_smem_desc(bo + U::kBBytes, kLboB, 128),
+                         b3 = umma_smem_desc(bo + 2 * U::kBBytes, kLboB, 128);
+          const uint32_t acc = ks > 0;
+          umma_i8_ts(blk, a1, b1, U::kIdesc, acc);  // level 2
+          umma_i8_ts(blk + U::N, a1, b2, U::kIdesc, acc);  // level 3
+          umma_i8_ts(blk + U::N, a2, b1, U::kIdesc, 1);
+          umma_i8_ts(blk + 2 * U::N, a1, b3, U::kIdesc, acc);  // level 4
+          umma_i8_ts(blk + 2 * U::N, a2, b2, U::kIdesc, 1);
+          umma_i8_ts(blk + 2 * U::N, a3, b1, U::kIdesc, 1);
+        }
+      umma_commit(mma_bar);
+    }
+    mbar_wait(mma_bar, j & 1u);
+    tc_fence_after();
+    const uint64_t tb = cstream.base() + gpos;
+    cstream.advance();
+#pragma unroll
+    for (int cc = 0; cc < kNc; cc += 16) {
+      const int c = part * kNc + cc;
+      uint32_t l2[16], l3[16], l4[16];
+      tmem_ld16(row + c, l2);
+      tmem_ld16(row + U::N + c, l3);
+      tmem_ld16(row + 2 * U::N + c, l4);
+      tmem_wait_ld<16>(l2);
+      tmem_wait_ld<16>(l3);
+      tmem_wait_ld<16>(l4);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int n = c + e;
+        // 2^14 acc2 + 2^7 acc3 + acc4, two round-to-nearest steps
+        const float f = fmaf(small_i2f(l2[e]), 16384.0f, fmaf(small_i2f(l3[e]), 128.0f, small_i2f(l4[e])));
+        const float y = f * (sg * b_scale[n]);
+        if constexpr (U::TPG == 1) {
+          if (n < D) p.re[tb + p.goff[n]] = y;
+          else p.im[tb + p.goff[n - D]] = y;
+        } else {  // part 0: the real parts (columns [0, D)), part 1: the imaginary parts
+          (part ? p.im : p.re)[tb + p.goff[cc + e]] = y;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(U::T) : "memory");
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(U::kTmemCols) : "memory");
+  }
+}
+
+}  // namespace tsg
