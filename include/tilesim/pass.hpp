@@ -39,6 +39,10 @@ struct PassConfig {
   double perm_sweeps_smem = 0.5;
   double standalone_sweeps = 1.08;
   int reg_bits = 3;  // register positions a register op may mix (2^M / 256 amplitudes per thread)
+  // a run of at least this many consecutive qubit-permutation gates (SWAP
+  // layers) becomes one permutation step: one in-place sweep (two for a
+  // permutation that is not an involution) instead of a sweep per gate
+  int min_permute_run = 3;
   // testing: every eligible gate joins (no cost test, single-gate passes allowed);
   // pass_config() sets it when the environment has TSG_PASS_FORCE=1
   bool force = false;
@@ -71,6 +75,11 @@ bool monomial(const LaunchStructure& ls);
 // 5-qubit sweep.  Returns {ls} when every bit is mixed.
 std::vector<LaunchStructure> split_blocks(const LaunchStructure& ls, int precision_bits);
 
+// A sub-gate without controls whose snapped matrix is a 0/1 permutation that
+// moves bit b of the sub-index to bit sigma[b] (SWAP and products of SWAPs,
+// e.g. QFT's bit-reversal layer after fusion): the gate permutes qubits.
+bool qubit_permutation(const LaunchStructure& ls, std::vector<int>* sigma);
+
 // How one gate can be executed inside a pass (or not at all).
 PassRole pass_role(const LaunchStructure& ls, const PassConfig& cfg);
 
@@ -79,6 +88,7 @@ int pass_op_bytes(const LaunchStructure& ls, const PassConfig& cfg);
 
 struct PassStep {
   bool is_pass = false;
+  bool is_permute = false;  // a run of qubit-permutation gates (qubit_permutation), one k_permute step
   std::vector<int> gates;  // program gate indices, program order
   std::vector<int> high;   // pass only: the M - L high tile qubits, ascending
 };
@@ -91,7 +101,9 @@ double standalone_sweeps(const LaunchStructure& ls, const PassConfig& cfg);
 // inside it than on its own, the union of the mixed qubits above L fits
 // M - L and the blob / op budgets hold; a finished pass whose estimated cost
 // exceeds that of launching its gates one by one is emitted as standalone
-// gates.  Identity gates (nothing to launch) are dropped.
+// gates.  Identity gates (nothing to launch) are dropped.  Runs of at least
+// min_permute_run consecutive qubit-permutation gates become one permutation
+// step (is_permute).
 std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int n, const PassConfig& cfg);
 
 }  // namespace tilesim

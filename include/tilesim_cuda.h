@@ -222,7 +222,8 @@ int tsc_estimate_cost(const tsc_cost_model* cm, int k, uint64_t op_count, int th
 /* Tile-pass grouping (tilesim/pass.hpp) of a fused circuit, as
  * tsg_program_create would do it for precision_bits.  Host only.
  * step_of_gate[n_gates]: step index of each gate (-1: identity, no launch);
- * step_is_pass[n_gates] and step_high[16 * n_gates] (-1 padded) describe
+ * step_is_pass[n_gates] (0 single-gate launch, 1 tile pass, 2 qubit
+ * permutation step) and step_high[16 * n_gates] (-1 padded) describe
  * steps 0 .. *n_steps - 1 (there are never more steps than gates). */
 int tsc_plan_passes(const tsc_circuit* fused, int precision_bits, double zero_tol, double one_tol, int* step_of_gate,
                     int* step_is_pass, int* step_high, uint64_t* n_steps);

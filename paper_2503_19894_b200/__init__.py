@@ -92,7 +92,7 @@ class StepInfo(C.Structure):
                 ("high", C.c_int * 16), ("kernel", C.c_char * 48)]
 
 
-STEP_KINDS = ("gate", "diag_batch", "pass")
+STEP_KINDS = ("gate", "diag_batch", "pass", "permute")
 
 
 class _FusionConfigC(C.Structure):
@@ -592,7 +592,8 @@ class Program:
 
 def plan_passes(fused: Circuit, precision: str = "f64", zero_tol=1e-8, one_tol=1e-8) -> list:
     """Host-only tile-pass grouping (tilesim/pass.hpp) exactly as Program builds it:
-    a list of steps {"gates": [...], "is_pass": bool, "high": [...]} in launch order."""
+    a list of steps {"gates": [...], "is_pass": bool, "is_permute": bool, "high": [...]}
+    in launch order (is_permute: a run of qubit-permutation gates, one k_permute step)."""
     bits = {"f64": 64, "f32": 32, "c128": 64, "c64": 32}[precision]
     g = max(1, len(fused))
     sog = np.zeros(g, dtype=np.int32)
@@ -601,8 +602,8 @@ def plan_passes(fused: Circuit, precision: str = "f64", zero_tol=1e-8, one_tol=1
     ns = _u64()
     _check(_lib.tsc_plan_passes(fused._h, bits, zero_tol, one_tol, sog.ctypes.data_as(_ip), isp.ctypes.data_as(_ip),
                                 high.ctypes.data_as(_ip), C.byref(ns)))
-    steps = [{"gates": [], "is_pass": bool(isp[s]), "high": [int(h) for h in high[16 * s:16 * s + 16] if h >= 0]}
-             for s in range(ns.value)]
+    steps = [{"gates": [], "is_pass": bool(isp[s] == 1), "is_permute": bool(isp[s] == 2),
+              "high": [int(h) for h in high[16 * s:16 * s + 16] if h >= 0]} for s in range(ns.value)]
     for gi in range(len(fused)):
         if sog[gi] >= 0:
             steps[sog[gi]]["gates"].append(gi)

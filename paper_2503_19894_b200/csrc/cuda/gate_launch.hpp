@@ -189,4 +189,17 @@ struct PassLaunch {
 int launch_pass_f64(const PassLaunch& p, cudaStream_t stream, int num_sms);
 int launch_pass_f32(const PassLaunch& p, cudaStream_t stream, int num_sms);
 
+// ---------------------------------------------------------- permutations
+// A run of qubit-permutation gates (SWAP layers) applied as ONE involutive
+// qubit permutation of the state, in place: new[y] = old[P(y)] with P moving
+// index bit q to p[q], p an involution (permute.cu).
+struct PermuteLaunch {
+  int n = 0;
+  void* re = nullptr;
+  void* im = nullptr;
+  int p[64] = {};
+};
+int launch_permute_f64(const PermuteLaunch& p, cudaStream_t stream, int num_sms);
+int launch_permute_f32(const PermuteLaunch& p, cudaStream_t stream, int num_sms);
+
 }  // namespace tsg

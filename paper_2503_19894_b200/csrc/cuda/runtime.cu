@@ -219,8 +219,16 @@ struct ProgramPass {
   std::vector<int> gates;
 };
 
-// One launch of a program: a single gate, a diagonal batch or a tile pass.
-enum StepKind : int { kStepGate = 0, kStepBatch = 1, kStepPass = 2 };
+// A run of qubit-permutation gates as one qubit permutation of the state:
+// one in-place k_permute sweep per involution (one, or two when the composed
+// permutation is not an involution).
+struct ProgramPermute {
+  std::vector<std::vector<int>> invs;  // launch order
+};
+
+// One launch of a program: a single gate, a diagonal batch, a tile pass or a
+// qubit permutation.
+enum StepKind : int { kStepGate = 0, kStepBatch = 1, kStepPass = 2, kStepPermute = 3 };
 struct ProgramStep {
   int kind = kStepGate;
   int gate = 0;   // first gate applied by the step
@@ -237,6 +245,7 @@ struct tsg_program {
   std::vector<ProgramGate> gates;
   std::vector<ProgramBatch> batches;
   std::vector<ProgramPass> passes;
+  std::vector<ProgramPermute> permutes;
   std::vector<ProgramStep> steps;
   void* arena = nullptr;
   double planning_s = 0.0;
@@ -419,6 +428,18 @@ void run_step(tsg_state* st, tsg_program* prog, const ProgramStep& step) {
     b.tables = reinterpret_cast<const double*>(arena + prog->batches[step.index].table_offset);
     st->prec == 64 ? tsg::launch_diag_batch_f64(b, st->stream, st->ctx->num_sms)
                    : tsg::launch_diag_batch_f32(b, st->stream, st->ctx->num_sms);
+    return;
+  }
+  if (step.kind == kStepPermute) {
+    for (const std::vector<int>& inv : prog->permutes[step.index].invs) {
+      tsg::PermuteLaunch pl;
+      pl.n = prog->n;
+      pl.re = st->re;
+      pl.im = st->im;
+      for (int q = 0; q < prog->n; ++q) pl.p[q] = inv[q];
+      st->prec == 64 ? tsg::launch_permute_f64(pl, st->stream, st->ctx->num_sms)
+                     : tsg::launch_permute_f32(pl, st->stream, st->ctx->num_sms);
+    }
     return;
   }
   if (step.kind == kStepPass) {
@@ -1125,6 +1146,51 @@ bool split_pays(const LaunchStructure& ls, const std::vector<LaunchStructure>& p
   return true;
 }
 
+// The qubit permutation a run of permutation gates applies, as involutions.
+// Index bit q of the result comes from bit src[q] of the input (new[y] =
+// old[Pi(y)], Pi moving bit q to src[q]).  Gate g (targets t, sigma) moves
+// the bit at t[b] to t[sigma[b]].  A permutation that is not an involution
+// is split cycle by cycle into I2 o I1 (reflections of each cycle), applied
+// as the sweep with I2, then the sweep with I1.
+ProgramPermute compose_permutation(const tsg_program* prog, const std::vector<int>& gates) {
+  const int n = prog->n;
+  std::vector<int> src(n);
+  for (int q = 0; q < n; ++q) src[q] = q;
+  for (int gi : gates) {
+    const LaunchStructure& ls = prog->gates[gi].ls;
+    std::vector<int> sigma;
+    if (!qubit_permutation(ls, &sigma)) throw SimError("permutation step: gate is not a qubit permutation");
+    std::vector<int> next = src;
+    for (int b = 0; b < ls.ks; ++b) next[ls.sub_targets[sigma[b]]] = src[ls.sub_targets[b]];
+    src = std::move(next);
+  }
+  ProgramPermute out;
+  bool invol = true;
+  for (int q = 0; q < n; ++q) invol &= src[src[q]] == q;
+  if (invol) {
+    out.invs.push_back(src);
+    return out;
+  }
+  std::vector<int> i1(n), i2(n);
+  std::vector<bool> seen(n, false);
+  for (int q = 0; q < n; ++q) {
+    if (seen[q]) continue;
+    std::vector<int> cyc;
+    for (int r = q; !seen[r]; r = src[r]) {
+      seen[r] = true;
+      cyc.push_back(r);
+    }
+    const int m = static_cast<int>(cyc.size());
+    for (int k = 0; k < m; ++k) {
+      i1[cyc[k]] = cyc[(m - k) % m];      // c_k -> c_{-k}
+      i2[cyc[k]] = cyc[(m + 1 - k) % m];  // c_k -> c_{1-k}
+    }
+  }
+  out.invs.push_back(i2);
+  out.invs.push_back(i1);
+  return out;
+}
+
 // Steps of a program: tile passes (tilesim/pass.hpp) when the state holds at
 // least one tile, else per-gate launches with diagonal batches.
 void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
@@ -1138,7 +1204,12 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
       ProgramStep step;
       step.gate = st.gates.front();
       step.n_gates = static_cast<int>(st.gates.size());
-      if (st.is_pass) {
+      if (st.is_permute) {
+        step.kind = kStepPermute;
+        step.index = static_cast<int>(prog->permutes.size());
+        prog->permutes.push_back(compose_permutation(prog, st.gates));
+        for (size_t i = 1; i < st.gates.size(); ++i) prog->gates[st.gates[i]].in_batch = true;
+      } else if (st.is_pass) {
         step.kind = kStepPass;
         step.index = static_cast<int>(prog->passes.size());
         prog->passes.push_back(prog->prec == 64 ? build_pass<double>(prog, st, cfg, arena)
@@ -1225,6 +1296,13 @@ std::unique_ptr<tsg_program> build_program(tsg_ctx* ctx, const Circuit& fused, d
   for (const ProgramStep& step : prog->steps) {  // one launch per step (block splits: one per part)
     const ProgramGate& pg = prog->gates[step.gate];
     const bool split = step.kind == kStepGate && !pg.subs.empty();
+    if (step.kind == kStepPermute) {
+      const uint64_t sweeps = prog->permutes[step.index].invs.size();
+      prog->launches += sweeps;
+      prog->bytes += sweeps * 2 * (uint64_t{1} << prog->n) * amp;
+      prog->touched_bytes += sweeps * 2 * (uint64_t{1} << prog->n) * amp;
+      continue;
+    }
     prog->launches += split ? pg.subs.size() : 1;
     prog->bytes += 2 * (uint64_t{1} << prog->n) * amp;
     double frac = step.kind != kStepGate ? 1.0 : touched_fraction(pg.ls);
@@ -1805,7 +1883,10 @@ int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* ou
     out->first_gate = static_cast<uint64_t>(st.gate);
     out->n_gates = static_cast<uint64_t>(st.n_gates);
     std::string name;
-    if (st.kind == kStepPass) {
+    if (st.kind == kStepPermute) {
+      const size_t sweeps = prog->permutes[st.index].invs.size();
+      name = sweeps == 1 ? "k_permute" : "k_permute x" + std::to_string(sweeps);
+    } else if (st.kind == kStepPass) {
       const ProgramPass& pp = prog->passes[st.index];
       out->n_high = pp.launch.tile_log2 - pp.launch.run_log2;
       for (int h = 0; h < out->n_high; ++h) out->high[h] = pp.launch.high[h];

@@ -220,7 +220,7 @@ int tsc_plan_passes(const tsc_circuit* fused, int precision_bits, double zero_to
     for (size_t s = 0; s < steps.size(); ++s) {
       if (step_of_gate)
         for (int g : steps[s].gates) step_of_gate[g] = static_cast<int>(s);
-      if (step_is_pass) step_is_pass[s] = steps[s].is_pass ? 1 : 0;
+      if (step_is_pass) step_is_pass[s] = steps[s].is_pass ? 1 : (steps[s].is_permute ? 2 : 0);
       if (step_high)
         for (int h = 0; h < 16; ++h)
           step_high[16 * s + h] = h < static_cast<int>(steps[s].high.size()) ? steps[s].high[h] : -1;

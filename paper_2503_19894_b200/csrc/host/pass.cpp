@@ -32,6 +32,7 @@ PassConfig pass_config(int precision_bits) {
   }
   const char* f = std::getenv("TSG_PASS_FORCE");
   c.force = f && f[0] == '1';
+  if (std::getenv("TSG_NO_PERMUTE")) c.min_permute_run = 0;
   return c;
 }
 
@@ -162,6 +163,39 @@ double standalone_sweeps(const LaunchStructure& ls, const PassConfig& cfg) {
   return cfg.standalone_sweeps * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
 }
 
+bool qubit_permutation(const LaunchStructure& ls, std::vector<int>* sigma) {
+  if (ls.klass == KernelClass::Identity || ls.klass == KernelClass::Diagonal || !ls.controls.empty() || ls.ks < 1)
+    return false;
+  const int D = 1 << ls.ks;
+  if (static_cast<int>(ls.sub_re.size()) != D * D) return false;
+  std::vector<int> dest(D, -1);  // column j -> row of its single 1
+  for (int r = 0; r < D; ++r)
+    for (int c = 0; c < D; ++c) {
+      const double re = ls.sub_re[static_cast<size_t>(r) * D + c], im = ls.sub_im[static_cast<size_t>(r) * D + c];
+      if (im != 0.0 || (re != 0.0 && re != 1.0)) return false;
+      if (re == 1.0) {
+        if (dest[c] >= 0) return false;
+        dest[c] = r;
+      }
+    }
+  std::vector<int> sg(ls.ks);
+  for (int b = 0; b < ls.ks; ++b) {
+    const int d = dest[1 << b];
+    if (d <= 0 || (d & (d - 1)) != 0) return false;
+    sg[b] = __builtin_ctz(static_cast<unsigned>(d));
+  }
+  for (int j = 0; j < D; ++j) {
+    int y = 0;
+    for (int b = 0; b < ls.ks; ++b) y |= ((j >> b) & 1) << sg[b];
+    if (dest[j] != y) return false;
+  }
+  bool moves = false;
+  for (int b = 0; b < ls.ks; ++b) moves |= sg[b] != b;
+  if (!moves) return false;
+  if (sigma) *sigma = sg;
+  return true;
+}
+
 std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int n, const PassConfig& cfg) {
   std::vector<PassStep> steps;
   const int L = cfg.run_log2, M = cfg.tile_log2;
@@ -206,6 +240,25 @@ std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int
   for (int i = 0; i < static_cast<int>(gates.size()); ++i) {
     const LaunchStructure& ls = gates[i];
     if (ls.klass == KernelClass::Identity) continue;
+    if (passes_possible && cfg.min_permute_run > 0 && qubit_permutation(ls, nullptr)) {
+      // a run of consecutive qubit permutations (identity gates in between ignored)
+      std::vector<int> run;
+      int j = i;
+      for (; j < static_cast<int>(gates.size()); ++j) {
+        if (gates[j].klass == KernelClass::Identity) continue;
+        if (!qubit_permutation(gates[j], nullptr)) break;
+        run.push_back(j);
+      }
+      if (static_cast<int>(run.size()) >= cfg.min_permute_run) {
+        flush();
+        PassStep s;
+        s.is_permute = true;
+        s.gates = std::move(run);
+        steps.push_back(std::move(s));
+        i = j - 1;
+        continue;
+      }
+    }
     PassRole role = passes_possible ? pass_role(ls, cfg) : PassRole::Standalone;
     if (role != PassRole::Standalone && !cfg.force && pass_op_sweeps(ls, cfg) >= standalone_sweeps(ls, cfg))
       role = PassRole::Standalone;  // cheaper on its own kernel
