@@ -64,8 +64,16 @@ struct DmmaShape {
 };
 // 8 n-blocks per warp where registers allow; 4 for the widest sub-gates so
 // that 16 consumer warps fit per SM (DMMA issue needs the warps).
+#ifndef TSG_D5_AMPS
+#define TSG_D5_AMPS 11
+#endif
+#ifndef TSG_D5_NRB
+#define TSG_D5_NRB 4
+#endif
 template <typename Real, int KS>
-using DShape = DmmaShape<KS, sizeof(Real) == 8 ? 11 : 12, (KS >= 5 || (sizeof(Real) == 4 && KS >= 4)) ? 4 : 8>;
+using DShape = DmmaShape<KS, sizeof(Real) == 8 ? (KS == 5 ? TSG_D5_AMPS : 11) : 12,
+                         (sizeof(Real) == 8 && KS == 5) ? TSG_D5_NRB
+                                                        : ((KS >= 5 || (sizeof(Real) == 4 && KS >= 4)) ? 4 : 8)>;
 
 // Real = storage type of the state (double: complex128, float: complex64);
 // the product always runs in FP64 on the DMMA pipe (complex64 amplitudes are

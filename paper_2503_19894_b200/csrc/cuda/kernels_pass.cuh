@@ -389,12 +389,17 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
   const int n_groups = ops[o].ks, nT = ops[o].log2_groups, nX = ops[o].log2_rsplit;
   ++o;
   if (n_groups > 0) {
-    // build: entry e of group g = product over members (inactive controls skip)
+    // build: entry e of group g = product over members (inactive controls
+    // skip); the groups' entries are laid out back to back in gtab (at most
+    // kPassMaxGEntries <= kPassThreads), so thread tid builds flat entry tid:
+    // every group in parallel, one short member chain per thread
+    static_assert(kPassMaxGEntries <= kPassThreads, "one group entry per thread");
     int og = o;
     for (int g = 0; g < n_groups; ++g) {
       const PassOp& gh = ops[og];
       const int sbits = gh.ks, m = gh.log2_groups;
-      for (int e = tid; e < (1 << sbits); e += kPassThreads) {
+      const int e = tid - gh.data_off;
+      if (e >= 0 && e < (1 << sbits)) {
         // two interleaved partial products halve the dependent multiply chain
         Real fr[2] = {Real(1), Real(1)}, fi[2] = {Real(0), Real(0)};
         for (int t = 1; t <= m; ++t) {

@@ -145,10 +145,14 @@ __host__ __device__ constexpr size_t umma_fixed_smem() {
   using U = UmmaShape<KS>;
   return 3 * size_t{U::kBBytes} + U::N * sizeof(float);  // B slices, B row scales
 }
-// registers for two CTAs per SM (multiple of 8)
+// registers for two CTAs per SM: the register file is split over the four
+// SM sub-partitions, and 2 x 9 warps put 5 warps on some of them, so a
+// thread may hold 16384 / (5 * 32) = 102 registers (multiple of 8: 96) --
+// 112 registers left room for only one CTA per SM (ncu occupancy limit)
 template <int KS>
 constexpr int umma_max_regs() {
-  return (65536 / (2 * (UmmaShape<KS>::T + 32))) / 8 * 8;  // 112
+  constexpr int warps = 2 * (UmmaShape<KS>::T / 32 + 1);
+  return (16384 / (((warps + 3) / 4) * 32)) / 8 * 8;
 }
 
 template <int KS, int STAGES>
