@@ -509,6 +509,35 @@ bool try_umma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   // geometry without chunked runs (the simt layout): one bulk copy per run
   if (!dmma_geometry<float, KS>(g, p, &dsmem, &dstages, /*simt=*/true)) return false;
   if (p.chunk_log2 != p.L) return false;
+  // Low targets or controls spread a warp's groups (one per lane) through the
+  // run: when their stage reads would pile 16 or more lanes onto one bank,
+  // cut the runs into padded 64-amplitude chunks (more, smaller bulk copies;
+  // measured slower below that conflict degree)
+  auto degree = [&](int chunk_log2, uint32_t chunk_stride) {
+    int words[32] = {0}, worst = 0;
+    for (uint32_t l = 0; l < 32; ++l) {
+      uint32_t gp = 0;
+      for (int i = 0; i < p.n_gmask; ++i) gp += (l & p.gmask[i]) << i;
+      gp |= p.ctrl_lo;
+      const uint32_t a = (gp >> chunk_log2) * chunk_stride + (gp & ((1u << chunk_log2) - 1));
+      worst = std::max(worst, ++words[a % 32]);
+    }
+    return worst;
+  };
+  static const bool chunking = !std::getenv("TSG_UMMA_NO_CHUNK");
+  const uint32_t cstride = 64 + kRunPadBytes / sizeof(float);
+  if (chunking && p.L > 6 && degree(p.L, p.run_stride) >= 16 && degree(6, cstride) <= 4) {
+    uint32_t low_of[1 << KS], run_of[1 << KS];
+    for (int j = 0; j < (1 << KS); ++j) {  // each element's run and in-run offset
+      run_of[j] = p.soff[j] / p.run_stride;
+      low_of[j] = p.soff[j] % p.run_stride;
+    }
+    p.chunk_log2 = 6;
+    p.chunk_stride = cstride;
+    p.run_stride = (1u << (p.L - 6)) * p.chunk_stride;
+    for (int j = 0; j < (1 << KS); ++j)
+      p.soff[j] = run_of[j] * p.run_stride + (low_of[j] >> 6) * p.chunk_stride + (low_of[j] & 63u);
+  }
   p.re = static_cast<float*>(g.re);
   p.im = static_cast<float*>(g.im);
   p.mat = static_cast<const double*>(g.dev_mat);

@@ -171,7 +171,12 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const uint32_t run_bytes = (1u << p.L) * sizeof(float);
+  // runs are copied as 2^chunk_log2-amplitude chunks, chunk_stride apart
+  // (one chunk per run unless a low target makes the lanes' groups stride
+  // through the run: then 256-byte chunks, padded, spread them over banks)
+  const int chunk_shift = p.L - p.chunk_log2;
+  const int n_chunks = p.n_runs << chunk_shift;
+  const uint32_t chunk_bytes = (1u << p.chunk_log2) * sizeof(float);
   const uint64_t first = blockIdx.x, step = gridDim.x;
 
   if (tid == 0) {
@@ -240,13 +245,14 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
       lstream.advance();
       float* dr = buf + (2 * s) * stage_elems;
       float* di = dr + stage_elems;
-      if (lane == 0) mbar_expect_tx(&full[s], 2u * run_bytes * static_cast<uint32_t>(p.n_runs));
+      if (lane == 0) mbar_expect_tx(&full[s], 2u * chunk_bytes * static_cast<uint32_t>(n_chunks));
       __syncwarp();
-      for (int r = lane; r < p.n_runs; r += 32) {
-        const uint32_t so = r * p.run_stride;
-        const uint64_t go = base + p.roff[r];
-        bulk_g2s(dr + so, p.re + go, run_bytes, &full[s]);
-        bulk_g2s(di + so, p.im + go, run_bytes, &full[s]);
+      for (int c = lane; c < n_chunks; c += 32) {
+        const int r = c >> chunk_shift, q = c & ((1 << chunk_shift) - 1);
+        const uint32_t so = r * p.run_stride + q * p.chunk_stride;
+        const uint64_t go = base + p.roff[r] + (static_cast<uint64_t>(q) << p.chunk_log2);
+        bulk_g2s(dr + so, p.re + go, chunk_bytes, &full[s]);
+        bulk_g2s(di + so, p.im + go, chunk_bytes, &full[s]);
       }
     };
     for (int s = 0; s < STAGES; ++s)
@@ -266,6 +272,7 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
   // (t mod G) / 128), part t / G of the row's columns (warp-uniform)
   const int grp = tid % U::G, part = U::TPG > 1 ? tid / U::G : 0;  // (compile-time 0 for KS = 4: column indices stay static)
   const uint32_t gpos = dmma_group_pos(p, static_cast<uint32_t>(grp));  // raw in-run position
+  const uint32_t spos = dmma_pad(p, gpos);                               // its shared-memory offset
   const uint32_t row = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
                        static_cast<uint32_t>((grp >> 7) * U::BLK);  // this group's TMEM lane, its block
   const uint32_t b_addr = smem_addr(b_ops);
@@ -284,8 +291,8 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
     float m = 0.0f;
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-      v[c] = xr[p.soff[c] + gpos];
-      v[D + c] = xi[p.soff[c] + gpos];
+      v[c] = xr[p.soff[c] + spos];
+      v[D + c] = xi[p.soff[c] + spos];
       m = fmaxf(m, fmaxf(fabsf(v[c]), fabsf(v[D + c])));
     }
     __syncwarp();

@@ -6,7 +6,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("PB_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2503_19894_b200 as ts  # noqa: E402
 
 kind, n, kmax, first, count = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])

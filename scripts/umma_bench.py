@@ -10,8 +10,9 @@ from tests._util import random_gate_matrix  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 kss = [int(x) for x in sys.argv[2:]] or [3, 4, 5]
 sets = {3: [[0, 1, 2], [3, 4, 5], [8, 9, 10], [20, 25, 29], [2, 9, 17]],
-        4: [[0, 1, 2, 3], [4, 5, 6, 7], [8, 9, 10, 11], [26, 27, 28, 29], [1, 9, 17, 25]],
-        5: [[0, 1, 2, 3, 4], [5, 6, 7, 8, 9], [10, 11, 12, 13, 14], [25, 26, 27, 28, 29], [0, 7, 14, 21, 28]]}
+        4: [[0, 1, 2, 3], [4, 5, 6, 7], [8, 9, 10, 11], [26, 27, 28, 29], [1, 9, 17, 25], [2, 3, 4, 5], [1, 2, 3, 4]],
+        5: [[0, 1, 2, 3, 4], [5, 6, 7, 8, 9], [10, 11, 12, 13, 14], [25, 26, 27, 28, 29], [0, 7, 14, 21, 28],
+            [1, 2, 3, 4, 5], [3, 7, 10, 12, 15]]}
 sv = ts.Statevector(n, "f32").init_zero()
 bytes_ = 2 * 8 * (1 << n)
 for ks in kss:

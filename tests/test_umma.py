@@ -38,6 +38,7 @@ def _state(n, seed):
     ([4, 5, 6, 7], "dense"), ([1, 5, 9, 13], "dense"), ([12, 13, 14, 15], "dense"), ([2, 3, 11, 12], "dense"),
     ([5, 6, 7, 8, 9], "dense"), ([3, 7, 10, 12, 15], "dense"), ([11, 12, 13, 14, 15], "dense"),
     ([2, 6, 7, 8, 9], "controlled"), ([3, 4, 5, 9, 14, 15], "controlled"), ([1, 2, 3, 4, 5, 6], "controlled"),
+    ([2, 3, 4, 5], "dense"), ([1, 2, 3, 4], "dense"), ([1, 2, 3, 4, 5], "dense"),  # chunked stage (low targets)
 ])
 def test_umma_gate_matches_numpy(targets, kind):
     n = 16
