@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="print the per-kernel-class table to stderr")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded (NCCL) step even on one GPU (0 global qubits: exercises that path)")
     return ap.parse_args()
 
 
@@ -73,11 +75,17 @@ class Dist:
             self.dist.barrier()
 
     def max(self, x: float) -> float:
+        return self._reduce(x, "MAX")
+
+    def sum(self, x: float) -> float:
+        return self._reduce(x, "SUM")
+
+    def _reduce(self, x: float, op: str) -> float:
         if self.world == 1:
             return x
         import torch
         t = torch.tensor([x], dtype=torch.float64)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        self.dist.all_reduce(t, op=getattr(self.dist.ReduceOp, op))
         return float(t.item())
 
     def close(self):
@@ -206,10 +214,11 @@ def run_sharded(args, rank, world, local, dist):
         uid = ts.DistState.unique_id()
     else:
         uid = None
-    import torch.distributed as tdist
-    obj = [uid]
-    tdist.broadcast_object_list(obj, src=0)
-    uid = obj[0]
+    if world > 1:
+        import torch.distributed as tdist
+        obj = [uid]
+        tdist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
     (fq, sq), (fr, sr), front_s = build_circuits(ts, n, args.kmax)
     pq, pr = ts.ShardPlan(fq, g), ts.ShardPlan(fr, g)
     d = ts.DistState(n, g, rank, uid, "f64", ctx)
@@ -220,17 +229,37 @@ def run_sharded(args, rank, world, local, dist):
     clocks = ClockSampler(local)
     dist.barrier()
     clocks.start()
-    t_dev, xs, xbytes = 0.0, 0.0, 0
+    t_dev, xs, xbytes, launches = 0.0, 0.0, 0, 0
     for _ in range(args.steps):
         for plan in (pq, pr):
             rep = d.run(plan)
             t_dev += rep["execution_s"]
             xs += rep["exchange_s"]
             xbytes += rep["exchanged_bytes"]
+            launches += rep["launches"]
     clock_info = clocks.stop()
     dist.barrier()
     t_step = dist.max(t_dev / args.steps)
     x_step = dist.max(xs / args.steps)
+    # e2e through the public API: generate + fuse + shard plans + init + run +
+    # a host-side result (this rank's squared norm, summed over ranks)
+    e2e = None
+    if not args.no_e2e:
+        times = []
+        for _ in range(max(1, min(args.steps, 2))):
+            dist.barrier()
+            t0 = time.perf_counter()
+            (fq2, _), (fr2, _), _ = build_circuits(ts, n, args.kmax)
+            p1, p2 = ts.ShardPlan(fq2, g), ts.ShardPlan(fr2, g)
+            d.init_basis(0x2AAAAAAA & ((1 << n) - 1))
+            d.run(p1)
+            d.run(p2)
+            nrm = dist.sum(d.local_sumsq())
+            times.append(time.perf_counter() - t0)
+            assert abs(nrm - 1.0) < 1e-6, nrm
+        h2d = sum(gt.matrix.size * 16 + 4 * len(gt.targets) for gt in fq.gates() + fr.gates())
+        e2e = {"value": dist.max(statistics.median(times)), "unit": "s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 8, "includes": "generate+fuse+shard-plan+init+run+norm readback"}
     if rank == 0:
         iq, ir = pq.info(), pr.info()
         print(json.dumps({
@@ -245,14 +274,14 @@ def run_sharded(args, rank, world, local, dist):
             "exchange": {"seconds_per_step": x_step, "bytes_per_rank_per_step": xbytes // max(1, args.steps),
                          "nvlink_GBps": (xbytes / max(1, args.steps)) / x_step / 1e9 if x_step > 0 else None,
                          "exposed": "exchanges are not overlapped yet (exposed = seconds_per_step)"},
-            "gpu_launches": None, "clocks": clock_info, "e2e": None, "cpu_baseline": None}))
+            "gpu_launches": launches, "clocks": clock_info, "e2e": e2e, "cpu_baseline": None}))
     dist.close()
 
 
 def run_ours(args):
     rank, world, local = dist_env()
     dist = Dist(world)
-    if world > 1:
+    if world > 1 or args.sharded:
         return run_sharded(args, rank, world, local, dist)
     import numpy as np
 
