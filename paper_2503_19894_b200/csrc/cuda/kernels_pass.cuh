@@ -35,6 +35,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels_dmma.cuh"
 
@@ -514,6 +515,77 @@ struct PassCopy {
   static_assert(S::kRunLen % kEpc == 0, "runs are whole chunks");
 };
 
+// Registers <-> tile in shared memory.  When the layout's lowest register
+// positions are the tile's lowest positions (vb of them), the registers
+// i .. i + 2^vb - 1 are consecutive elements of one 16-byte unit: one vector
+// access each (complex64: a warp then moves whole 16-byte units instead of
+// piling 4-byte accesses onto a few banks; complex128 keeps scalar moves).
+template <typename Real, int R>
+__device__ __forceinline__ void regs_to_smem(Real* xr, Real* xi, const uint32_t (&at)[R], const Real (&ar)[R],
+                                             const Real (&ai)[R], int vb) {
+  if constexpr (sizeof(Real) == 4 && R % 4 == 0) {
+    if (vb >= 2) {
+#pragma unroll
+      for (int i = 0; i < R; i += 4) {
+        *reinterpret_cast<float4*>(xr + at[i]) = make_float4(ar[i], ar[i + 1], ar[i + 2], ar[i + 3]);
+        *reinterpret_cast<float4*>(xi + at[i]) = make_float4(ai[i], ai[i + 1], ai[i + 2], ai[i + 3]);
+      }
+      return;
+    }
+  }
+  if constexpr (sizeof(Real) == 4 && R % 2 == 0) {
+    if (vb >= 1) {
+      using V2 = float2;
+#pragma unroll
+      for (int i = 0; i < R; i += 2) {
+        *reinterpret_cast<V2*>(xr + at[i]) = V2{ar[i], ar[i + 1]};
+        *reinterpret_cast<V2*>(xi + at[i]) = V2{ai[i], ai[i + 1]};
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    xr[at[i]] = ar[i];
+    xi[at[i]] = ai[i];
+  }
+}
+
+template <typename Real, int R>
+__device__ __forceinline__ void smem_to_regs(const Real* xr, const Real* xi, const uint32_t (&at)[R], Real (&ar)[R],
+                                             Real (&ai)[R], int vb) {
+  if constexpr (sizeof(Real) == 4 && R % 4 == 0) {
+    if (vb >= 2) {
+#pragma unroll
+      for (int i = 0; i < R; i += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(xr + at[i]);
+        const float4 b = *reinterpret_cast<const float4*>(xi + at[i]);
+        ar[i] = a.x, ar[i + 1] = a.y, ar[i + 2] = a.z, ar[i + 3] = a.w;
+        ai[i] = b.x, ai[i + 1] = b.y, ai[i + 2] = b.z, ai[i + 3] = b.w;
+      }
+      return;
+    }
+  }
+  if constexpr (sizeof(Real) == 4 && R % 2 == 0) {
+    if (vb >= 1) {
+      using V2 = float2;
+#pragma unroll
+      for (int i = 0; i < R; i += 2) {
+        const V2 a = *reinterpret_cast<const V2*>(xr + at[i]);
+        const V2 b = *reinterpret_cast<const V2*>(xi + at[i]);
+        ar[i] = a.x, ar[i + 1] = a.y;
+        ai[i] = b.x, ai[i + 1] = b.y;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    ar[i] = xr[at[i]];
+    ai[i] = xi[at[i]];
+  }
+}
+
 template <typename Real, int M, int L, int STAGES>
 __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant__ PassParams p) {
   using S = PassShape<Real, M, L>;
@@ -589,6 +661,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
   constexpr int R = S::kIter;  // amplitudes per thread (register layout)
   Real ar[R], ai[R];
   uint32_t at[R];      // padded shared-memory offsets of the registers (current layout)
+  int vb = 0;          // vector width (log2) of the current layout's register <-> smem moves
   uint32_t xt = 0;     // tile coordinate of the thread part of the current layout
   uint32_t irun = 0;   // runs with diagonal groups so far (table double-buffering)
   uint32_t j = 0;
@@ -619,11 +692,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
       const int kind = op.kind;
       if (kind == kPassLayout) {
         if (!in_smem) {
-#pragma unroll
-          for (int i = 0; i < R; ++i) {
-            xr[at[i]] = ar[i];
-            xi[at[i]] = ai[i];
-          }
+          regs_to_smem<Real, R>(xr, xi, at, ar, ai, vb);
           consumer_bar();  // the tile is in shared memory in full
         } else if (o > 0) {
           consumer_bar();  // after shared-memory ops: their writes are visible
@@ -641,9 +710,9 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
           for (int k = 0; k < kBits; ++k)
             if ((i >> k) & 1) a += pd[k];
           at[i] = a;
-          ar[i] = xr[a];
-          ai[i] = xi[a];
         }
+        vb = op.ks;  // vector width of this layout (host: lowest register positions = lowest tile positions)
+        smem_to_regs<Real, R>(xr, xi, at, ar, ai, vb);
         in_smem = false;
         ++o;
       } else if (kind == kPassRun) {
@@ -660,11 +729,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
         ++o;
       } else {  // SGen / SPerm: through shared memory
         if (!in_smem) {
-#pragma unroll
-          for (int i = 0; i < R; ++i) {
-            xr[at[i]] = ar[i];
-            xi[at[i]] = ai[i];
-          }
+          regs_to_smem<Real, R>(xr, xi, at, ar, ai, vb);
           in_smem = true;
         }
         consumer_bar();
@@ -674,22 +739,12 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
         ++o;
         if (o < p.n_ops && ops[o].kind != kPassSGen && ops[o].kind != kPassSPerm && ops[o].kind != kPassLayout) {
           consumer_bar();  // back to the registers of the current layout
-#pragma unroll
-          for (int i = 0; i < R; ++i) {
-            ar[i] = xr[at[i]];
-            ai[i] = xi[at[i]];
-          }
+          smem_to_regs<Real, R>(xr, xi, at, ar, ai, vb);
           in_smem = false;
         }
       }
     }
-    if (!in_smem) {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        xr[at[i]] = ar[i];
-        xi[at[i]] = ai[i];
-      }
-    }
+    if (!in_smem) regs_to_smem<Real, R>(xr, xi, at, ar, ai, vb);
     consumer_bar();  // all ops done: write the tile back
     const Real* st = buf + (2 * s) * S::kStageElems;
 #pragma unroll

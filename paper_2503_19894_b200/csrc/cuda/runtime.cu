@@ -569,10 +569,13 @@ struct PassGeom {
       if (P[k] == p) return k;
     return -1;
   }
-  int thread_bit(int p) const {  // index among the non-register positions
-    int b = 0;
-    for (int q = 0; q < p; ++q) b += reg_bit(q) < 0;
-    return b;
+  // thread-id bit b -> tile position: the non-register positions, lanes
+  // (bits 0-4) first; set by build_layout_op for each layout
+  std::vector<int> tpos;
+  int thread_bit(int p) const {
+    for (size_t b = 0; b < tpos.size(); ++b)
+      if (tpos[b] == p) return static_cast<int>(b);
+    return -1;
   }
 };
 
@@ -590,23 +593,32 @@ tsg::PassOp blank_op(int kind) {
 }
 
 template <typename Real>
-tsg::PassOp build_layout_op(const PassGeom& g, std::vector<unsigned char>& data) {
+tsg::PassOp build_layout_op(PassGeom& g, std::vector<unsigned char>& data) {
   tsg::PassOp op = blank_op(tsg::kPassLayout);
-  std::vector<int> P = g.P;
-  uint64_t gm[16];
   if (g.r + 1 > 6) throw SimError("pass: too many register positions");
-  op.n_xmask = tsg::insertion_masks(P.data(), g.r, g.M - g.r, gm);
-  for (int m = 0; m < op.n_xmask; ++m) op.xmask[m] = static_cast<uint32_t>(gm[m]);
-  // per-thread tile coordinate of the thread part (deposit of tid over the
-  // non-register positions), looked up instead of recomputed every tile
+  std::vector<int> free_pos;
+  for (int p = 0; p < g.M; ++p)
+    if (g.reg_bit(p) < 0) free_pos.push_back(p);
+  if (static_cast<int>(free_pos.size()) != tsg::kPassLogThreads) throw SimError("pass: thread positions");
+  g.tpos = free_pos;  // ascending: lanes on the lowest free positions
+  // per-thread tile coordinate of the thread part, looked up instead of
+  // recomputed every tile
   pad16(data);
   op.aux_off = static_cast<int32_t>(data.size());
   for (uint32_t t = 0; t < static_cast<uint32_t>(tsg::kPassThreads); ++t) {
-    uint64_t x = 0;
-    for (int m = 0; m < op.n_xmask; ++m) x += (t & gm[m]) << m;
-    append_pod(data, static_cast<uint32_t>(x));
+    uint32_t x = 0;
+    for (size_t b = 0; b < g.tpos.size(); ++b) x |= ((t >> b) & 1u) << g.tpos[b];
+    append_pod(data, x);
   }
   for (int k = 0; k < g.r; ++k) op.dep[k] = static_cast<uint32_t>(padded_offset<Real>(1u << g.P[k], g.L));
+  // vector width of the register <-> shared-memory moves: register positions
+  // 0, 1, .. = tile positions 0, 1, .. keep 2^vb registers in one 16-byte unit
+  // (complex64 only: HES-30 pass 32.3 -> 24.2 ms; the kernel keeps scalar
+  // moves for complex128, where pairs measured no faster)
+  const int vmax = sizeof(Real) == 4 ? 2 : 0;
+  int vb = 0;
+  while (vb < vmax && vb < g.r && g.P[vb] == vb) ++vb;
+  op.ks = vb;
   return op;
 }
 
