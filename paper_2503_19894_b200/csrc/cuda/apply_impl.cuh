@@ -487,32 +487,22 @@ void launch_umma(const DmmaParams<float, KS>& p, size_t smem, cudaStream_t s, in
   cuda_check(cudaGetLastError(), "k_stream_umma launch");
 }
 
-// Lanes own consecutive groups: a target or control on bit 0 spreads a
-// warp's stage reads over many banks and its global stores over twice the
-// sectors (measured 3-4x slower there than the DMMA product).
-inline bool umma_takes(const GateLaunch& g) {
-  if (!g.dev_mat || !g.full_range || !((umma_ks_mask() >> g.ks) & 1u)) return false;
-  for (int b = 0; b < g.ks; ++b)
-    if (g.sub_targets[b] == 0) return false;
-  for (int c = 0; c < g.n_ctrl; ++c)
-    if (g.ctrl[c] == 0) return false;
-  return true;
-}
-
+// Geometry of a k_stream_umma launch, or false when the gate stays on the
+// DMMA product.  Lanes own consecutive groups, so low targets / controls
+// spread a warp's stage reads over few banks and its global stores over more
+// sectors: with a target or control on bit 0 the tensor-core kernel only
+// takes gates whose lanes stay (nearly) contiguous, e.g. [0, 7, 14, 21, 28]
+// (4.0 ms vs 8.1 ms for the DMMA product; [0, 1, 2, 3]: 11.4 vs 7.4 ms).
 template <int KS>
-bool try_umma(const GateLaunch& g, cudaStream_t s, int num_sms) {
-  if (!umma_takes(g)) return false;
-  DmmaParams<float, KS> p;
+bool umma_plan(const GateLaunch& g, DmmaParams<float, KS>& p) {
+  if (!g.dev_mat || !g.full_range || !((umma_ks_mask() >> KS) & 1u)) return false;
   std::memset(&p, 0, sizeof p);
   size_t dsmem = 0;
   int dstages = 0;
   // geometry without chunked runs (the simt layout): one bulk copy per run
   if (!dmma_geometry<float, KS>(g, p, &dsmem, &dstages, /*simt=*/true)) return false;
   if (p.chunk_log2 != p.L) return false;
-  // Low targets or controls spread a warp's groups (one per lane) through the
-  // run: when their stage reads would pile 16 or more lanes onto one bank,
-  // cut the runs into padded 64-amplitude chunks (more, smaller bulk copies;
-  // measured slower below that conflict degree)
+  // most words any bank receives from the 32 lanes' first stage read
   auto degree = [&](int chunk_log2, uint32_t chunk_stride) {
     int words[32] = {0}, worst = 0;
     for (uint32_t l = 0; l < 32; ++l) {
@@ -524,9 +514,17 @@ bool try_umma(const GateLaunch& g, cudaStream_t s, int num_sms) {
     }
     return worst;
   };
+  const int d0 = degree(p.L, p.run_stride);
+  bool bit0 = false;
+  for (int b = 0; b < g.ks; ++b) bit0 |= g.sub_targets[b] == 0;
+  for (int c = 0; c < g.n_ctrl; ++c) bit0 |= g.ctrl[c] == 0;
+  if (bit0 && d0 > 2) return false;
+  // Runs whose stage reads would pile 16 or more lanes onto one bank are cut
+  // into padded 64-amplitude chunks (more, smaller bulk copies: measured
+  // slower below that conflict degree)
   static const bool chunking = !std::getenv("TSG_UMMA_NO_CHUNK");
   const uint32_t cstride = 64 + kRunPadBytes / sizeof(float);
-  if (chunking && p.L > 6 && degree(p.L, p.run_stride) >= 16 && degree(6, cstride) <= 4) {
+  if (chunking && p.L > 6 && d0 >= 16 && degree(6, cstride) <= 4) {
     uint32_t low_of[1 << KS], run_of[1 << KS];
     for (int j = 0; j < (1 << KS); ++j) {  // each element's run and in-run offset
       run_of[j] = p.soff[j] / p.run_stride;
@@ -538,6 +536,25 @@ bool try_umma(const GateLaunch& g, cudaStream_t s, int num_sms) {
     for (int j = 0; j < (1 << KS); ++j)
       p.soff[j] = run_of[j] * p.run_stride + (low_of[j] >> 6) * p.chunk_stride + (low_of[j] & 63u);
   }
+  return true;
+}
+
+inline bool umma_takes(const GateLaunch& g) {
+  if (g.ks == 4) {
+    DmmaParams<float, 4> p;
+    return umma_plan<4>(g, p);
+  }
+  if (g.ks == 5) {
+    DmmaParams<float, 5> p;
+    return umma_plan<5>(g, p);
+  }
+  return false;
+}
+
+template <int KS>
+bool try_umma(const GateLaunch& g, cudaStream_t s, int num_sms) {
+  DmmaParams<float, KS> p;
+  if (!umma_plan<KS>(g, p)) return false;
   p.re = static_cast<float*>(g.re);
   p.im = static_cast<float*>(g.im);
   p.mat = static_cast<const double*>(g.dev_mat);

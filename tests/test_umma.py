@@ -39,6 +39,7 @@ def _state(n, seed):
     ([5, 6, 7, 8, 9], "dense"), ([3, 7, 10, 12, 15], "dense"), ([11, 12, 13, 14, 15], "dense"),
     ([2, 6, 7, 8, 9], "controlled"), ([3, 4, 5, 9, 14, 15], "controlled"), ([1, 2, 3, 4, 5, 6], "controlled"),
     ([2, 3, 4, 5], "dense"), ([1, 2, 3, 4], "dense"), ([1, 2, 3, 4, 5], "dense"),  # chunked stage (low targets)
+    ([0, 7, 11, 15], "dense"), ([0, 6, 9, 12, 14], "dense"),  # bit-0 target, lanes nearly contiguous
 ])
 def test_umma_gate_matches_numpy(targets, kind):
     n = 16
@@ -85,9 +86,14 @@ def test_umma_norm_does_not_drift():
     assert fid >= 1 - 1e-5, 1 - fid
 
 
-def test_umma_skips_bit0_geometry():
-    """A target on qubit 0 goes to the DMMA product (see umma_takes)."""
+def test_umma_bit0_geometry():
+    """A target on qubit 0: the tensor-core kernel only when the lanes stay
+    nearly contiguous (umma_plan); contiguous low targets keep the DMMA product."""
     c = ts.Circuit(14)
-    c.add_matrix([0, 3, 6, 9], random_gate_matrix(4, 3, "dense"))
+    c.add_matrix([0, 1, 2, 3], random_gate_matrix(4, 3, "dense"))
     prog = ts.Program(c, "f32")
     assert [s["kernel"] for s in prog.steps()] == ["k_stream_dmma<ks=4>"]
+    c = ts.Circuit(16)
+    c.add_matrix([0, 7, 11, 15], random_gate_matrix(4, 4, "dense"))
+    prog = ts.Program(c, "f32")
+    assert [s["kernel"] for s in prog.steps()] == ["k_stream_umma<ks=4>"]
