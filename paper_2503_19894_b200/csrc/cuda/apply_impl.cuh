@@ -141,7 +141,10 @@ void run_tile(const GateLaunch& g, cudaStream_t s, int num_sms) {
   p.fixed_or = g.fixed_or;
   p.n_masks = g.n_masks;
   for (int i = 0; i < g.n_masks; ++i) p.masks[i] = g.masks[i];
-  for (int j = 0; j < (1 << KS); ++j) p.off[j] = g.off[j];
+  // dev_mat rows / columns are in the launch's element order (GateLaunch::perm,
+  // chosen for the DMMA kernels; this kernel runs when their tile geometry
+  // does not fit, e.g. states smaller than one DMMA tile)
+  for (int j = 0; j < (1 << KS); ++j) p.off[j] = g.off[g.perm[j]];
   if (p.n_tiles == 0) return;
   auto kern = k_tile<Real, KS, G, RT, GT>;
   static bool configured = false;
@@ -706,6 +709,30 @@ int launch_gate_impl(const GateLaunch& g, cudaStream_t s, int num_sms) {
 
 // Name of the kernel template launch_gate_impl selects for a full-range
 // launch (reports / profiles), e.g. "k_stream_dmma<ks=5>".
+// Whether k_stream_dmma's tile geometry fits the state (else launch_gate_impl
+// falls through to k_tile / k_direct)
+template <typename Real>
+bool dmma_fits(const GateLaunch& g) {
+  size_t smem = 0;
+  int stages = 0;
+  switch (g.ks) {
+    case 3: {
+      DmmaParams<Real, 3> p{};
+      return dmma_geometry<Real, 3>(g, p, &smem, &stages, false);
+    }
+    case 4: {
+      DmmaParams<Real, 4> p{};
+      return dmma_geometry<Real, 4>(g, p, &smem, &stages, false);
+    }
+    case 5: {
+      DmmaParams<Real, 5> p{};
+      return dmma_geometry<Real, 5>(g, p, &smem, &stages, false);
+    }
+    default:
+      return false;
+  }
+}
+
 template <typename Real>
 std::string kernel_name_impl(const GateLaunch& g) {
   constexpr int DM = PrecisionTraits<Real>::kDirectMax;
@@ -713,8 +740,10 @@ std::string kernel_name_impl(const GateLaunch& g) {
   int klass = g.klass;
   if (klass == 0) return "none";
   if ((klass == 2 || klass == 3) && sizeof(Real) == 4 && umma_takes(g)) return "k_stream_umma" + ks + ">";
-  if (g.full_range && (klass == 2 || klass == 3) && g.ks >= 3 && g.ks <= 5 && g.dev_mat)
-    return (dmma_mode() == 1 && sizeof(Real) == 8 ? "k_dmma_direct" : "k_stream_dmma") + ks + ">";
+  if (g.full_range && (klass == 2 || klass == 3) && g.ks >= 3 && g.ks <= 5 && g.dev_mat) {
+    if (dmma_mode() == 1 && sizeof(Real) == 8) return "k_dmma_direct" + ks + ">";
+    if (dmma_fits<Real>(g)) return "k_stream_dmma" + ks + ">";
+  }
   if (klass == 1 && !g.full_range) klass = g.ks <= DM ? 2 : 3;
   if (klass == 2 && g.ks > DM) klass = 3;
   switch (klass) {

@@ -173,3 +173,26 @@ def test_program_graph_and_profile():
     prog.run(a, use_graph=True)  # cached graph replay
     prog.run(b, use_graph=False)
     assert ts.compare_states(a, b) == 0.0
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("n", [5, 6, 8, 10, 12, 13])
+def test_small_states_every_kernel_path(n, prec):
+    """States smaller than a tile pass / a tensor-core tile: the executor must
+    pick kernels that fit (per-gate launches, smaller products) and still match
+    the oracle; random fused circuits with 1..5-qubit blocks."""
+    rng = np.random.default_rng(n * 10 + prec)
+    c = ts.Circuit(n)
+    for i in range(40):
+        k = int(rng.integers(1, min(5, n) + 1))
+        t = sorted(int(q) for q in rng.choice(n, size=k, replace=False))
+        kind = ["dense", "perm", "diag", "controlled"][i % 4] if k > 1 else "dense"
+        c.add_matrix(t, random_gate_matrix(k, 700 + i, kind))
+    fused, _ = ts.run_fusion(c, ts.FusionConfig(k_max=5))
+    sv = ts.Statevector(n, PREC[prec]).init_random(2)
+    re0, im0 = sv.download()
+    ts.run_circuit(fused, sv)
+    dt = np.float64 if prec == 64 else np.float32
+    ore, oim = re0.astype(dt), im0.astype(dt)
+    ob.run_circuit(to_oracle(fused), ore, oim)
+    assert ts.compare_states(sv, (ore.astype(np.float64), oim.astype(np.float64))) <= (1e-10 if prec == 64 else 1e-5)
