@@ -176,11 +176,12 @@ def test_program_graph_and_profile():
 
 
 @pytest.mark.parametrize("prec", [64, 32])
-@pytest.mark.parametrize("n", [5, 6, 8, 10, 12, 13])
-def test_small_states_every_kernel_path(n, prec):
+@pytest.mark.parametrize("n,kmax", [(1, 1), (2, 2), (3, 3), (4, 4), (5, 5), (6, 5), (7, 6), (8, 5), (10, 5),
+                                    (10, 6), (12, 5), (13, 6)])
+def test_small_states_every_kernel_path(n, kmax, prec):
     """States smaller than a tile pass / a tensor-core tile: the executor must
     pick kernels that fit (per-gate launches, smaller products) and still match
-    the oracle; random fused circuits with 1..5-qubit blocks."""
+    the oracle; random fused circuits with 1..kmax-qubit blocks."""
     rng = np.random.default_rng(n * 10 + prec)
     c = ts.Circuit(n)
     for i in range(40):
@@ -188,7 +189,7 @@ def test_small_states_every_kernel_path(n, prec):
         t = sorted(int(q) for q in rng.choice(n, size=k, replace=False))
         kind = ["dense", "perm", "diag", "controlled"][i % 4] if k > 1 else "dense"
         c.add_matrix(t, random_gate_matrix(k, 700 + i, kind))
-    fused, _ = ts.run_fusion(c, ts.FusionConfig(k_max=5))
+    fused, _ = ts.run_fusion(c, ts.FusionConfig(k_max=kmax))
     sv = ts.Statevector(n, PREC[prec]).init_random(2)
     re0, im0 = sv.download()
     ts.run_circuit(fused, sv)
