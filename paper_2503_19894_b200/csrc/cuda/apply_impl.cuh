@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 #include <cstdlib>
@@ -278,7 +279,8 @@ bool try_stream(const GateLaunch& g, cudaStream_t s, int num_sms) {
 
 // ------------------------------------------------------------ stream_dmma
 template <typename Real, int KS>
-bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, int* stages, bool simt) {
+bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, int* stages, bool simt,
+                   bool few_tiles = false) {
   using S = DShape<Real, KS>;
   int tg[24], nt = 0;  // all targets (controls + sub-targets), ascending
   {
@@ -369,7 +371,11 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
     return worst;
   };
   p.chunk_log2 = L;
-  const int chunk = sizeof(Real) == 8 ? 5 : 6;  // 256-byte chunks
+  // 256-byte chunks; complex128 products with at most half of their 8 x 4
+  // tiles nonzero are bound by the producer's copy issue rather than by the
+  // B-fragment loads: 512-byte chunks (half the bulk copies; RQC-30's
+  // 5-qubit launches 186 -> 179 ms, dense ones measured better at 256)
+  const int chunk = sizeof(Real) == 8 ? (few_tiles ? 6 : 5) : 6;
   // only for ks = 5, whose stages are loaded and never bulk-stored: more,
   // smaller bulk copies measured slower for the HBM-bound ks <= 4 kernels
   const bool direct_out = KS >= 5 || (sizeof(Real) == 4 && KS >= 4);  // k_stream_dmma kDirectOut
@@ -428,10 +434,6 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   for (int b = 0; b < g.ks; ++b) lowest = std::min(lowest, g.sub_targets[b]);
   for (int c = 0; c < g.n_ctrl; ++c) lowest = std::min(lowest, g.ctrl[c]);
   const bool simt = sizeof(Real) == 4 && KS <= 3 && lowest >= 5;
-  if (!dmma_geometry<Real, KS>(g, p, &smem, &stages, simt)) return false;
-  p.re = static_cast<Real*>(g.re);
-  p.im = static_cast<Real*>(g.im);
-  p.mat = static_cast<const double*>(g.dev_mat);
   constexpr int D = S::D;
   for (int rb = 0; rb < S::RB; ++rb)
     for (int k = 0; k < S::KST; ++k) {
@@ -449,6 +451,16 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
       p.nzblk[2] |= static_cast<uint32_t>(nzs) << bit;
     }
   const bool sparse = (p.nzblk[0] & p.nzblk[1] & p.nzblk[2]) != (S::RB * S::KST >= 32 ? ~0u : ((1u << (S::RB * S::KST)) - 1));
+  const int most = std::max({__builtin_popcount(p.nzblk[0]), __builtin_popcount(p.nzblk[1]), __builtin_popcount(p.nzblk[2])});
+  if (!dmma_geometry<Real, KS>(g, p, &smem, &stages, simt, 2 * most <= S::RB * S::KST)) return false;
+  p.re = static_cast<Real*>(g.re);
+  p.im = static_cast<Real*>(g.im);
+  p.mat = static_cast<const double*>(g.dev_mat);
+  static const bool debug = std::getenv("TSG_DMMA_DEBUG") != nullptr;
+  if (debug)
+    std::fprintf(stderr, "dmma ks=%d L=%d chunk=%d runs=%d stages=%d smem=%zu tiles=%d/%d/%d of %d sparse=%d\n", KS, p.L,
+                 p.chunk_log2, p.n_runs, stages, smem, __builtin_popcount(p.nzblk[0]), __builtin_popcount(p.nzblk[1]),
+                 __builtin_popcount(p.nzblk[2]), S::RB * S::KST, sparse ? 1 : 0);
   switch (stages) {
     case 3:
       sparse ? launch_dmma_pick<Real, KS, 3, true>(p, smem, s, num_sms, simt)
