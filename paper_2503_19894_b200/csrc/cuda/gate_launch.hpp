@@ -155,7 +155,9 @@ struct PassOp {  // 192 bytes, built on the host, read from shared memory
   uint8_t tb_pos[8], tb_jbit[8];  // RGen / RPerm: block bits on thread positions
   int32_t n_tb;
   int32_t n_xmask;
-  uint8_t reserved[32];
+  int32_t thr_off;  // RGen / RPerm: per-thread u8 table (block bits from thread positions, 0xff: thread
+                    // controls inactive), -1 when the op has neither
+  uint8_t reserved[28];
 };
 static_assert(sizeof(PassOp) == 192, "PassOp layout");
 

@@ -290,25 +290,35 @@ __host__ __device__ constexpr int deposit_c(int j, int mask) {
 // sub-group s (register index with the RM bits clear) uses block
 // tc | thread-position block bits | register block bits of s.
 template <typename Real, int R, int RM, bool PERM>
-__device__ __forceinline__ void reg_gen(const PassOp& op, const unsigned char* blob, uint32_t tc, uint32_t xt,
+__device__ __forceinline__ void reg_gen(const PassOp& op, const unsigned char* blob, uint32_t tc, int tid,
                                         Real (&ar)[R], Real (&ai)[R]) {
   using R2 = typename Real2Of<Real>::T;
   constexpr int KE = __builtin_popcount(RM);
   constexpr int D = 1 << KE;
-  if ((xt & op.tctl_mask) != op.tctl_val) return;
   uint32_t jt = tc;
-  for (int b = 0; b < op.n_tb; ++b) jt |= ((xt >> op.tb_pos[b]) & 1u) << op.tb_jbit[b];
+  const int thr_off = op.thr_off;
+  if (thr_off >= 0) {  // host table: block bits on thread positions; 0xff = controls inactive
+    const uint32_t v = blob[thr_off + tid];
+    if (v == 0xffu) return;
+    jt |= v;
+  }
+  // the op's register-bit fields, once (the sub-group loop below is unrolled)
+  constexpr int kRegBits = __builtin_ctz(R);
+  uint32_t dep[kRegBits > 0 ? kRegBits : 1];
+#pragma unroll
+  for (int k = 0; k < kRegBits; ++k) dep[k] = op.dep[k];
+  const uint32_t ictl_mask = op.ictl_mask, ictl_val = op.ictl_val;
   const unsigned char* blocks = blob + op.aux_off;
   constexpr int kSrcBytes = (4 * D + 15) & ~15;
   constexpr int kBlockBytes = PERM ? kSrcBytes + D * static_cast<int>(sizeof(R2)) : (D * D + 1) * static_cast<int>(sizeof(R2));
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     if (s & RM) continue;  // compile time
-    if ((static_cast<uint32_t>(s) & op.ictl_mask) != op.ictl_val) continue;
+    if ((static_cast<uint32_t>(s) & ictl_mask) != ictl_val) continue;
     uint32_t jb = jt;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if ((R >> k) > 1 && ((s >> k) & 1)) jb |= op.dep[k];
+    for (int k = 0; k < kRegBits; ++k)
+      if ((s >> k) & 1) jb |= dep[k];
     const unsigned char* blk = blocks + jb * kBlockBytes;
     Real vr[D], vi[D];
 #pragma unroll
@@ -355,16 +365,16 @@ __device__ __forceinline__ void reg_gen(const PassOp& op, const unsigned char* b
 
 // rmask: mixed bits among the r register bits (at most 3 of them)
 template <typename Real, int R, bool PERM, int RM = 1>
-__device__ __forceinline__ void reg_gen_dispatch(const PassOp& op, const unsigned char* blob, uint32_t tc, uint32_t xt,
+__device__ __forceinline__ void reg_gen_dispatch(const PassOp& op, const unsigned char* blob, uint32_t tc, int tid,
                                                  Real (&ar)[R], Real (&ai)[R]) {
   if constexpr (RM < R) {
     if constexpr (__builtin_popcount(RM) <= 3) {
       if (op.rmask == RM) {
-        reg_gen<Real, R, RM, PERM>(op, blob, tc, xt, ar, ai);
+        reg_gen<Real, R, RM, PERM>(op, blob, tc, tid, ar, ai);
         return;
       }
     }
-    reg_gen_dispatch<Real, R, PERM, RM + 1>(op, blob, tc, xt, ar, ai);
+    reg_gen_dispatch<Real, R, PERM, RM + 1>(op, blob, tc, tid, ar, ai);
   }
 }
 
@@ -723,8 +733,8 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
       } else if (kind == kPassRGen || kind == kPassRPerm) {
         const uint32_t tc = tcs[o];
         if (!(tc >> 31)) {
-          if (kind == kPassRPerm) reg_gen_dispatch<Real, R, true>(op, blob, tc, xt, ar, ai);
-          else reg_gen_dispatch<Real, R, false>(op, blob, tc, xt, ar, ai);
+          if (kind == kPassRPerm) reg_gen_dispatch<Real, R, true>(op, blob, tc, tid, ar, ai);
+          else reg_gen_dispatch<Real, R, false>(op, blob, tc, tid, ar, ai);
         }
         ++o;
       } else {  // SGen / SPerm: through shared memory

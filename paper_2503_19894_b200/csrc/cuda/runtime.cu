@@ -843,6 +843,22 @@ tsg::PassOp build_reg_op(const LaunchStructure& ls, const PassGeom& g, std::vect
       op.tb_jbit[op.n_tb++] = static_cast<uint8_t>(i);
     }
   }
+  // per-thread table: this thread's block bits on thread positions, 0xff when
+  // its controls on thread positions are inactive (one lookup per op and tile
+  // instead of a loop over tb_pos)
+  op.thr_off = -1;
+  if (op.n_tb > 0 || op.tctl_mask != 0) {
+    pad16(data);
+    op.thr_off = static_cast<int32_t>(data.size());
+    for (uint32_t t = 0; t < static_cast<uint32_t>(tsg::kPassThreads); ++t) {
+      uint32_t x = 0;
+      for (size_t b = 0; b < g.tpos.size(); ++b) x |= ((t >> b) & 1u) << g.tpos[b];
+      uint32_t v = 0;
+      for (int b = 0; b < op.n_tb; ++b) v |= ((x >> op.tb_pos[b]) & 1u) << op.tb_jbit[b];
+      if ((x & op.tctl_mask) != op.tctl_val) v = 0xffu;
+      data.push_back(static_cast<unsigned char>(v));
+    }
+  }
   pad16(data);
   op.data_off = static_cast<int32_t>(data.size());
   op.aux_off = op.data_off;
@@ -1099,6 +1115,8 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
     }
     op.data_off += static_cast<int32_t>(data_base);
     if (op.kind != tsg::kPassDiagI && op.kind != tsg::kPassDMember) op.aux_off += static_cast<int32_t>(data_base);
+    if ((op.kind == tsg::kPassRGen || op.kind == tsg::kPassRPerm) && op.thr_off >= 0)
+      op.thr_off += static_cast<int32_t>(data_base);
   }
   std::vector<unsigned char> blob;
   for (int r = 0; r < (1 << nh); ++r) {
