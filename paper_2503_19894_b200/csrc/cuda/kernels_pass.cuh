@@ -311,6 +311,55 @@ __device__ __forceinline__ void reg_gen(const PassOp& op, const unsigned char* b
   const unsigned char* blocks = blob + op.aux_off;
   constexpr int kSrcBytes = (4 * D + 15) & ~15;
   constexpr int kBlockBytes = PERM ? kSrcBytes + D * static_cast<int>(sizeof(R2)) : (D * D + 1) * static_cast<int>(sizeof(R2));
+  if constexpr (!PERM && R / D > 1) {
+    // every sub-group uses the same block (no block bits on register
+    // positions, no register controls): each matrix entry is read once and
+    // applied to all R / D sub-groups, with each output's FMA sequence (and
+    // so its rounding) unchanged
+    bool uniform = ictl_mask == 0;
+#pragma unroll
+    for (int k = 0; k < kRegBits; ++k) uniform = uniform && (((RM >> k) & 1) || dep[k] == 0);
+    if (uniform) {
+      constexpr int NS = R / D;
+      const R2* mat = reinterpret_cast<const R2*>(blocks + jt * kBlockBytes);
+      Real vr[NS][D], vi[NS][D];
+#pragma unroll
+      for (int q = 0, s = 0; s < R; ++s) {
+        if (s & RM) continue;  // compile time
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          vr[q][j] = ar[s | deposit_c(j, RM)];
+          vi[q][j] = ai[s | deposit_c(j, RM)];
+        }
+        ++q;
+      }
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        Real yr[NS], yi[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) yr[q] = yi[q] = Real(0);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const R2 m = mat[r * D + c];
+#pragma unroll
+          for (int q = 0; q < NS; ++q) {
+            yr[q] = fma(m.x, vr[q][c], yr[q]);  // k_direct's order
+            yi[q] = fma(m.x, vi[q][c], yi[q]);
+            yr[q] = fma(-m.y, vi[q][c], yr[q]);
+            yi[q] = fma(m.y, vr[q][c], yi[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0, s = 0; s < R; ++s) {
+          if (s & RM) continue;
+          ar[s | deposit_c(r, RM)] = yr[q];
+          ai[s | deposit_c(r, RM)] = yi[q];
+          ++q;
+        }
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     if (s & RM) continue;  // compile time
