@@ -255,6 +255,7 @@ struct tsg_program {
     cudaGraphExec_t exec = nullptr;
   };
   std::map<std::pair<tsg_state*, uint64_t>, Graph> graphs;
+  std::map<std::pair<tsg_state*, uint64_t>, int> uses;  // runs per state before a graph is captured
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -1836,6 +1837,16 @@ static cudaGraphExec_t program_graph(tsg_state* st, tsg_program* prog) {
   return it->second.exec;
 }
 
+// Graphs pay off on reuse: the first run of a program on a state launches
+// its kernels directly (no capture / instantiate on a one-shot run), later
+// runs replay a captured graph.
+static bool graph_ready(tsg_state* st, tsg_program* prog, int use_graph) {
+  if (!use_graph) return false;
+  const auto key = std::make_pair(st, st->serial);
+  if (prog->graphs.count(key)) return true;
+  return ++prog->uses[key] > 1;
+}
+
 static void enqueue_program(tsg_state* st, tsg_program* prog, int use_graph) {
   require(st->n == prog->n && st->prec == prog->prec, "program was built for a different state shape");
   use_device(st->ctx);
@@ -1846,16 +1857,17 @@ static void enqueue_program(tsg_state* st, tsg_program* prog, int use_graph) {
 int tsg_program_enqueue(tsg_state* st, tsg_program* prog, int use_graph) {
   TSG_TRY({
     require(st && prog, "null argument");
-    enqueue_program(st, prog, use_graph);
+    enqueue_program(st, prog, graph_ready(st, prog, use_graph));
   })
 }
 
 int tsg_program_run(tsg_state* st, tsg_program* prog, int use_graph, tsg_run_report* report) {
   TSG_TRY({
     require(st && prog, "null argument");
-    if (use_graph) program_graph(st, prog);  // capture before the timed events
+    const bool graph = graph_ready(st, prog, use_graph);
+    if (graph) program_graph(st, prog);  // capture before the timed events
     ck(cudaEventRecord(prog->ev0, st->stream), "event");
-    enqueue_program(st, prog, use_graph);
+    enqueue_program(st, prog, graph);
     ck(cudaEventRecord(prog->ev1, st->stream), "event");
     ck(cudaEventSynchronize(prog->ev1), "run sync");
     float ms = 0.f;
