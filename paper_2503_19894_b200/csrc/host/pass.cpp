@@ -161,12 +161,35 @@ double pass_op_sweeps(const LaunchStructure& ls, const PassConfig& cfg) {
 
 double standalone_sweeps(const LaunchStructure& ls, const PassConfig& cfg) {
   double sweeps = cfg.standalone_sweeps;
-  // complex64 4-5 qubit sub-gates with a target on qubit 0 and a contiguous
-  // low run of targets (e.g. [0, 1, 2, 3]) stay on the FP64-widened DMMA
-  // product, whose lanes lose coalescing there: measured 2.8-3.0 sweeps
-  if (cfg.amp_real_bytes == 4 && ls.ks >= 4 && !ls.sub_targets.empty() && ls.sub_targets[0] == 0 &&
-      ls.sub_targets[1] == 1)
-    sweeps = 2.8;
+  if (cfg.amp_real_bytes == 4 && ls.ks >= 4) {
+    // complex64 4-5 qubit sub-gates run on the INT8 tensor-core kernel, one
+    // group per lane: its cost follows how the lanes' groups spread over the
+    // shared-memory banks -- the 32 lanes take the 5 lowest qubits that are
+    // neither targets nor controls (scripts/umma_bench.py, B200):
+    //   <= 2 lanes per bank 1.1 (ks 5: 1.5) sweeps, 8: 1.7, 16: 2.5
+    // and a low contiguous target run from qubit 0 stays on the FP64-widened
+    // DMMA product: 2.8
+    static const bool old_model = std::getenv("TSG_PASS_C64_FLAT") != nullptr;
+    if (!old_model) {
+      std::vector<int> busy(ls.sub_targets);
+      busy.insert(busy.end(), ls.controls.begin(), ls.controls.end());
+      int lane_pos[5], nl = 0;
+      for (int q = 0; nl < 5; ++q)
+        if (std::find(busy.begin(), busy.end(), q) == busy.end()) lane_pos[nl++] = q;
+      int cnt[32] = {0}, deg = 0;
+      for (int l = 0; l < 32; ++l) {
+        int x = 0;
+        for (int b = 0; b < 5; ++b) x |= ((l >> b) & 1) << lane_pos[b];
+        deg = std::max(deg, ++cnt[x % 32]);
+      }
+      const bool low_run = ls.sub_targets[0] == 0 && ls.sub_targets[1] == 1;
+      if (low_run) sweeps = 2.8;
+      else if (deg >= 16) sweeps = 2.5;
+      else if (deg >= 8) sweeps = 1.7;
+      else if (deg >= 4) sweeps = 1.3;
+      else sweeps = ls.ks >= 5 ? 1.5 : 1.1;
+    }
+  }
   return sweeps * std::ldexp(1.0, -static_cast<int>(ls.controls.size()));
 }
 
