@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-aux", action="store_true", help="skip the auxiliary QAOA-30 complex64 measurement")
     ap.add_argument("--breakdown", action="store_true", help="print the per-kernel-class table to stderr")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded (NCCL) step even on one GPU (0 global qubits: exercises that path)")
@@ -374,6 +375,20 @@ def run_ours(args):
     if not args.no_cpu_baseline and world == 1 and rank == 0:
         cpu = cpu_baseline(fq, fr, n, args.cpu_seconds)
 
+    # auxiliary (not the headline): BASELINE.json config 3, QAOA-30 (p = 4)
+    # complex64 with fusion k <= 5, device seconds (median of 3 after warm-up)
+    aux = None
+    if not args.no_aux and world == 1:
+        qa, sqa = ts.run_fusion(ts.gen_benchmark("qaoa", n, 4, 7), ts.FusionConfig(k_max=args.kmax))
+        pqa = ts.Program(qa, "f32", ctx=ctx)
+        sq32 = ts.Statevector(n, "f32", ctx=ctx).init_basis(0)
+        for _ in range(2):
+            pqa.run(sq32)
+        ts_q = sorted(pqa.run(sq32)["execution_s"] for _ in range(3))
+        aux = {"qaoa30_c64_k5": {"seconds": ts_q[1], "gates": f"{sqa['original_gate_count']}->{sqa['fused_block_count']}",
+                                 "steps": len(pqa.steps())}}
+        del pqa, sq32
+
     out = {
         "metric": "30q circuit sim time (s) + per-gate HBM GB/s vs peak",
         "value": t_step,
@@ -412,6 +427,7 @@ def run_ours(args):
         "clocks": clock_info,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "aux": aux,
     }
     if args.breakdown and rank == 0:
         for k, v in sorted(groups.items(), key=lambda kv: -kv[1]["seconds"]):
