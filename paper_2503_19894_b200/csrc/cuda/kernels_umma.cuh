@@ -363,8 +363,10 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const int n = c + e;
-        // 2^14 acc2 + 2^7 acc3 + acc4, two round-to-nearest steps
-        const float f = fmaf(small_i2f(l2[e]), 16384.0f, fmaf(small_i2f(l3[e]), 128.0f, small_i2f(l4[e])));
+        // 2^14 acc2 + (2^7 acc3 + acc4): the bracket exactly in INT32 (< 2^28),
+        // then two round-to-nearest steps
+        const int t34 = static_cast<int>(l3[e]) * 128 + static_cast<int>(l4[e]);
+        const float f = fmaf(small_i2f(l2[e]), 16384.0f, __int2float_rn(t34));
         const float y = f * (sg * b_scale[n]);
         if constexpr (U::TPG == 1) {
           if (n < D) p.re[tb + p.goff[n]] = y;
