@@ -203,3 +203,17 @@ def test_forced_single_op_pass(prec, mixed, block):
     ore, oim = re0.astype(dt), im0.astype(dt)
     ob.run_circuit(to_oracle(c), ore, oim)
     assert ts.compare_states(sv, (ore.astype(np.float64), oim.astype(np.float64))) <= BAR[prec]
+
+
+def test_c64_low_target_runs_join_passes():
+    """complex64 4-qubit gates on a low target run from qubit 0 would fall back
+    to the FP64-widened DMMA product (~2.8 sweeps): the planner prices them so
+    and puts them into passes (HES-24 c64, k <= 5)."""
+    fused, _ = ts.run_fusion(ts.gen_benchmark("hes", 24, 6, 42), ts.FusionConfig(k_max=5))
+    steps = ts.plan_passes(fused, "f32")
+    in_pass = {g for s in steps if s["is_pass"] for g in s["gates"]}
+    low = [i for i in range(len(fused))
+           if list(fused.gate(i).targets)[:2] == [0, 1] and len(fused.gate(i).targets) >= 4
+           and ts.plan_kernel(fused.gate(i), 24).info()["kernel"] != "diagonal"]
+    assert low, "the case must contain low-run gates"
+    assert all(i in in_pass for i in low), (low, in_pass)
