@@ -157,7 +157,9 @@ int tsg_program_gate_info(const tsg_program* prog, uint64_t i, tsg_plan_info* ou
 /* Launch steps of a program, in order.  A step applies n_gates consecutive
  * (non-identity) gates of the program with ONE kernel: kind 0 a single gate,
  * 1 a diagonal batch, 2 a tile pass (tilesim/pass.hpp: one HBM sweep for the
- * run; high[] are its tile qubits above the contiguous runs). */
+ * run; high[] are its tile qubits above the contiguous runs), 3 a qubit
+ * permutation (a run of SWAP-type gates; one in-place sweep, two when the
+ * composed permutation is not an involution). */
 typedef struct tsg_step_info {
   int kind;
   uint64_t first_gate;
