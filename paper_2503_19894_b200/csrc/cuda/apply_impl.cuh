@@ -16,7 +16,7 @@
 #include "kernels_umma.cuh"
 
 #ifndef TSG_UMMA_DEFAULT_KS
-#define TSG_UMMA_DEFAULT_KS 0x30u  // ks 4, 5
+#define TSG_UMMA_DEFAULT_KS 0x70u  // ks 4, 5, 6
 #endif
 
 namespace tsg {
@@ -278,10 +278,10 @@ bool try_stream(const GateLaunch& g, cudaStream_t s, int num_sms) {
 }
 
 // ------------------------------------------------------------ stream_dmma
-template <typename Real, int KS>
+template <typename Real, int KS, int LOG2G_ = DShape<Real, KS>::LOG2G>
 bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, int* stages, bool simt,
                    bool few_tiles = false) {
-  using S = DShape<Real, KS>;
+  constexpr int kLog2G = LOG2G_;  // groups per tile of the caller's kernel (DShape's by default)
   int tg[24], nt = 0;  // all targets (controls + sub-targets), ascending
   {
     int a = 0, b = 0;
@@ -290,12 +290,12 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
       else tg[nt++] = g.sub_targets[b++];
     }
   }
-  int L = S::LOG2G;
+  int L = kLog2G;
   for (;;) {
     int below = 0;
     for (int i = 0; i < nt; ++i) below += tg[i] < L;
-    if (S::LOG2G + below == L) break;
-    L = S::LOG2G + below;
+    if (kLog2G + below == L) break;
+    L = kLog2G + below;
   }
   // element bit b of the launch's element order (GateLaunch::perm, a qubit
   // permutation) is qubit st[b]; runs follow the same order, so the smem
@@ -319,7 +319,7 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   p.ctrl_lo = static_cast<uint32_t>(g.fixed_or & low_mask);
   p.n_tmask = insertion_masks(high_pos, n_high, tile_bits, p.tmask);
   uint64_t gm[kMaxMasks + 12];
-  p.n_gmask = insertion_masks(low_pos, n_low, S::LOG2G, gm);
+  p.n_gmask = insertion_masks(low_pos, n_low, kLog2G, gm);
   if (p.n_gmask > kMaxMasks || p.n_tmask > kMaxMasks) return false;
   for (int i = 0; i < p.n_gmask; ++i) p.gmask[i] = static_cast<uint32_t>(gm[i]);
   for (int r = 0; r < p.n_runs; ++r) {
@@ -388,7 +388,8 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   // Two CTAs per SM beat deeper pipelines (measured): 3 stages when two CTAs
   // still fit in shared memory, else 2.
   const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(Real);
-  const size_t fixed = (simt ? dmma_m_smem_bytes<Real, KS, true>() : dmma_m_smem_bytes<Real, KS>()) + 128;
+  size_t fixed = 128;  // (6-qubit geometries serve k_stream_umma, which sizes its own shared memory)
+  if constexpr (KS <= 5) fixed += simt ? dmma_m_smem_bytes<Real, KS, true>() : dmma_m_smem_bytes<Real, KS>();
   const size_t per_cta = 110 * 1024;
   *stages = 3 * stage + fixed <= per_cta ? 3 : 2;
   *smem = *stages * stage + fixed;
@@ -483,7 +484,7 @@ inline uint32_t umma_ks_mask() {
     const char* e = std::getenv("TSG_UMMA");
     if (e && std::string(e) == "0") return 0u;
     const char* m = std::getenv("TSG_UMMA_KS");
-    return (m ? static_cast<uint32_t>(std::strtoul(m, nullptr, 0)) : TSG_UMMA_DEFAULT_KS) & 0x30u;
+    return (m ? static_cast<uint32_t>(std::strtoul(m, nullptr, 0)) : TSG_UMMA_DEFAULT_KS) & 0x70u;
   }();
   return mask;
 }
@@ -497,7 +498,7 @@ void launch_umma(const DmmaParams<float, KS>& p, size_t smem, cudaStream_t s, in
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "umma smem");
     configured_smem = smem;
   }
-  const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * 2);
+  const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * U::kCtasPerSm);
   kern<<<static_cast<unsigned>(blocks), U::T + 32, smem, s>>>(p);
   cuda_check(cudaGetLastError(), "k_stream_umma launch");
 }
@@ -515,7 +516,7 @@ bool umma_plan(const GateLaunch& g, DmmaParams<float, KS>& p) {
   size_t dsmem = 0;
   int dstages = 0;
   // geometry without chunked runs (the simt layout): one bulk copy per run
-  if (!dmma_geometry<float, KS>(g, p, &dsmem, &dstages, /*simt=*/true)) return false;
+  if (!dmma_geometry<float, KS, UmmaShape<KS>::LOG2G>(g, p, &dsmem, &dstages, /*simt=*/true)) return false;
   if (p.chunk_log2 != p.L) return false;
   // most words any bank receives from the 32 lanes' first stage read
   auto degree = [&](int chunk_log2, uint32_t chunk_stride) {
@@ -563,6 +564,10 @@ inline bool umma_takes(const GateLaunch& g) {
     DmmaParams<float, 5> p;
     return umma_plan<5>(g, p);
   }
+  if (g.ks == 6) {
+    DmmaParams<float, 6> p;
+    return umma_plan<6>(g, p);
+  }
   return false;
 }
 
@@ -577,6 +582,11 @@ bool try_umma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   // so that a third CTA never lands on an SM (tcgen05.alloc would wait)
   const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(float);
   const size_t fixed = umma_fixed_smem<KS>() + 256;
+  if constexpr (UmmaShape<KS>::kCtasPerSm == 1) {  // one CTA per SM (all of TMEM): > 114 KB keeps it so
+    if (fixed + 2 * stage > 227 * 1024) return false;
+    launch_umma<KS, 2>(p, std::max(fixed + 2 * stage, size_t{120} * 1024), s, num_sms);
+    return true;
+  }
   static const int max_stages = std::getenv("TSG_UMMA_STAGES") ? std::atoi(std::getenv("TSG_UMMA_STAGES")) : 3;
   if (max_stages >= 3 && fixed + 3 * stage <= 113 * 1024) {
     launch_umma<KS, 3>(p, std::max(fixed + 3 * stage, size_t{80} * 1024), s, num_sms);
@@ -658,6 +668,7 @@ bool launch_stream_if(const GateLaunch& g, cudaStream_t s, int num_sms) {
       case 3: return try_dmma<float, 3>(g, s, num_sms);
       case 4: return try_umma<4>(g, s, num_sms) || try_dmma<float, 4>(g, s, num_sms);
       case 5: return try_umma<5>(g, s, num_sms) || try_dmma<float, 5>(g, s, num_sms);
+      case 6: return try_umma<6>(g, s, num_sms);
       default: return false;
     }
   }

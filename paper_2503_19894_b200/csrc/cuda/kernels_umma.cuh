@@ -51,9 +51,12 @@ namespace tsg {
 
 template <int KS>
 struct UmmaShape {
-  static_assert(KS == 4 || KS == 5, "k_stream_umma: 4- and 5-qubit sub-gates");
+  static_assert(KS >= 4 && KS <= 6, "k_stream_umma: 4- to 6-qubit sub-gates");
   static constexpr int D = 1 << KS;
-  static constexpr int LOG2G = 12 - KS;  // 4096-amplitude tiles (DShape<float, KS>)
+  // 4096-amplitude tiles (DShape<float, KS>); 8192 for 6 qubits so that one
+  // 128-group M block fills a tile
+  static constexpr int AMPS_LOG2 = KS == 6 ? 13 : 12;
+  static constexpr int LOG2G = AMPS_LOG2 - KS;
   static constexpr int G = 1 << LOG2G;   // groups per tile
   static constexpr int T = 256;          // consumer threads
   static constexpr int TPG = T / G;      // threads per group (KS = 5: two, each half the columns)
@@ -63,7 +66,9 @@ struct UmmaShape {
   static constexpr int MB = G / 128;     // 128-group M blocks
   static constexpr int KSTEPS = K / 32;  // INT8 MMA K = 32
   static constexpr int ACOLS = K / 4;    // TMEM columns of one A slice row
-  static constexpr int kTmemCols = 256;
+  // 6 qubits: 3 x 128 accumulator + 3 x 32 slice columns -> all 512 columns, one CTA per SM
+  static constexpr int kTmemCols = KS == 6 ? 512 : 256;
+  static constexpr int kCtasPerSm = KS == 6 ? 1 : 2;
   static constexpr int BLK = kTmemCols / MB;  // TMEM columns per M block
   static_assert(3 * N + 3 * ACOLS <= BLK, "tensor-memory budget");
   static constexpr uint32_t kBBytes = uint32_t(N) * K;  // one slice of B (INT8)
@@ -151,7 +156,7 @@ __host__ __device__ constexpr size_t umma_fixed_smem() {
 // 112 registers left room for only one CTA per SM (ncu occupancy limit)
 template <int KS>
 constexpr int umma_max_regs() {
-  constexpr int warps = 2 * (UmmaShape<KS>::T / 32 + 1);
+  constexpr int warps = UmmaShape<KS>::kCtasPerSm * (UmmaShape<KS>::T / 32 + 1);
   return (16384 / (((warps + 3) / 4) * 32)) / 8 * 8;
 }
 
@@ -287,13 +292,26 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
     mbar_wait(&full[s], (j / STAGES) & 1u);
     const float* xr = buf + (2 * s) * stage_elems;
     const float* xi = xr + stage_elems;
-    float v[U::K];
+    // this thread's values: the whole row (one thread per group), or its
+    // part -- part 0 the real parts, part 1 the imaginary parts -- with the
+    // row's scale still taken over both
+    float v[U::K / U::TPG];
     float m = 0.0f;
+    if constexpr (U::TPG == 1) {
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      v[c] = xr[p.soff[c] + spos];
-      v[D + c] = xi[p.soff[c] + spos];
-      m = fmaxf(m, fmaxf(fabsf(v[c]), fabsf(v[D + c])));
+      for (int c = 0; c < D; ++c) {
+        v[c] = xr[p.soff[c] + spos];
+        v[D + c] = xi[p.soff[c] + spos];
+        m = fmaxf(m, fmaxf(fabsf(v[c]), fabsf(v[D + c])));
+      }
+    } else {
+      static_assert(U::TPG == 2, "two threads per group");
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const float a = xr[p.soff[c] + spos], b = xi[p.soff[c] + spos];
+        v[c] = part ? b : a;
+        m = fmaxf(m, fmaxf(fabsf(a), fabsf(b)));
+      }
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
@@ -309,11 +327,7 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
       for (int q = 0; q < 8; ++q) {
         uint32_t e1[4], e2[4], e3[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float x = v[4 * (cc + q) + e];
-          if constexpr (U::TPG > 1) x = part ? v[kAc * 4 + 4 * (cc + q) + e] : x;
-          slice3(x * inv, e1[e], e2[e], e3[e]);
-        }
+        for (int e = 0; e < 4; ++e) slice3(v[4 * (cc + q) + e] * inv, e1[e], e2[e], e3[e]);
         w1[q] = __byte_perm(__byte_perm(e1[0], e1[1], 0x0040), __byte_perm(e1[2], e1[3], 0x0040), 0x5410);
         w2[q] = __byte_perm(__byte_perm(e2[0], e2[1], 0x0040), __byte_perm(e2[2], e2[3], 0x0040), 0x5410);
         w3[q] = __byte_perm(__byte_perm(e3[0], e3[1], 0x0040), __byte_perm(e3[2], e3[3], 0x0040), 0x5410);
