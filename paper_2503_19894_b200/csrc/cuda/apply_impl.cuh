@@ -534,13 +534,16 @@ bool umma_plan(const GateLaunch& g, DmmaParams<float, KS>& p) {
   bool bit0 = false;
   for (int b = 0; b < g.ks; ++b) bit0 |= g.sub_targets[b] == 0;
   for (int c = 0; c < g.n_ctrl; ++c) bit0 |= g.ctrl[c] == 0;
-  if (bit0 && d0 > 2) return false;
+  // (6 qubits have no DMMA product to fall back to: k_tile is ~3x slower
+  // than even a bank-conflicted tensor-core launch)
+  if (bit0 && d0 > 2 && KS <= 5) return false;
   // Runs whose stage reads would pile 16 or more lanes onto one bank are cut
   // into padded 64-amplitude chunks (more, smaller bulk copies: measured
   // slower below that conflict degree)
   static const bool chunking = !std::getenv("TSG_UMMA_NO_CHUNK");
   const uint32_t cstride = 64 + kRunPadBytes / sizeof(float);
-  if (chunking && p.L > 6 && d0 >= 16 && degree(6, cstride) <= 4) {
+  const int d6 = p.L > 6 ? degree(6, cstride) : d0;
+  if (chunking && p.L > 6 && d0 >= 16 && (d6 <= 4 || (KS == 6 && 2 * d6 <= d0))) {
     uint32_t low_of[1 << KS], run_of[1 << KS];
     for (int j = 0; j < (1 << KS); ++j) {  // each element's run and in-run offset
       run_of[j] = p.soff[j] / p.run_stride;

@@ -41,7 +41,7 @@ def _state(n, seed):
     ([2, 3, 4, 5], "dense"), ([1, 2, 3, 4], "dense"), ([1, 2, 3, 4, 5], "dense"),  # chunked stage (low targets)
     ([0, 7, 11, 15], "dense"), ([0, 6, 9, 12, 14], "dense"),  # bit-0 target, lanes nearly contiguous
     ([6, 7, 8, 9, 10, 11], "dense"), ([2, 5, 7, 9, 12, 15], "dense"), ([3, 4, 5, 6, 7, 8], "perm"),  # 6 qubits
-    ([1, 4, 6, 8, 10, 13, 15], "controlled"),
+    ([1, 4, 6, 8, 10, 13, 15], "controlled"), ([0, 1, 2, 3, 4, 5], "dense"),  # 6 qubits from bit 0 (chunked)
 ])
 def test_umma_gate_matches_numpy(targets, kind):
     n = 16
