@@ -1,4 +1,4 @@
-// k_stream_umma: complex64 sub-gates of 4 and 5 qubits on the 5th-generation
+// k_stream_umma: complex64 sub-gates of 4 to 6 qubits on the 5th-generation
 // tensor cores, in exact integer arithmetic (tcgen05.mma.kind::i8, INT32
 // accumulators in TMEM).
 //
@@ -25,21 +25,22 @@
 // TF32 split, whose FP32 tensor-core accumulation truncates (measured: the
 // norm fell by ~2e-7 per gate), the result carries no bias.
 //
-// Tensor memory per 128-group M block (KS = 4: two blocks, KS = 5: one):
+// Tensor memory per 128-group M block (KS = 4: two blocks, KS = 5, 6: one):
 //   [acc2 | acc3 | acc4] 2D INT32 columns each, then the three A slices of
 //   the block's rows, 2D / 4 columns each (4 INT8 per 32-bit column).
 // 256 consumer threads: thread t owns group g = t mod G = TMEM lane g mod 128
-// of block g / 128 (KS = 5: two threads per group, each half of the row's
-// columns): it reads its group's 2D values from the stage, slices them and
-// writes its own TMEM row (tcgen05.st) -- no shared-memory staging of A.  B's slices sit in
-// shared memory in the canonical K-major no-swizzle layout (core matrices of
-// 8 rows x 16 bytes, rows 16 bytes apart; 8-row groups 128 bytes apart; the
-// next 16 K-bytes N x 16 bytes further).  Thread 0 issues 6 MMAs per K step
-// (K = 32 INT8) and commits to an mbarrier; the threads then read their
-// row's accumulators and store Yr, Yi straight to global memory (lanes own
-// consecutive groups: coalesced rows).  256 TMEM columns and < 113 KB of
-// shared memory per CTA: two CTAs per SM overlap one's MMAs and epilogue with
-// the other's loads.
+// of block g / 128 (KS = 5, 6: two threads per group, the real / imaginary
+// half of the row): it reads its group's values from the stage, slices them
+// and writes its own TMEM row (tcgen05.st) -- no shared-memory staging of A.
+// B's slices sit in shared memory in the canonical K-major no-swizzle layout
+// (core matrices of 8 rows x 16 bytes, rows 16 bytes apart; 8-row groups 128
+// bytes apart; the next 16 K-bytes N x 16 bytes further).  Thread 0 issues 6
+// MMAs per K step (K = 32 INT8) and commits to an mbarrier; the threads then
+// read their row's accumulators and store Yr, Yi straight to global memory
+// (lanes own consecutive groups: coalesced rows).  KS = 4, 5: 256 TMEM
+// columns and < 113 KB of shared memory per CTA, two CTAs per SM overlap
+// one's MMAs and epilogue with the other's loads; KS = 6: 8192-amplitude
+// tiles, all 512 columns, one CTA per SM.
 #pragma once
 
 #include <cmath>
