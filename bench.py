@@ -247,7 +247,7 @@ def run_sharded(args, rank, world, local, dist):
     e2e = None
     if not args.no_e2e:
         times = []
-        for _ in range(max(1, min(args.steps, 2))):
+        for _ in range(max(1, min(args.steps, 3))):  # median of up to 3 end-to-end steps
             dist.barrier()
             t0 = time.perf_counter()
             (fq2, _), (fr2, _), _ = build_circuits(ts, n, args.kmax)
@@ -353,7 +353,7 @@ def run_ours(args):
         for g in fq.gates() + fr.gates():
             h2d += g.matrix.size * 16 + 4 * len(g.targets)
         d2h = 8 + 16 * 64
-        for _ in range(max(1, min(args.steps, 2))):
+        for _ in range(max(1, min(args.steps, 3))):  # median of up to 3 end-to-end steps
             t0 = time.perf_counter()
             (fq2, _), (fr2, _), _ = build_circuits(ts, n, args.kmax)
             p1 = ts.Program(fq2, "f64", ctx=ctx)
