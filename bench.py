@@ -35,7 +35,15 @@ sys.path.insert(0, ROOT)
 
 N_QUBITS = 30
 WORKLOAD = "qft30+rqc30_d20_c128_sizeonly_k5"
+METRIC = "30q circuit sim time (s) + per-gate HBM GB/s vs peak"
 FALLBACK_HBM_GBS = 6650.0
+
+
+def config_block(n, kmax, qft_gates, rqc_gates):
+    """The workload, identical in both arms (the driver compares them)."""
+    return {"workload": WORKLOAD, "n_qubits": n, "precision": "complex128", "fusion": f"size-only k<={kmax}",
+            "qft_gates": qft_gates, "rqc_gates": rqc_gates, "input": "basis state |0x2AAAAAAA>",
+            "l2": f"state {2 ** n * 16 / 2 ** 30:g} GiB >> 126 MB L2; no flush needed"}
 
 
 def parse_args():
@@ -167,6 +175,26 @@ def build_circuits(ts, n, kmax):
     return (fq, sq), (fr, sr), time.perf_counter() - t0
 
 
+def fused_stream_sha16(gate_lists):
+    """sha256 over every fused gate (int32 targets, complex128 row-major matrix)
+    of the step's circuits: both arms print it, so the CPU reference arm is seen
+    to time the same fused gate stream as the GPU arm."""
+    import hashlib
+
+    import numpy as np
+
+    h = hashlib.sha256()
+    for gates in gate_lists:
+        for t, m in gates:
+            h.update(np.asarray(t, dtype=np.int32).tobytes())
+            h.update(np.ascontiguousarray(m, dtype=np.complex128).tobytes())
+    return h.hexdigest()[:16]
+
+
+def product_stream(fused):
+    return [(g.targets, g.matrix) for g in fused.gates()]
+
+
 def breakdown(ts, progs, sv, n):
     """Per-kernel device time from CUDA events around every launch step
     (Program.steps(): single gates, diagonal batches and tile passes)."""
@@ -279,6 +307,37 @@ def run_sharded(args, rank, world, local, dist):
     dist.close()
 
 
+def qft20_vs_oracle(ts, ctx):
+    """BASELINE configs[0]: QFT-20 on |0x5A5A5>, reference fusion
+    k <= 3, GPU device seconds next to the CPU oracle's full run_circuit
+    (all host threads) and the max |dpsi| between the two."""
+    import numpy as np
+
+    from oracle import binding as ob
+
+    n1, x = 20, 0x5A5A5
+    f1, st1 = ts.run_fusion(ts.gen_benchmark("qft", n1), ts.FusionConfig(k_max=3))
+    p1 = ts.Program(f1, "f64", ctx=ctx)
+    s1 = ts.Statevector(n1, "f64", ctx=ctx)
+    secs = []
+    for _ in range(5):
+        s1.init_basis(x)
+        secs.append(p1.run(s1)["execution_s"])
+    s1.init_basis(x)
+    p1.run(s1)
+    o = ob.Circuit(n1)
+    for g in f1.gates():
+        o.add_matrix(g.targets, g.matrix)
+    re = np.zeros(1 << n1)
+    im = np.zeros(1 << n1)
+    re[x] = 1.0
+    threads = os.cpu_count() or 1
+    r = ob.run_circuit(o, re, im, threads=threads, s=1)
+    return {"seconds": sorted(secs)[2], "gates": f"{st1['original_gate_count']}->{st1['fused_block_count']}",
+            "cpu_oracle_seconds": r["planning_s"] + r["execution_s"], "cpu_threads": threads,
+            "maxdiff_vs_cpu_oracle": ts.compare_states(s1, (re, im))}
+
+
 def run_ours(args):
     rank, world, local = dist_env()
     dist = Dist(world)
@@ -369,28 +428,45 @@ def run_ours(args):
             # one_tol=1e-8 lowering of cos(phi)~1 in tiny CP phases perturbs the norm by ~1e-8 (SPEC semantics)
             assert abs(nrm - 1.0) < 1e-6, nrm
         e2e = {"value": dist.max(statistics.median(e2e_times)), "unit": "s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "includes": "generate+fuse+plan+upload+init+run+readback"}
+               "d2h_bytes_per_step": int(d2h), "includes": "generate+fuse+plan+upload+init+run+readback",
+               "readback": "the state's norm (device reduction) and 64 sampled amplitudes, not the 16 GiB state"}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1 and rank == 0:
-        cpu = cpu_baseline(fq, fr, n, args.cpu_seconds)
+        cpu = cpu_baseline(n, args.kmax, args.cpu_seconds)
 
-    # auxiliary (not the headline): BASELINE.json config 3, QAOA-30 (p = 4)
-    # complex64 with fusion k <= 5, device seconds (median of 3 after warm-up)
+    # auxiliary (not the headline), device seconds, median of 3 after warm-up:
+    #   BASELINE.json configs[2]: QAOA-30 (p = 4) complex64, fusion k <= 5
+    #   SURVEY §8(d) C2b dense class: ALA-30 (depth 20, seed 42) complex128, k <= 5
+    #   configs[0] / C1: QFT-20 complex128, fusion k <= 3, against the CPU oracle
+    #                    run in full on this host (parity and CPU seconds)
     aux = None
     if not args.no_aux and world == 1:
+        aux = {}
+
+        def dev_seconds(prog, state):
+            for _ in range(2):
+                prog.run(state)
+            return sorted(prog.run(state)["execution_s"] for _ in range(3))[1]
+
         qa, sqa = ts.run_fusion(ts.gen_benchmark("qaoa", n, 4, 7), ts.FusionConfig(k_max=args.kmax))
         pqa = ts.Program(qa, "f32", ctx=ctx)
         sq32 = ts.Statevector(n, "f32", ctx=ctx).init_basis(0)
-        for _ in range(2):
-            pqa.run(sq32)
-        ts_q = sorted(pqa.run(sq32)["execution_s"] for _ in range(3))
-        aux = {"qaoa30_c64_k5": {"seconds": ts_q[1], "gates": f"{sqa['original_gate_count']}->{sqa['fused_block_count']}",
-                                 "steps": len(pqa.steps())}}
+        aux["qaoa30_c64_k5"] = {"seconds": dev_seconds(pqa, sq32),
+                                "gates": f"{sqa['original_gate_count']}->{sqa['fused_block_count']}",
+                                "steps": len(pqa.steps())}
         del pqa, sq32
+        al, sal = ts.run_fusion(ts.gen_benchmark("ala", n, 20, 42), ts.FusionConfig(k_max=args.kmax))
+        pal = ts.Program(al, "f64", ctx=ctx)
+        sv.init_random(1)
+        aux["ala30_c128_k5"] = {"seconds": dev_seconds(pal, sv),
+                                "gates": f"{sal['original_gate_count']}->{sal['fused_block_count']}",
+                                "steps": len(pal.steps())}
+        del pal
+        aux["qft20_c128_k3"] = qft20_vs_oracle(ts, ctx)
 
     out = {
-        "metric": "30q circuit sim time (s) + per-gate HBM GB/s vs peak",
+        "metric": METRIC,
         "value": t_step,
         "unit": "s",
         "n_gpus": world,
@@ -402,12 +478,12 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (generated QFT-30 / RQC-30 circuits, basis-state input)",
-        "config": {"workload": WORKLOAD, "n_qubits": n, "precision": "complex128", "fusion": f"size-only k<={args.kmax}",
-                   "qft_gates": f"{sq['original_gate_count']}->{sq['fused_block_count']}",
-                   "rqc_gates": f"{sr['original_gate_count']}->{sr['fused_block_count']}",
-                   "l2": "state 16 GiB >> 126 MB L2; no flush needed", "parallelism": f"replicas x{world}",
-                   "front_end_s": front_s, "per_circuit_s": {"qft30": pq.run(sv)["execution_s"],
-                                                             "rqc30": pr.run(sv)["execution_s"]}},
+        "config": config_block(n, args.kmax, f"{sq['original_gate_count']}->{sq['fused_block_count']}",
+                               f"{sr['original_gate_count']}->{sr['fused_block_count']}"),
+        "parallelism": f"replicas x{world}",
+        "fused_stream_sha16": fused_stream_sha16([product_stream(fq), product_stream(fr)]),
+        "front_end_s": front_s,
+        "per_circuit_s": {"qft30": pq.run(sv)["execution_s"], "rqc30": pr.run(sv)["execution_s"]},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": dom_name, "peak_source": peak_kind,
@@ -440,33 +516,87 @@ def run_ours(args):
 
 
 # ----------------------------------------------------------- CPU oracle leg
-def _cpu_sample(circuits, n, budget_s, threads):
-    """Time the oracle's run_circuit (SPEC apply_kernel, all threads) gate by
-    gate on a 2^n host state until the budget is spent; extrapolate per step."""
-    import numpy as np
-
+# The reference ships no runnable simulator, so its CPU path is
+# the oracle's SPEC-faithful run_circuit (specialised apply_kernel, all host
+# threads; oracle/oracle.cpp).  Circuits are generated AND fused by the oracle
+# itself (no product code on this leg); the fused stream's hash is printed so
+# it can be matched against the GPU arm's.  A full 30-qubit step takes ~5 min
+# on 16 cores, so each timed step runs EVERY fused gate over one stratum
+# (1/S of its group range, a different stratum per step) and scales by S;
+# profiles/r02/cpu_full_validate.json checks that estimate against a full run.
+def oracle_circuits(n, kmax):
     from oracle import binding as ob
 
-    re = np.zeros(1 << n)
-    im = np.zeros(1 << n)
-    re[0] = 1.0
-    total = 0.0
-    detail = []
-    per_circ_budget = budget_s / len(circuits)
-    for fused in circuits:
-        o = ob.Circuit(n)
-        for g in fused.gates():
-            o.add_matrix(g.targets, g.matrix)
-        G = len(o)
-        spent, done = 0.0, 0
-        while done < G and spent < per_circ_budget:
-            t = ob.run_circuit(o, re, im, threads=threads, s=1, g_begin=done, g_end=done + 1)
-            spent += t["planning_s"] + t["execution_s"]
-            done += 1
-        est = spent / done * G
-        total += est
-        detail.append({"gates_timed": done, "gates_total": G, "seconds_timed": spent, "seconds_est": est})
-    return total, detail
+    out = []
+    for kind, depth, seed in (("qft", 1, 0), ("rqc", 20, 42)):
+        fused, stats = ob.run_fusion(ob.gen_benchmark(kind, n, depth, seed), mode="size", k_max=kmax)
+        out.append((kind, fused, stats))
+    return out
+
+
+class CpuStep:
+    """One bounded CPU sample of the step: every fused gate of QFT-n and RQC-n
+    over stratum i of S of its group range, on a resident 2^n host state."""
+
+    def __init__(self, n, kmax, threads):
+        import numpy as np
+
+        from oracle import binding as ob
+
+        self.ob, self.n, self.threads = ob, n, threads
+        self.circs = oracle_circuits(n, kmax)
+        self.sha16 = fused_stream_sha16([[(t, m) for t, m, *_ in c.gates()] for _, c, _ in self.circs])
+        self.gates_total = sum(len(c) for _, c, _ in self.circs)
+        self.re = np.zeros(1 << n)
+        self.im = np.zeros(1 << n)
+        self.re.fill(0.0)  # first-touch the pages outside the timed region
+        self.im.fill(0.0)
+        self.re[0x2AAAAAAA & ((1 << n) - 1)] = 1.0
+        self.slices = 1
+        self.next = 0
+
+    def run(self):
+        """Returns (seconds measured, seconds scaled to the whole step, gates timed)."""
+        t = 0.0
+        gates = 0
+        for _, c, _ in self.circs:
+            r = self.ob.run_circuit_slice(c, self.re, self.im, self.next, self.slices, threads=self.threads, s=1)
+            t += r["planning_s"] + r["execution_s"]
+            gates += len(c)
+        self.next += 1
+        return t, t * self.slices, gates
+
+    def calibrate(self, step_budget_s):
+        """Pick S (a power of two) so one sampled step takes about step_budget_s."""
+        self.slices = 1024
+        t, full, _ = self.run()
+        s = 1
+        while s < 4096 and full / s > step_budget_s:
+            s *= 2
+        self.slices = s
+        self.next = 0
+        return full
+
+    def describe(self, budget_s):
+        return (f"oracle run_circuit (SPEC apply_kernel, s=1, {self.threads} threads), circuits generated and fused "
+                f"by the oracle; per step every one of the {self.gates_total} fused gates over 1/{self.slices} of "
+                f"its group range (a different stratum each step), scaled x{self.slices}; step budget "
+                f"{budget_s:.1f}s")
+
+
+def cpu_baseline(n, kmax, budget_s, samples=2):
+    threads = os.cpu_count() or 1
+    if _host_mem_gb() < 2.5 * (2 ** n * 16) / 1e9:
+        return {"value": None, "unit": "s", "cores": threads, "kind": "port",
+                "sample": f"skipped: host RAM below 2.5x the 2^{n} complex128 state"}
+    cs = CpuStep(n, kmax, threads)
+    cs.calibrate(budget_s / samples)
+    vals = [cs.run() for _ in range(samples)]
+    return {"value": statistics.median(v[1] for v in vals), "unit": "s", "cores": threads, "kind": "port",
+            "sample": cs.describe(budget_s / samples), "fused_stream_sha16": cs.sha16,
+            "detail": {"gates_timed": vals[-1][2], "gates_total": cs.gates_total,
+                       "sample_fraction_per_step": 1.0 / cs.slices, "steps": samples,
+                       "seconds_measured": [v[0] for v in vals]}}
 
 
 def _host_mem_gb():
@@ -480,57 +610,59 @@ def _host_mem_gb():
     return 0.0
 
 
-def cpu_baseline(fq, fr, n, budget_s):
-    threads = os.cpu_count() or 1
-    n_cpu = n
-    scale = 1.0
-    if _host_mem_gb() < 2.5 * (2 ** n * 16) / 1e9:
-        n_cpu = n - 2
-        scale = 4.0
-    if n_cpu != n:
-        import paper_2503_19894_b200 as ts
-        (fq, _), (fr, _), _ = build_circuits(ts, n_cpu, 5)
-    est, detail = _cpu_sample([fq, fr], n_cpu, budget_s, threads)
-    return {"value": est * scale, "unit": "s", "cores": threads, "kind": "port",
-            "sample": f"oracle run_circuit (SPEC apply_kernel, s=1, {threads} threads) on the first gates of the "
-                      f"fused QFT/RQC circuits at n={n_cpu} within {budget_s:.0f}s, extrapolated linearly in gate "
-                      f"count" + (" and x4 to n=30" if scale != 1.0 else ""),
-            "detail": detail}
-
-
 def run_reference(args):
+    """--impl reference: the CPU path (oracle port of SPEC's run_circuit) on all
+    host cores, same metric/config as our arm; rank 0 only under torchrun."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import paper_2503_19894_b200 as ts  # host-only circuit generation + fusion (no GPU use)
-
     n = args.n
-    (fq, _), (fr, _), _ = build_circuits(ts, n, args.kmax)
-    budget = max(4.0, min(args.cpu_seconds, 60.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        _cpu_sample([fq, fr], n, budget / 2, os.cpu_count() or 1)
-    vals = []
-    detail = None
-    for _ in range(args.steps):
-        v, detail = _cpu_sample([fq, fr], n, budget, os.cpu_count() or 1)
-        vals.append(v)
-    v = statistics.median(vals)
     threads = os.cpu_count() or 1
+    cs = CpuStep(n, args.kmax, threads)
+    # the whole --steps K --warmup W run in about 3 minutes
+    budget = max(2.0, min(args.cpu_seconds, 180.0 / max(1, args.steps + args.warmup)))
+    cs.calibrate(budget)
+    for _ in range(args.warmup):
+        cs.run()
+    vals = [cs.run() for _ in range(args.steps)]
+    v = statistics.median(x[1] for x in vals)
+    stats = {kind: f"{st['original_gate_count']}->{st['fused_block_count']}" for kind, _, st in cs.circs}
     print(json.dumps({
-        "impl": "reference", "metric": "30q circuit sim time (s) + per-gate HBM GB/s vs peak", "value": v,
+        "impl": "reference", "metric": METRIC, "value": v,
         "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (generated QFT-30 / RQC-30 circuits)",
-        "config": {"workload": WORKLOAD, "n_qubits": n, "precision": "complex128", "fusion": f"size-only k<={args.kmax}"},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "port",
-                         "sample": f"per step: oracle run_circuit on the first gates of each fused circuit within "
-                                   f"{budget:.1f}s, extrapolated linearly in gate count", "detail": detail},
+        "data": "synthetic (generated QFT-30 / RQC-30 circuits, basis-state input)",
+        "config": config_block(n, args.kmax, stats["qft"], stats["rqc"]),
+        "fused_stream_sha16": cs.sha16,
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "port", "sample": cs.describe(budget),
+                         "detail": {"gates_timed": vals[-1][2], "gates_total": cs.gates_total,
+                                    "sample_fraction_per_step": 1.0 / cs.slices,
+                                    "seconds_measured_median": statistics.median(x[0] for x in vals)}},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
+def relaunch_under_torchrun(args):
+    """--gpus N without a torchrun environment: spawn the N ranks ourselves
+    (one process per GPU, rendezvous on 127.0.0.1) and pass through rank 0's
+    output; returns the exit code."""
+    import socket
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", 0))
+    if world == 0 and args.gpus > 1:
+        raise SystemExit(relaunch_under_torchrun(args))
+    if world and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one process per GPU")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -69,6 +69,9 @@ int tsg_state_init_basis(tsg_state* st, uint64_t index);
 /* deterministic pseudo-random normalized state (DESIGN.md §5 hash) */
 int tsg_state_init_random(tsg_state* st, uint64_t seed);
 int tsg_state_upload(tsg_state* st, const double* re, const double* im);
+/* amplitudes [begin, begin + count) from host fp64 arrays (checkpoint chunks,
+ * single-amplitude edits in tests) */
+int tsg_state_upload_range(tsg_state* st, uint64_t begin, uint64_t count, const double* re, const double* im);
 int tsg_state_download(tsg_state* st, double* re, double* im);
 int tsg_state_download_range(tsg_state* st, uint64_t begin, uint64_t count, double* re, double* im);
 int tsg_state_copy(tsg_state* dst, const tsg_state* src);

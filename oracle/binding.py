@@ -65,6 +65,8 @@ def _load():
     lib.orc_reference_apply.argtypes = [C.c_int, C.c_int, _ip, _dp, _vp, _vp, C.c_int]
     lib.orc_run_circuit.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                                     C.c_int, _dp]
+    lib.orc_run_circuit_slice.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, _u64,
+                                          _u64, _dp]
     lib.orc_reference_run.argtypes = [_vp, _vp, _vp, C.c_int]
     lib.orc_norm.argtypes = [_vp, _vp, _u64, C.c_int]
     lib.orc_norm.restype = C.c_double
@@ -263,6 +265,15 @@ def run_circuit(c: Circuit, re, im, threads=1, s=0, zt=1e-8, ot=1e-8, g_begin=0,
     times = np.zeros(2)
     _check(LIB.orc_run_circuit(c.h, re.ctypes.data, im.ctypes.data, _prec(re), threads, s, zt, ot, g_begin, g_end,
                                times.ctypes.data_as(_dp)))
+    return {"planning_s": float(times[0]), "execution_s": float(times[1])}
+
+
+def run_circuit_slice(c: Circuit, re, im, slice_: int, n_slices: int, threads=1, s=0, zt=1e-8, ot=1e-8):
+    """Every gate of `c` over stratum `slice_` of `n_slices` equal parts of its
+    group range (a bounded, stratified sample of run_circuit's work)."""
+    times = np.zeros(2)
+    _check(LIB.orc_run_circuit_slice(c.h, re.ctypes.data, im.ctypes.data, _prec(re), threads, s, zt, ot, slice_,
+                                     n_slices, times.ctypes.data_as(_dp)))
     return {"planning_s": float(times[0]), "execution_s": float(times[1])}
 
 

@@ -1080,21 +1080,49 @@ static void reference_apply(const Gate& g, int n, R* re, R* im) {
 // ------------------------------------------------------------------- sim ---
 // run_circuit: plan each gate, split [0, 2^(n-k-s)) into
 // `threads` contiguous chunks (remainder to the last), barrier per gate.
+// The group range [lo, hi) of one gate (the whole [0, T) in run_circuit;
+// one stratum of it in the bench's bounded CPU sample) split over threads.
 template <typename R>
-static void apply_threads(const Plan& p, R* re, R* im, const Mat* over, int threads) {
-  uint64_t T = 1ULL << (p.n - p.k - p.s);
+static void apply_threads(const Plan& p, R* re, R* im, const Mat* over, int threads, uint64_t lo, uint64_t hi) {
   if (threads <= 1) {
-    apply_range<R>(p, re, im, over, 0, T);
+    apply_range<R>(p, re, im, over, lo, hi);
     return;
   }
-  uint64_t chunk = T / (uint64_t)threads;
+  uint64_t chunk = (hi - lo) / (uint64_t)threads;
   std::vector<std::thread> pool;
   for (int i = 0; i < threads; ++i) {
-    uint64_t b = chunk * (uint64_t)i;
-    uint64_t e = (i + 1 == threads) ? T : chunk * (uint64_t)(i + 1);
+    uint64_t b = lo + chunk * (uint64_t)i;
+    uint64_t e = (i + 1 == threads) ? hi : lo + chunk * (uint64_t)(i + 1);
     if (b < e) pool.emplace_back([&, b, e] { apply_range<R>(p, re, im, over, b, e); });
   }
   for (auto& th : pool) th.join();
+}
+
+template <typename R>
+static void apply_threads(const Plan& p, R* re, R* im, const Mat* over, int threads) {
+  apply_threads<R>(p, re, im, over, threads, 0, 1ULL << (p.n - p.k - p.s));
+}
+
+// Every gate of the circuit over stratum `slice` of `n_slices` equal parts of
+// its group range: the same per-gate work pattern as run_circuit on a 1/n_slices
+// sample of every gate (bench.py's bounded CPU baseline; not a simulation).
+template <typename R>
+static void run_circ_slice(const Circ& c, R* re, R* im, int threads, int s, double zt, double ot, uint64_t slice,
+                           uint64_t n_slices, double* t_plan, double* t_exec) {
+  double tp = 0, te = 0;
+  for (const Gate& g : c.g) {
+    auto a = std::chrono::steady_clock::now();
+    Plan p = make_plan(g, c.n, s, zt, ot, false);
+    auto b = std::chrono::steady_clock::now();
+    const uint64_t T = 1ULL << (p.n - p.k - p.s);
+    const uint64_t ns = std::min<uint64_t>(n_slices, T), sl = slice % ns;
+    apply_threads<R>(p, re, im, nullptr, threads, T / ns * sl, sl + 1 == ns ? T : T / ns * (sl + 1));
+    auto e = std::chrono::steady_clock::now();
+    tp += std::chrono::duration<double>(b - a).count();
+    te += std::chrono::duration<double>(e - b).count();
+  }
+  *t_plan = tp;
+  *t_exec = te;
 }
 
 template <typename R>
@@ -1372,6 +1400,17 @@ int orc_run_circuit(void* c, void* re, void* im, int prec, int threads, int s, d
       times[0] = tp;
       times[1] = te;
     }
+  })
+}
+// every gate over stratum `slice` of `n_slices` of its group range
+// (bench.py's bounded CPU sample); times[0]=plan s, times[1]=exec s
+int orc_run_circuit_slice(void* c, void* re, void* im, int prec, int threads, int s, double zt, double ot,
+                          uint64_t slice, uint64_t n_slices, double* times) {
+  GUARD({
+    Circ* C = (Circ*)c;
+    if (n_slices == 0) throw Err(2, "n_slices must be positive");
+    if (prec == 64) run_circ_slice<double>(*C, (double*)re, (double*)im, threads, s, zt, ot, slice, n_slices, &times[0], &times[1]);
+    else run_circ_slice<float>(*C, (float*)re, (float*)im, threads, s, zt, ot, slice, n_slices, &times[0], &times[1]);
   })
 }
 // unfused dense oracle run over a circuit

@@ -124,6 +124,7 @@ _sig("tsg_state_init_zero", [_vp])
 _sig("tsg_state_init_basis", [_vp, _u64])
 _sig("tsg_state_init_random", [_vp, _u64])
 _sig("tsg_state_upload", [_vp, _dp, _dp])
+_sig("tsg_state_upload_range", [_vp, _u64, _u64, _dp, _dp])
 _sig("tsg_state_download", [_vp, _dp, _dp])
 _sig("tsg_state_download_range", [_vp, _u64, _u64, _dp, _dp])
 _sig("tsg_state_copy", [_vp, _vp])
@@ -431,6 +432,15 @@ class Statevector:
         if re.size != 1 << self.n or im.size != 1 << self.n:
             raise ConfigError("host arrays must have 2^n entries")
         _check(_lib.tsg_state_upload(self._h, re.ctypes.data_as(_dp), im.ctypes.data_as(_dp)))
+        return self
+
+    def upload_range(self, begin: int, re: np.ndarray, im: np.ndarray):
+        """Overwrite amplitudes [begin, begin + len(re)) from host arrays."""
+        re = np.ascontiguousarray(re, dtype=np.float64).reshape(-1)
+        im = np.ascontiguousarray(im, dtype=np.float64).reshape(-1)
+        if re.size != im.size:
+            raise ConfigError("re and im must have the same length")
+        _check(_lib.tsg_state_upload_range(self._h, begin, re.size, re.ctypes.data_as(_dp), im.ctypes.data_as(_dp)))
         return self
 
     def download(self, begin: int = 0, count: int | None = None):

@@ -115,6 +115,33 @@ void run_diag(const GateLaunch& g, cudaStream_t s, int num_sms) {
   cuda_check(cudaGetLastError(), "k_diag launch");
 }
 
+template <typename Real>
+void run_diag_wide(const GateLaunch& g, cudaStream_t s, int num_sms) {
+  DiagWideParams<Real> p;
+  std::memset(&p, 0, sizeof p);
+  p.re = static_cast<Real*>(g.re);
+  p.im = static_cast<Real*>(g.im);
+  p.table = static_cast<const double*>(g.dev_mat);
+  if (!p.table) throw std::runtime_error("wide diagonal launched without a device table");
+  p.fixed_or = g.fixed_or;
+  p.n_ctrl = g.n_ctrl;
+  p.ks = g.ks;
+  for (int i = 0; i < g.n_ctrl; ++i) p.ctrl[i] = g.ctrl[i];
+  for (int b = 0; b < g.ks; ++b) p.tq[b] = g.sub_targets[b];
+  p.full_range = g.full_range;
+  if (g.full_range) {
+    p.n_work = uint64_t{1} << (g.n - g.n_ctrl);
+  } else {
+    p.g_begin = g.g_begin;
+    p.n_work = (g.g_end - g.g_begin) << g.ks;
+    p.n_masks = g.n_masks;
+    for (int i = 0; i < g.n_masks; ++i) p.masks[i] = g.masks[i];
+  }
+  if (p.n_work == 0) return;
+  k_diag_wide<Real><<<grid_for(p.n_work, num_sms), 256, 0, s>>>(p);
+  cuda_check(cudaGetLastError(), "k_diag_wide launch");
+}
+
 template <typename Real, int KD>
 void pick_diag(const GateLaunch& g, cudaStream_t s, int num_sms) {
   const int low_ctrl = g.n_ctrl > 0 ? g.ctrl[0] : 64;
@@ -696,6 +723,10 @@ int launch_gate_impl(const GateLaunch& g, cudaStream_t s, int num_sms) {
   constexpr int DM = PrecisionTraits<Real>::kDirectMax;
   int klass = g.klass;
   if (klass == 0) return 0;
+  if (klass == 1 && g.ks > kMaxSub) {
+    run_diag_wide<Real>(g, s, num_sms);
+    return 1;
+  }
   if (launch_stream_if<Real>(g, s, num_sms)) return 1;
   if (klass == 1 && !g.full_range) klass = g.ks <= DM ? 2 : 3;  // sub-range: group-space kernels
   if (klass == 2 && g.ks > DM) klass = 3;
@@ -765,6 +796,7 @@ std::string kernel_name_impl(const GateLaunch& g) {
   const std::string ks = "<ks=" + std::to_string(g.ks);
   int klass = g.klass;
   if (klass == 0) return "none";
+  if (klass == 1 && g.ks > kMaxSub) return "k_diag_wide" + ks + ">";
   if ((klass == 2 || klass == 3) && sizeof(Real) == 4 && umma_takes(g)) return "k_stream_umma" + ks + ">";
   if (g.full_range && (klass == 2 || klass == 3) && g.ks >= 3 && g.ks <= 5 && g.dev_mat) {
     if (dmma_mode() == 1 && sizeof(Real) == 8) return "k_dmma_direct" + ks + ">";

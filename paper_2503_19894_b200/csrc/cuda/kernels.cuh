@@ -232,6 +232,49 @@ __global__ void __launch_bounds__(256) k_diag(const __grid_constant__ DiagParams
   }
 }
 
+// Diagonal sub-gates wider than k_diag's parameter table (7..12 qubits: a
+// fused QAOA / IQP phase layer under the paper's k_max = 7 preset).  The
+// 2^ks-entry table (fp64 re | im) is read through the read-only cache.  Full
+// range: one thread per active amplitude.  Sub-range [g_begin, g_end) of the
+// s = 0 group space: one thread per (group, entry).
+template <typename Real>
+struct DiagWideParams {
+  Real* re;
+  Real* im;
+  const double* table;  // [2^ks re][2^ks im]
+  uint64_t fixed_or;
+  int n_ctrl, ks;
+  int ctrl[12];  // ascending
+  int tq[12];    // sub-target qubits, ascending
+  bool full_range;
+  uint64_t n_work;   // full range: active amplitudes; sub-range: groups x 2^ks
+  uint64_t g_begin;  // sub-range: first group
+  uint64_t masks[kMaxMasks];
+  int n_masks;
+};
+
+template <typename Real>
+__global__ void __launch_bounds__(256) k_diag_wide(const __grid_constant__ DiagWideParams<Real> p) {
+  const uint64_t D = uint64_t{1} << p.ks;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < p.n_work; w += stride) {
+    uint64_t idx;
+    unsigned j = 0;
+    if (p.full_range) {
+      idx = insert_zero_bits(w, p.ctrl, p.n_ctrl) | p.fixed_or;
+      for (int b = 0; b < p.ks; ++b) j |= static_cast<unsigned>((idx >> p.tq[b]) & 1u) << b;
+    } else {
+      j = static_cast<unsigned>(w & (D - 1));
+      idx = group_base(p.g_begin + (w >> p.ks), p.masks, p.n_masks) | p.fixed_or;
+      for (int b = 0; b < p.ks; ++b) idx |= static_cast<uint64_t>((j >> b) & 1u) << p.tq[b];
+    }
+    const Real dr = static_cast<Real>(__ldg(p.table + j)), di = static_cast<Real>(__ldg(p.table + D + j));
+    const Real r0 = p.re[idx], i0 = p.im[idx];
+    p.re[idx] = fma(dr, r0, -di * i0);
+    p.im[idx] = fma(dr, i0, di * r0);
+  }
+}
+
 // ------------------------------------------------------- diagonal batches
 // One streaming pass applies a run of diagonal gates (DiagBatchLaunch).
 template <typename Real>

@@ -325,6 +325,16 @@ tsg::GateLaunch make_launch(const KernelPlan& p, const LaunchStructure& ls) {
 // (k_tile reads the first two blocks, k_stream_dmma / k_dmma_direct all
 // three), rows and columns in the launch's element order (GateLaunch::perm).
 std::vector<unsigned char> tile_matrix_bytes(const LaunchStructure& ls, const tsg::GateLaunch& g) {
+  if (g.klass == 1 && ls.ks > tsg::kMaxSub) {  // wide diagonal (k_diag_wide): [diag re][diag im], fp64
+    const size_t D = size_t{1} << ls.ks;
+    std::vector<unsigned char> out(2 * D * sizeof(double));
+    double* d = reinterpret_cast<double*>(out.data());
+    for (size_t j = 0; j < D; ++j) {
+      d[j] = ls.sub_re[j * D + j];
+      d[D + j] = ls.sub_im[j * D + j];
+    }
+    return out;
+  }
   const size_t dd = ls.sub_re.size();
   const int D = 1 << ls.ks;
   std::vector<unsigned char> out(3 * dd * sizeof(double));
@@ -1481,25 +1491,35 @@ int tsg_state_init_random(tsg_state* st, uint64_t seed) {
   })
 }
 
-int tsg_state_upload(tsg_state* st, const double* re, const double* im) {
+int tsg_state_upload_range(tsg_state* st, uint64_t begin, uint64_t count, const double* re, const double* im) {
   TSG_TRY({
     require(st && re && im, "null argument");
+    require(begin <= st->size() && count <= st->size() - begin, "upload range outside the state");
     use_device(st->ctx);
     if (st->prec == 64) {
-      ck(cudaMemcpyAsync(st->re, re, st->size() * 8, cudaMemcpyHostToDevice, st->stream), "upload re");
-      ck(cudaMemcpyAsync(st->im, im, st->size() * 8, cudaMemcpyHostToDevice, st->stream), "upload im");
+      ck(cudaMemcpyAsync((double*)st->re + begin, re, count * 8, cudaMemcpyHostToDevice, st->stream), "upload re");
+      ck(cudaMemcpyAsync((double*)st->im + begin, im, count * 8, cudaMemcpyHostToDevice, st->stream), "upload im");
     } else {
-      for (uint64_t b = 0; b < st->size(); b += kStage) {
-        const uint64_t c = std::min(kStage, st->size() - b);
+      for (uint64_t b = 0; b < count; b += kStage) {
+        const uint64_t c = std::min(kStage, count - b);
         ck(cudaMemcpyAsync(st->stage, re + b, c * 8, cudaMemcpyHostToDevice, st->stream), "upload re");
         ck(cudaMemcpyAsync(st->stage + kStage, im + b, c * 8, cudaMemcpyHostToDevice, st->stream), "upload im");
-        k_convert<float, double><<<ew_grid(st->ctx, c), 256, 0, st->stream>>>((float*)st->re + b, st->stage, c);
-        k_convert<float, double><<<ew_grid(st->ctx, c), 256, 0, st->stream>>>((float*)st->im + b, st->stage + kStage, c);
+        k_convert<float, double><<<ew_grid(st->ctx, c), 256, 0, st->stream>>>((float*)st->re + begin + b, st->stage, c);
+        k_convert<float, double><<<ew_grid(st->ctx, c), 256, 0, st->stream>>>((float*)st->im + begin + b,
+                                                                             st->stage + kStage, c);
         ck(cudaGetLastError(), "k_convert");
       }
     }
     ck(cudaStreamSynchronize(st->stream), "upload sync");
   })
+}
+
+int tsg_state_upload(tsg_state* st, const double* re, const double* im) {
+  if (!st) {
+    tsg_detail::set_error("null handle");
+    return TSG_ERR_CONFIG;
+  }
+  return tsg_state_upload_range(st, 0, st->size(), re, im);
 }
 
 int tsg_state_download_range(tsg_state* st, uint64_t begin, uint64_t count, double* re, double* im) {
