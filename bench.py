@@ -229,9 +229,9 @@ def breakdown(ts, progs, sv, n):
 
 def run_sharded(args, rank, world, local, dist):
     """N > 1: the same 30-qubit step sharded over N GPUs by global qubits
-    (tilesim/shard.hpp), NCCL swaps, one process per GPU (strong scaling)."""
-    import numpy as np  # noqa: F401
-
+    (tilesim/shard.hpp), one process per GPU; exchanges are in-place
+    peer-memory kernels over CUDA IPC (NVLink / NVSwitch), pipelined with the
+    local gates after them where the plan allows (strong scaling)."""
     import paper_2503_19894_b200 as ts
 
     if world & (world - 1):
@@ -239,18 +239,16 @@ def run_sharded(args, rank, world, local, dist):
     g = world.bit_length() - 1
     n = args.n
     ctx = ts.Context(local)
-    if rank == 0:
-        uid = ts.DistState.unique_id()
-    else:
-        uid = None
-    if world > 1:
-        import torch.distributed as tdist
-        obj = [uid]
-        tdist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+
+    def bcast_uid():
+        obj = [ts.DistState.unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
     (fq, sq), (fr, sr), front_s = build_circuits(ts, n, args.kmax)
     pq, pr = ts.ShardPlan(fq, g), ts.ShardPlan(fr, g)
-    d = ts.DistState(n, g, rank, uid, "f64", ctx)
+    d = ts.DistState(n, g, rank, bcast_uid(), "f64", ctx)
     d.init_basis(0x2AAAAAAA & ((1 << n) - 1))
     for _ in range(args.warmup):
         d.run(pq)
@@ -270,6 +268,10 @@ def run_sharded(args, rank, world, local, dist):
     dist.barrier()
     t_step = dist.max(t_dev / args.steps)
     x_step = dist.max(xs / args.steps)
+    # compute-only timeline (the same local segments, no exchange): exposed
+    # swap time = step - compute-only
+    dist.barrier()
+    c_step = dist.max(sum(d.run_local_only(p)["execution_s"] for p in (pq, pr)))
     # e2e through the public API: generate + fuse + shard plans + init + run +
     # a host-side result (this rank's squared norm, summed over ranks)
     e2e = None
@@ -289,21 +291,50 @@ def run_sharded(args, rank, world, local, dist):
         h2d = sum(gt.matrix.size * 16 + 4 * len(gt.targets) for gt in fq.gates() + fr.gates())
         e2e = {"value": dist.max(statistics.median(times)), "unit": "s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 8, "includes": "generate+fuse+shard-plan+init+run+norm readback"}
+    d.close()
+    # auxiliary: SURVEY §8(d) C4 (RQC-33 c128) at this GPU count, and C5
+    # (TFIM-36 c64) when 8 GPUs hold it; device seconds, median of 3
+    aux = {}
+    if not args.no_aux:
+        for name, kind, nn, depth, prec, min_world in (("rqc33_c128", "rqc", 33, 20, "f64", 1),
+                                                        ("tfim36_c64", "hes", 36, 20, "f32", 8)):
+            if world < min_world:
+                continue
+            fa, _ = ts.run_fusion(ts.gen_benchmark(kind, nn, depth, 42), ts.FusionConfig(k_max=args.kmax))
+            pa = ts.ShardPlan(fa, g)
+            da = ts.DistState(nn, g, rank, bcast_uid(), prec, ctx)
+            da.init_basis(0)
+            da.run(pa)
+            reps = [da.run(pa) for _ in range(3)]
+            secs = sorted(dist.max(r["execution_s"]) for r in reps)[1]
+            comp = dist.max(da.run_local_only(pa)["execution_s"])
+            ia = pa.info()
+            aux[name] = {"seconds": secs, "compute_only_s": comp, "exposed_exchange_s": max(0.0, secs - comp),
+                         "exchange_s": dist.max(statistics.median(r["exchange_s"] for r in reps)),
+                         "exchanges": ia["exchanges"], "pipelined_exchanges": ia["pipelined_exchanges"],
+                         "bytes_sent_per_rank": reps[0]["exchanged_bytes"]}
+            da.close()
     if rank == 0:
         iq, ir = pq.info(), pr.info()
+        sent = xbytes / max(1, args.steps)
         print(json.dumps({
-            "metric": "30q circuit sim time (s) + per-gate HBM GB/s vs peak", "value": t_step, "unit": "s",
+            "metric": METRIC, "value": t_step, "unit": "s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generated QFT-30 / RQC-30 circuits, basis-state input)",
-            "config": {"workload": WORKLOAD, "n_qubits": n, "precision": "complex128",
-                       "fusion": f"size-only k<={args.kmax}", "parallelism": f"{g} global qubits over {world} GPUs",
-                       "swaps_per_step": iq["swaps"] + ir["swaps"],
-                       "rank_blocks_per_step": iq["rank_blocks"] + ir["rank_blocks"], "front_end_s": front_s},
-            "exchange": {"seconds_per_step": x_step, "bytes_per_rank_per_step": xbytes // max(1, args.steps),
-                         "nvlink_GBps": (xbytes / max(1, args.steps)) / x_step / 1e9 if x_step > 0 else None,
-                         "exposed": "exchanges are not overlapped yet (exposed = seconds_per_step)"},
-            "gpu_launches": launches, "clocks": clock_info, "e2e": e2e, "cpu_baseline": None}))
+            "config": config_block(n, args.kmax, f"{sq['original_gate_count']}->{sq['fused_block_count']}",
+                                   f"{sr['original_gate_count']}->{sr['fused_block_count']}"),
+            "parallelism": f"{g} global qubits over {world} GPUs (one process per GPU, peer-memory exchanges)",
+            "fused_stream_sha16": fused_stream_sha16([product_stream(fq), product_stream(fr)]),
+            "exchange": {"exchanges_per_step": iq["exchanges"] + ir["exchanges"],
+                         "pipelined_per_step": iq["pipelined_exchanges"] + ir["pipelined_exchanges"],
+                         "rank_blocks_per_step": iq["rank_blocks"] + ir["rank_blocks"],
+                         "seconds_per_step": x_step, "bytes_sent_per_rank_per_step": int(sent),
+                         "nvlink_GBps": sent / x_step / 1e9 if x_step > 0 else None,
+                         "nvlink_frac_of_900": sent / x_step / 900e9 if x_step > 0 else None,
+                         "compute_only_s_per_step": c_step, "exposed_s_per_step": max(0.0, t_step - c_step)},
+            "front_end_s": front_s, "gpu_launches": launches, "clocks": clock_info, "e2e": e2e,
+            "cpu_baseline": None, "aux": aux}))
     dist.close()
 
 
@@ -464,6 +495,14 @@ def run_ours(args):
                                 "steps": len(pal.steps())}
         del pal
         aux["qft20_c128_k3"] = qft20_vs_oracle(ts, ctx)
+        # SURVEY §8(d) C4 at one GPU (the 1-GPU point of its 1/2/4/8 curve):
+        # RQC-33 depth 20 complex128, a 128 GiB state
+        f33, s33 = ts.run_fusion(ts.gen_benchmark("rqc", 33, 20, 42), ts.FusionConfig(k_max=args.kmax))
+        p33 = ts.Program(f33, "f64", ctx=ctx)
+        sv33 = ts.Statevector(33, "f64", ctx=ctx).init_basis(0)
+        aux["rqc33_c128_k5"] = {"seconds": dev_seconds(p33, sv33),
+                                "gates": f"{s33['original_gate_count']}->{s33['fused_block_count']}"}
+        del p33, sv33
 
     out = {
         "metric": METRIC,

@@ -11,10 +11,18 @@
 //              RZ, fused ZZ phases, a controlled-U with a global control):
 //              rank r applies the sub-block selected by its own bits -- no
 //              communication (SURVEY.md §8e "exchange-free cases")
-//   Swap       exchange a global position with a local one: ranks r and
-//              r ^ 2^i swap the halves whose local bit differs from rank bit i
-//              (2^(n_local-1) amplitudes each way); the highest free local
-//              positions are chosen so the exchanged halves are contiguous
+//   Swap       exchange global positions with local ones, all pairs of one
+//              gate at once: the bit transpositions (G_i <-> L_i) form an
+//              involution of the physical index, applied in place over peer
+//              memory -- one grouped all-to-all among the ranks that differ
+//              in the G_i bits (each rank keeps 2^-m of its shard)
+//
+// Pipelining: the top `pipeline_bits` local positions T cut a shard into
+// 2^pipeline_bits slabs.  When the swap leaves T alone, the gates right after
+// it that never touch T (ShardOp::pipeline_ops of them) run slab by slab: the
+// exchange of slab c overlaps those gates on slab c - 1; the rest of the
+// segment runs on the whole shard once the exchange is complete.  The planner
+// avoids T when it picks the local half of a swap.
 #pragma once
 
 #include <cstdint>
@@ -31,6 +39,8 @@ struct ShardOp {
   Gate gate;  // physical, sorted targets and matching matrix (Local / RankBlock)
   std::vector<std::pair<int, int>> swaps;  // (global position >= n_local, local position < n_local)
   int source_gate = -1;                    // index in the fused circuit
+  int pipeline_bits = 0;                   // Swap: slabs (2^bits) the exchange and the next gates pipeline over
+  int pipeline_ops = 0;                    // Swap: how many of the following ops run slab by slab
 };
 
 struct ShardPlan {
@@ -38,12 +48,18 @@ struct ShardPlan {
   std::vector<ShardOp> ops;
   std::vector<int> final_pos;  // logical qubit -> physical position after the last op
   uint64_t swap_count = 0;     // single-qubit swaps
+  uint64_t swap_ops = 0;       // exchanges (grouped all-to-alls)
   uint64_t rank_block_count = 0;
+  uint64_t pipelined_swaps = 0;
+  double zero_tol = 1e-8, one_tol = 1e-8;  // classification used by the planner; executors plan with the same
+  int pipeline_bits = 0;                   // T = top pipeline_bits local positions
 };
 
 // zero_tol as in plan_kernel: entries whose two scalars classify Zero count
-// as structural zeros when testing block-diagonality.
-ShardPlan plan_sharded(const Circuit& fused, int n_global, double zero_tol = 1e-8, double one_tol = 1e-8);
+// as structural zeros when testing block-diagonality.  pipeline_bits: see
+// above (0 disables; clamped so a slab keeps >= 2^13 amplitudes).
+ShardPlan plan_sharded(const Circuit& fused, int n_global, double zero_tol = 1e-8, double one_tol = 1e-8,
+                       int pipeline_bits = 2);
 
 // The local sub-gate rank `rank` applies for a RankBlock op.  Returns a gate
 // with k >= 1 local targets, or a 0-qubit "scalar" gate (targets empty, 1x1

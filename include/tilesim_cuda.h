@@ -234,40 +234,61 @@ int tsc_plan_passes(const tsc_circuit* fused, int precision_bits, double zero_to
                     int* step_is_pass, int* step_high, uint64_t* n_steps);
 
 typedef struct tsc_shard_plan tsc_shard_plan;
-int tsc_shard_plan_create(const tsc_circuit* fused, int n_global, double zero_tol, double one_tol,
+/* pipeline_bits: the top local positions that cut a shard into slabs for
+ * exchange / compute overlap (shard.hpp; 0 disables, 2 is the default) */
+int tsc_shard_plan_create(const tsc_circuit* fused, int n_global, double zero_tol, double one_tol, int pipeline_bits,
                           tsc_shard_plan** out);
 int tsc_shard_plan_destroy(tsc_shard_plan* p);
 int tsc_shard_plan_info(const tsc_shard_plan* p, int* n_qubits, int* n_global, uint64_t* n_ops, uint64_t* swaps,
                         uint64_t* rank_blocks);
+/* exchanges (one grouped all-to-all each), how many pipeline, slab bits */
+int tsc_shard_plan_stats(const tsc_shard_plan* p, uint64_t* swap_ops, uint64_t* pipelined_swaps, int* pipeline_bits);
 /* op i: kind, gate (k, sorted physical targets, matrix 2*4^k; k = 0 for swaps),
- * swap pairs (2 ints each, *n_swaps of them), index of the source gate */
+ * swap pairs (2 ints each, *n_swaps of them), index of the source gate,
+ * pipeline bits of a swap and how many following ops run slab by slab */
 int tsc_shard_plan_op(const tsc_shard_plan* p, uint64_t i, int* kind, int* k, int* targets, double* matrix,
-                      int* n_swaps, int* swap_pairs, int* source_gate);
+                      int* n_swaps, int* swap_pairs, int* source_gate, int* pipeline_bits, int* pipeline_ops);
 /* local sub-gate of a rank-block op for `rank` (k may be 0: a scalar) */
 int tsc_shard_rank_subgate(const tsc_shard_plan* p, uint64_t i, uint64_t rank, int* k, int* targets, double* matrix);
 /* logical qubit -> physical position after the last op (n ints) */
 int tsc_shard_final_pos(const tsc_shard_plan* p, int* pos);
 
 /* --------------------------------------------- sharded execution (device) ---
- * Virtual shards: 2^n_global shard buffers on ONE device, swaps as device
- * copies -- the single-GPU emulation of the distributed path.  Host arrays
- * are the full state in logical order (fp64 SoA, 2^n entries). */
+ * Virtual shards: 2^n_global shard buffers on ONE device, exchanges by the
+ * distributed exchange kernel itself -- the single-GPU emulation of the
+ * distributed path.  Host arrays are the full state in logical order (fp64
+ * SoA, 2^n entries). */
 int tsg_vshard_run(tsg_ctx* ctx, const tsc_shard_plan* plan, int precision_bits, const double* re_in,
                    const double* im_in, double* re_out, double* im_out, tsg_run_report* report);
 
-/* One process per GPU over NCCL (dlopen'ed libnccl.so.2).  Rank 0 creates
- * the id, every rank passes the same 128 bytes (e.g. broadcast over
- * torch.distributed), world = 2^n_global. */
+/* One process per GPU of one box, world = 2^n_global.  Rank 0 makes the id
+ * (tsg_dist_unique_id: the name of a shared-memory rendezvous segment),
+ * every rank passes the same 128 bytes (e.g. broadcast over
+ * torch.distributed).  Shards are exported to every peer with CUDA IPC;
+ * an exchange is an in-place peer-memory kernel on a comm stream, ordered
+ * by interprocess events.  Several ranks may share one device (tests). */
 typedef struct tsg_dist tsg_dist;
 int tsg_dist_unique_id(unsigned char id[128]);
 int tsg_dist_create(tsg_ctx* ctx, int n_qubits, int precision_bits, int n_global, int rank, const unsigned char id[128],
                     tsg_dist** out);
-int tsg_dist_destroy(tsg_dist* d);
+int tsg_dist_destroy(tsg_dist* d);  /* collective: every rank calls it */
 int tsg_dist_init_basis(tsg_dist* d, uint64_t logical_index);  /* identity qubit map */
+/* this rank's 2^(n-n_global) amplitudes, physical order (fp64 SoA) */
+int tsg_dist_upload_local(tsg_dist* d, const double* re, const double* im);
+/* collective.  report: execution_s = device seconds on this rank's compute
+ * stream, exchange_s = device seconds of its exchange kernels,
+ * exchanged_bytes = bytes it sent */
 int tsg_dist_run(tsg_dist* d, const tsc_shard_plan* plan, tsg_run_report* report);
+/* the plan's local segments only (no exchange, not collective): the
+ * compute-only timeline exposed swap time is measured against; leaves the
+ * state meaningless */
+int tsg_dist_run_local_only(tsg_dist* d, const tsc_shard_plan* plan, tsg_run_report* report);
 /* this rank's 2^(n-n_global) amplitudes (physical order of the last plan) */
 int tsg_dist_download_local(tsg_dist* d, double* re, double* im);
 int tsg_dist_local_sumsq(tsg_dist* d, double* out);
+/* host-only check of the rendezvous (no device): `iters` rounds of
+ * write-slot / barrier / sum-all-slots; *checksum = sum over rounds */
+int tsg_rendezvous_selftest(const unsigned char id[128], int rank, int world, int iters, uint64_t* checksum);
 
 /* bench_cost_model on the GPU: for k in [1, k_max] and
  * densities {dense, half, quarter}, times the real kernel on a 2^bench_n

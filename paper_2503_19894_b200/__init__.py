@@ -637,10 +637,11 @@ def bench_cost_model(bench_n: int = 28, k_max: int = 6, precision: str = "f64", 
 
 
 # ============================================================== sharding ===
-_sig("tsc_shard_plan_create", [_vp, C.c_int, C.c_double, C.c_double, C.POINTER(_vp)])
+_sig("tsc_shard_plan_create", [_vp, C.c_int, C.c_double, C.c_double, C.c_int, C.POINTER(_vp)])
+_sig("tsc_shard_plan_stats", [_vp, C.POINTER(_u64), C.POINTER(_u64), _ip])
 _sig("tsc_shard_plan_destroy", [_vp])
 _sig("tsc_shard_plan_info", [_vp, _ip, _ip, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)])
-_sig("tsc_shard_plan_op", [_vp, _u64, _ip, _ip, _ip, _dp, _ip, _ip, _ip])
+_sig("tsc_shard_plan_op", [_vp, _u64, _ip, _ip, _ip, _dp, _ip, _ip, _ip, _ip, _ip])
 _sig("tsc_shard_rank_subgate", [_vp, _u64, _u64, _ip, _ip, _dp])
 _sig("tsc_shard_final_pos", [_vp, _ip])
 _sig("tsg_vshard_run", [_vp, _vp, C.c_int, _dp, _dp, _dp, _dp, C.POINTER(RunReport)])
@@ -649,6 +650,9 @@ _sig("tsg_dist_create", [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_
 _sig("tsg_dist_destroy", [_vp])
 _sig("tsg_dist_init_basis", [_vp, _u64])
 _sig("tsg_dist_run", [_vp, _vp, C.POINTER(RunReport)])
+_sig("tsg_dist_run_local_only", [_vp, _vp, C.POINTER(RunReport)])
+_sig("tsg_dist_upload_local", [_vp, _dp, _dp])
+_sig("tsg_rendezvous_selftest", [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(_u64)])
 _sig("tsg_dist_download_local", [_vp, _dp, _dp])
 _sig("tsg_dist_local_sumsq", [_vp, _dp])
 
@@ -658,9 +662,9 @@ SHARD_KINDS = ("local", "rank_block", "swap")
 class ShardPlan:
     """Global-qubit sharding of a fused circuit over 2^n_global ranks (tilesim/shard.hpp)."""
 
-    def __init__(self, fused: Circuit, n_global: int, zero_tol=1e-8, one_tol=1e-8):
+    def __init__(self, fused: Circuit, n_global: int, zero_tol=1e-8, one_tol=1e-8, pipeline_bits: int = 2):
         h = _vp()
-        _check(_lib.tsc_shard_plan_create(fused._h, n_global, zero_tol, one_tol, C.byref(h)))
+        _check(_lib.tsc_shard_plan_create(fused._h, n_global, zero_tol, one_tol, pipeline_bits, C.byref(h)))
         self._h = h.value
 
     def __del__(self):
@@ -672,22 +676,26 @@ class ShardPlan:
         n, g = C.c_int(), C.c_int()
         ops, sw, rb = _u64(), _u64(), _u64()
         _check(_lib.tsc_shard_plan_info(self._h, C.byref(n), C.byref(g), C.byref(ops), C.byref(sw), C.byref(rb)))
+        xo, pp, pb = _u64(), _u64(), C.c_int()
+        _check(_lib.tsc_shard_plan_stats(self._h, C.byref(xo), C.byref(pp), C.byref(pb)))
         return {"n": n.value, "n_global": g.value, "n_local": n.value - g.value, "ops": ops.value,
-                "swaps": sw.value, "rank_blocks": rb.value}
+                "swaps": sw.value, "rank_blocks": rb.value, "exchanges": xo.value, "pipelined_exchanges": pp.value,
+                "pipeline_bits": pb.value}
 
     def op(self, i: int) -> dict:
-        kind, k, ns, src = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        kind, k, ns, src, pb, po = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
         t = (C.c_int * 12)()
         m = np.zeros(2 * 4 ** 6)
         sp = (C.c_int * 64)()
         _check(_lib.tsc_shard_plan_op(self._h, i, C.byref(kind), C.byref(k), t, m.ctypes.data_as(_dp), C.byref(ns),
-                                      sp, C.byref(src)))
+                                      sp, C.byref(src), C.byref(pb), C.byref(po)))
         gate = None
         if kind.value != 2:
             d = 1 << k.value
             gate = Gate(list(t)[: k.value], m[: 2 * d * d].view(np.complex128).reshape(d, d).copy())
         return {"kind": SHARD_KINDS[kind.value], "gate": gate, "source_gate": src.value,
-                "swaps": [(sp[2 * s], sp[2 * s + 1]) for s in range(ns.value)]}
+                "swaps": [(sp[2 * s], sp[2 * s + 1]) for s in range(ns.value)], "pipeline_bits": pb.value,
+                "pipeline_ops": po.value}
 
     def ops(self):
         return [self.op(i) for i in range(self.info()["ops"])]
@@ -730,7 +738,9 @@ def vshard_run(plan: ShardPlan, re: np.ndarray, im: np.ndarray, precision: str =
 
 
 class DistState:
-    """This rank's shard of a 2^n statevector over 2^n_global processes (NCCL)."""
+    """This rank's shard of a 2^n statevector over 2^n_global processes of one
+    box: shards exported over CUDA IPC, exchanges as in-place peer-memory
+    kernels (tsg_dist_*).  Creation, run and close are collective."""
 
     @staticmethod
     def unique_id() -> bytes:
@@ -748,18 +758,36 @@ class DistState:
         self._h = h.value
         self.n, self.n_global, self.rank = n, n_global, rank
 
-    def __del__(self):
+    def close(self):
+        """Collective teardown (every rank must call it)."""
         if getattr(self, "_h", None) and _lib is not None:
             _lib.tsg_dist_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        self.close()
 
     def init_basis(self, x: int):
         _check(_lib.tsg_dist_init_basis(self._h, x))
         return self
 
+    def upload_local(self, re: np.ndarray, im: np.ndarray):
+        re = np.ascontiguousarray(re, dtype=np.float64)
+        im = np.ascontiguousarray(im, dtype=np.float64)
+        if re.size != 1 << (self.n - self.n_global) or im.size != re.size:
+            raise ConfigError("host arrays must have 2^(n - n_global) entries")
+        _check(_lib.tsg_dist_upload_local(self._h, re.ctypes.data_as(_dp), im.ctypes.data_as(_dp)))
+        return self
+
     def run(self, plan: ShardPlan) -> dict:
         r = RunReport()
         _check(_lib.tsg_dist_run(self._h, plan._h, C.byref(r)))
+        return r.as_dict()
+
+    def run_local_only(self, plan: ShardPlan) -> dict:
+        """The plan's local segments alone (compute-only timeline; state meaningless afterwards)."""
+        r = RunReport()
+        _check(_lib.tsg_dist_run_local_only(self._h, plan._h, C.byref(r)))
         return r.as_dict()
 
     def download_local(self):
@@ -772,3 +800,11 @@ class DistState:
         out = C.c_double()
         _check(_lib.tsg_dist_local_sumsq(self._h, C.byref(out)))
         return out.value
+
+
+def rendezvous_selftest(uid: bytes, rank: int, world: int, iters: int = 100) -> int:
+    """Host-only exercise of the ranks' shared-memory rendezvous (no device)."""
+    buf = (C.c_ubyte * 128)(*uid)
+    out = _u64()
+    _check(_lib.tsg_rendezvous_selftest(buf, rank, world, iters, C.byref(out)))
+    return out.value

@@ -1,8 +1,10 @@
 // C ABI for the host-only part of the surface: circuit IR, generators, text
 // format, fusion pass and cost model (include/tilesim_cuda.h, tsc_*).
+#include <atomic>
 #include <cstring>
 
 #include "handles.hpp"
+#include "rendezvous.hpp"
 #include "tilesim/pass.hpp"
 
 namespace tsg_detail {
@@ -229,11 +231,21 @@ int tsc_plan_passes(const tsc_circuit* fused, int precision_bits, double zero_to
   })
 }
 
-int tsc_shard_plan_create(const tsc_circuit* fused, int n_global, double zero_tol, double one_tol,
+int tsc_shard_plan_create(const tsc_circuit* fused, int n_global, double zero_tol, double one_tol, int pipeline_bits,
                           tsc_shard_plan** out) {
   TSG_TRY({
     require(fused && out, "null argument");
-    *out = new tsc_shard_plan{plan_sharded(fused->c, n_global, zero_tol, one_tol)};
+    static std::atomic<uint64_t> serial{0};
+    *out = new tsc_shard_plan{plan_sharded(fused->c, n_global, zero_tol, one_tol, pipeline_bits), ++serial};
+  })
+}
+
+int tsc_shard_plan_stats(const tsc_shard_plan* p, uint64_t* swap_ops, uint64_t* pipelined_swaps, int* pipeline_bits) {
+  TSG_TRY({
+    require(p != nullptr, "null handle");
+    if (swap_ops) *swap_ops = p->plan.swap_ops;
+    if (pipelined_swaps) *pipelined_swaps = p->plan.pipelined_swaps;
+    if (pipeline_bits) *pipeline_bits = p->plan.pipeline_bits;
   })
 }
 
@@ -266,7 +278,7 @@ static void put_gate(const Gate& g, int* k, int* targets, double* matrix) {
 }
 
 int tsc_shard_plan_op(const tsc_shard_plan* p, uint64_t i, int* kind, int* k, int* targets, double* matrix,
-                      int* n_swaps, int* swap_pairs, int* source_gate) {
+                      int* n_swaps, int* swap_pairs, int* source_gate, int* pipeline_bits, int* pipeline_ops) {
   TSG_TRY({
     require(p != nullptr, "null handle");
     require(i < p->plan.ops.size(), "op index out of range");
@@ -284,6 +296,8 @@ int tsc_shard_plan_op(const tsc_shard_plan* p, uint64_t i, int* kind, int* k, in
         swap_pairs[2 * s + 1] = op.swaps[s].second;
       }
     if (source_gate) *source_gate = op.source_gate;
+    if (pipeline_bits) *pipeline_bits = op.pipeline_bits;
+    if (pipeline_ops) *pipeline_ops = op.pipeline_ops;
   })
 }
 
@@ -301,6 +315,21 @@ int tsc_shard_final_pos(const tsc_shard_plan* p, int* pos) {
   TSG_TRY({
     require(p && pos, "null argument");
     for (int q = 0; q < p->plan.n; ++q) pos[q] = p->plan.final_pos[q];
+  })
+}
+
+int tsg_rendezvous_selftest(const unsigned char id[128], int rank, int world, int iters, uint64_t* checksum) {
+  TSG_TRY({
+    require(id && checksum, "null argument");
+    tilesim::ShmRendezvous rv(id, rank, world, sizeof(uint64_t), 120.0);
+    uint64_t sum = 0;
+    for (int it = 0; it < iters; ++it) {
+      *static_cast<uint64_t*>(rv.slot(rank)) = static_cast<uint64_t>(it) * 1000 + rank;
+      rv.barrier();
+      for (int r = 0; r < world; ++r) sum += *static_cast<uint64_t*>(rv.slot(r));
+      rv.barrier();
+    }
+    *checksum = sum;
   })
 }
 

@@ -16,6 +16,7 @@ struct tsc_circuit {
 
 struct tsc_shard_plan {
   tilesim::ShardPlan plan;
+  uint64_t serial = 0;  // unique per plan: executors key their prepared schedules on it
 };
 
 struct tsc_cost_model {

@@ -28,14 +28,19 @@ uint64_t physical_index(uint64_t x, const std::vector<int>& pos) {
   return p;
 }
 
-ShardPlan plan_sharded(const Circuit& fused, int n_global, double zt, double ot) {
+ShardPlan plan_sharded(const Circuit& fused, int n_global, double zt, double ot, int pipeline_bits) {
   const int n = fused.n_qubits;
   if (n_global < 0 || n_global >= n) throw ConfigError("n_global must be in [0, n)");
   ShardPlan plan;
   plan.n = n;
   plan.n_global = n_global;
   plan.n_local = n - n_global;
+  plan.zero_tol = zt;
+  plan.one_tol = ot;
   const int nl = plan.n_local;
+  if (pipeline_bits < 0) throw ConfigError("pipeline_bits must be >= 0");
+  plan.pipeline_bits = n_global == 0 ? 0 : std::max(0, std::min(pipeline_bits, nl - 13));
+  const int t_lo = nl - plan.pipeline_bits;  // T = [t_lo, nl)
   std::vector<int> pos(n), at(n);  // logical -> physical, physical -> logical
   for (int q = 0; q < n; ++q) pos[q] = at[q] = q;
   // next use of each logical qubit after gate gi (Belady eviction for swaps)
@@ -87,12 +92,16 @@ ShardPlan plan_sharded(const Circuit& fused, int n_global, double zt, double ot)
       if (pos[q] < nl) continue;
       int best = -1;
       size_t best_use = 0;
+      bool best_in_t = true;
       for (int cand = nl - 1; cand >= 0; --cand) {
         if (std::find(used.begin(), used.end(), cand) != used.end()) continue;
         const size_t u = next_use(at[cand], gi);
-        if (best < 0 || u > best_use) {
+        const bool in_t = cand >= t_lo;
+        // outside the pipeline slab bits T first, then furthest next use
+        if (best < 0 || (best_in_t && !in_t) || (in_t == best_in_t && u > best_use)) {
           best = cand;
           best_use = u;
+          best_in_t = in_t;
         }
       }
       if (best < 0) throw ConfigError("no free local qubit to swap with");
@@ -105,6 +114,7 @@ ShardPlan plan_sharded(const Circuit& fused, int n_global, double zt, double ot)
       used.push_back(lp);
     }
     plan.swap_count += sw.swaps.size();
+    ++plan.swap_ops;
     plan.ops.push_back(std::move(sw));
     ShardOp op;
     op.kind = ShardOp::Kind::Local;
@@ -113,6 +123,28 @@ ShardPlan plan_sharded(const Circuit& fused, int n_global, double zt, double ot)
     plan.ops.push_back(std::move(op));
   }
   plan.final_pos = pos;
+  // which exchanges can pipeline with the segment that follows them
+  if (plan.pipeline_bits > 0)
+    for (size_t i = 0; i < plan.ops.size(); ++i) {
+      ShardOp& sw = plan.ops[i];
+      if (sw.kind != ShardOp::Kind::Swap) continue;
+      bool ok = true;
+      for (const auto& pr : sw.swaps) ok = ok && pr.second < t_lo;
+      if (!ok) continue;
+      // the prefix of the following segment whose gates keep off T runs slab by slab
+      int prefix = 0;
+      for (size_t j = i + 1; j < plan.ops.size() && plan.ops[j].kind != ShardOp::Kind::Swap; ++j) {
+        bool off_t = true;
+        for (int t : plan.ops[j].gate.targets) off_t = off_t && (t >= nl || t < t_lo);
+        if (!off_t) break;
+        ++prefix;
+      }
+      if (prefix > 0) {
+        sw.pipeline_bits = plan.pipeline_bits;
+        sw.pipeline_ops = prefix;
+        ++plan.pipelined_swaps;
+      }
+    }
   return plan;
 }
 
