@@ -233,6 +233,12 @@ int tsc_estimate_cost(const tsc_cost_model* cm, int k, uint64_t op_count, int th
 int tsc_plan_passes(const tsc_circuit* fused, int precision_bits, double zero_tol, double one_tol, int* step_of_gate,
                     int* step_is_pass, int* step_high, uint64_t* n_steps);
 
+/* Compile (NVRTC, no device needed) the JIT tile-pass kernels a program of
+ * `fused` would use, into the JIT disk cache (TSG_JIT_CACHE_DIR); *n_passes =
+ * how many passes the program has.  Warms the cache ahead of a run. */
+int tsc_pass_jit_precompile(const tsc_circuit* fused, int precision_bits, double zero_tol, double one_tol,
+                            int* n_passes);
+
 typedef struct tsc_shard_plan tsc_shard_plan;
 /* pipeline_bits: the top local positions that cut a shard into slabs for
  * exchange / compute overlap (shard.hpp; 0 disables, 2 is the default) */

@@ -620,6 +620,18 @@ def plan_passes(fused: Circuit, precision: str = "f64", zero_tol=1e-8, one_tol=1
     return steps
 
 
+_sig("tsc_pass_jit_precompile", [_vp, C.c_int, C.c_double, C.c_double, _ip])
+
+
+def pass_jit_precompile(fused: Circuit, precision: str = "f64", zero_tol=1e-8, one_tol=1e-8) -> int:
+    """NVRTC-compile the JIT tile passes a Program of `fused` would use into the
+    JIT disk cache (host only); returns the program's pass count."""
+    n = C.c_int()
+    _check(_lib.tsc_pass_jit_precompile(fused._h, 64 if precision in ("f64", "c128") else 32, zero_tol, one_tol,
+                                        C.byref(n)))
+    return n.value
+
+
 def run_circuit(c: Circuit, sv: Statevector, zero_tol=1e-8, one_tol=1e-8, use_graph=True) -> dict:
     """run_circuit: plan every gate, apply in order on the device."""
     prec = "f64" if sv.precision_bits == 64 else "f32"

@@ -3,12 +3,18 @@
 // the per-precision launchers in apply_f64.cu / apply_f32.cu.
 #pragma once
 
+#ifndef __CUDACC_RTC__  // NVRTC (pass_jit.cpp) supplies the integer types
 #include <cstdint>
 #include <string>
 
 #include <cuda_runtime.h>
+#endif
 
 namespace tsg {
+
+// constexpr bit helpers usable in templates on both compilers
+__host__ __device__ constexpr int cx_popc(unsigned x) { return x ? int(x & 1u) + cx_popc(x >> 1) : 0; }
+__host__ __device__ constexpr int cx_ctz(unsigned x) { return (x & 1u) || !x ? 0 : 1 + cx_ctz(x >> 1); }
 
 constexpr int kMaxMasks = 13;  // k + 1 startIdx masks, k <= 12
 constexpr int kMaxSub = 6;     // largest non-diagonal sub-gate on the GPU
@@ -80,8 +86,10 @@ struct DiagBatchLaunch {
 int launch_diag_batch_f64(const DiagBatchLaunch& b, cudaStream_t stream, int num_sms);
 int launch_diag_batch_f32(const DiagBatchLaunch& b, cudaStream_t stream, int num_sms);
 
+#ifndef __CUDACC_RTC__
 // Name of the kernel template a launch selects (for reports / profiles).
 std::string kernel_name(const GateLaunch& g, int precision_bits);
+#endif
 
 // ------------------------------------------------------------ tile passes
 // A pass applies a run of fused gates to the state in ONE read + write of
@@ -187,6 +195,7 @@ struct PassLaunch {
   const void* blob = nullptr;  // device
   int blob_bytes = 0;
   int n_ops = 0;
+  const void* jit = nullptr;   // JIT-compiled kernel of this op table (pass_jit.cu), else the interpreter
 };
 int launch_pass_f64(const PassLaunch& p, cudaStream_t stream, int num_sms);
 int launch_pass_f32(const PassLaunch& p, cudaStream_t stream, int num_sms);

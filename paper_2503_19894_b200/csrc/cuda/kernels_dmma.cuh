@@ -32,8 +32,10 @@
 // ks <= 4 they write the results into the stage (in place) for the bulk store.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
 #include <type_traits>
+#endif
 
 #include "kernels_stream.cuh"
 

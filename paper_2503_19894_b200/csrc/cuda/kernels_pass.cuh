@@ -34,12 +34,22 @@
 // amplitude sets.
 #pragma once
 
+#ifndef __CUDACC_RTC__  // NVRTC (pass_jit.cpp) supplies the integer types
 #include <cstdint>
 #include <type_traits>
+#endif
 
 #include "kernels_dmma.cuh"
 
 namespace tsg {
+
+// Loops whose trip counts come from op fields: fully unrolled in a JIT pass
+// (the fields are constants there), left alone in the interpreter.
+#ifdef TSG_JIT
+#define TSG_JIT_UNROLL _Pragma("unroll")
+#else
+#define TSG_JIT_UNROLL
+#endif
 
 template <typename Real>
 struct Real2Of;
@@ -293,7 +303,7 @@ template <typename Real, int R, int RM, bool PERM>
 __device__ __forceinline__ void reg_gen(const PassOp& op, const unsigned char* blob, uint32_t tc, int tid,
                                         Real (&ar)[R], Real (&ai)[R]) {
   using R2 = typename Real2Of<Real>::T;
-  constexpr int KE = __builtin_popcount(RM);
+  constexpr int KE = cx_popc(RM);
   constexpr int D = 1 << KE;
   uint32_t jt = tc;
   const int thr_off = op.thr_off;
@@ -303,7 +313,7 @@ __device__ __forceinline__ void reg_gen(const PassOp& op, const unsigned char* b
     jt |= v;
   }
   // the op's register-bit fields, once (the sub-group loop below is unrolled)
-  constexpr int kRegBits = __builtin_ctz(R);
+  constexpr int kRegBits = cx_ctz(R);
   uint32_t dep[kRegBits > 0 ? kRegBits : 1];
 #pragma unroll
   for (int k = 0; k < kRegBits; ++k) dep[k] = op.dep[k];
@@ -417,7 +427,7 @@ template <typename Real, int R, bool PERM, int RM = 1>
 __device__ __forceinline__ void reg_gen_dispatch(const PassOp& op, const unsigned char* blob, uint32_t tc, int tid,
                                                  Real (&ar)[R], Real (&ai)[R]) {
   if constexpr (RM < R) {
-    if constexpr (__builtin_popcount(RM) <= 3) {
+    if constexpr (cx_popc(RM) <= 3) {
       if (op.rmask == RM) {
         reg_gen<Real, R, RM, PERM>(op, blob, tc, tid, ar, ai);
         return;
@@ -445,7 +455,7 @@ template <typename Real, int R>
 __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const unsigned char* blob, const uint32_t* tcs,
                                              int tid, Real (&ar)[R], Real (&ai)[R], typename Real2Of<Real>::T* gtab) {
   using R2 = typename Real2Of<Real>::T;
-  constexpr int kBits = __builtin_ctz(R);
+  constexpr int kBits = cx_ctz(R);
   const int n_groups = ops[o].ks, nT = ops[o].log2_groups, nX = ops[o].log2_rsplit;
   ++o;
   if (n_groups > 0) {
@@ -455,6 +465,7 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
     // every group in parallel, one short member chain per thread
     static_assert(kPassMaxGEntries <= kPassThreads, "one group entry per thread");
     int og = o;
+    TSG_JIT_UNROLL
     for (int g = 0; g < n_groups; ++g) {
       const PassOp& gh = ops[og];
       const int sbits = gh.ks, m = gh.log2_groups;
@@ -462,6 +473,7 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
       if (e >= 0 && e < (1 << sbits)) {
         // two interleaved partial products halve the dependent multiply chain
         Real fr[2] = {Real(1), Real(1)}, fi[2] = {Real(0), Real(0)};
+        TSG_JIT_UNROLL
         for (int t = 1; t <= m; ++t) {
           const PassOp& mo = ops[og + t];
           const uint32_t tc = tcs[og + t];
@@ -481,6 +493,7 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
     consumer_bar();
     // apply: one entry per group and amplitude
     og = o;
+    TSG_JIT_UNROLL
     for (int g = 0; g < n_groups; ++g) {
       const PassOp& gh = ops[og];
       const uint32_t tv = blob[gh.aux_off + tid];
@@ -504,6 +517,7 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
   // DiagT: one factor per thread (two interleaved partial products)
   Real ftr = Real(1), fti = Real(0), f2r = Real(1), f2i = Real(0);
   int t = 0;
+  TSG_JIT_UNROLL
   for (; t + 1 < nT; t += 2) {
     const PassOp& op0 = ops[o + t];
     const PassOp& op1 = ops[o + t + 1];
@@ -525,6 +539,7 @@ __device__ __forceinline__ int pass_diag_run(const PassOp* ops, int o, const uns
   }
   o += nT;
   // DiagX: amplitude by amplitude, k_diag's update
+  TSG_JIT_UNROLL
   for (int x = 0; x < nX; ++x, ++o) {
     const PassOp& op = ops[o];
     const uint32_t tc = tcs[o];
@@ -645,8 +660,104 @@ __device__ __forceinline__ void smem_to_regs(const Real* xr, const Real* xi, con
   }
 }
 
-template <typename Real, int M, int L, int STAGES>
-__global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant__ PassParams p) {
+// Per-thread interpreter state of one tile: the registers of the current
+// layout, their shared-memory offsets, and what carries across ops.
+template <typename Real, int R>
+struct PassRegs {
+  Real ar[R], ai[R];
+  uint32_t at[R];    // padded shared-memory offsets of the registers (current layout)
+  int vb = 0;        // vector width (log2) of the current layout's register <-> smem moves
+  uint32_t xt = 0;   // tile coordinate of the thread part of the current layout
+  uint32_t irun = 0; // runs with diagonal groups so far (table double-buffering)
+  bool in_smem = true;  // the registers have been stored (shared memory is current)
+};
+
+// One op (or one RUN with its members) of a tile; returns the next op index.
+// The interpreter calls it in a loop over the blob's op table; a JIT-compiled
+// pass (pass_jit.cpp) calls it once per op with `ops` a constexpr table and
+// `o` a literal, so every field folds to a constant.
+template <typename Real, int M, int L>
+__device__ __forceinline__ int pass_step(const PassOp* ops, int o, int n_ops, const unsigned char* blob,
+                                         const uint32_t* tcs, int tid, Real* xr, Real* xi,
+                                         typename Real2Of<Real>::T* fi_tab,
+                                         PassRegs<Real, PassShape<Real, M, L>::kIter>& rg) {
+  using S = PassShape<Real, M, L>;
+  constexpr int R = S::kIter;
+  const PassOp& op = ops[o];
+  const int kind = op.kind;
+  if (kind == kPassLayout) {
+    if (!rg.in_smem) {
+      regs_to_smem<Real, R>(xr, xi, rg.at, rg.ar, rg.ai, rg.vb);
+      consumer_bar();  // the tile is in shared memory in full
+    } else if (o > 0) {
+      consumer_bar();  // after shared-memory ops: their writes are visible
+    }
+    rg.xt = reinterpret_cast<const uint32_t*>(blob + op.aux_off)[tid];  // host-built per-thread coordinate
+    const uint32_t at0 = pass_addr<L, S::kStride>(rg.xt);
+    constexpr int kBits = cx_ctz(R);
+    uint32_t pd[kBits];  // padded offset of each register position (additive over disjoint bits)
+#pragma unroll
+    for (int k = 0; k < kBits; ++k) pd[k] = op.dep[k];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      uint32_t a = at0;
+#pragma unroll
+      for (int k = 0; k < kBits; ++k)
+        if ((i >> k) & 1) a += pd[k];
+      rg.at[i] = a;
+    }
+    rg.vb = op.ks;  // vector width of this layout (host: lowest register positions = lowest tile positions)
+    smem_to_regs<Real, R>(xr, xi, rg.at, rg.ar, rg.ai, rg.vb);
+    rg.in_smem = false;
+    return o + 1;
+  }
+  if (kind == kPassRun) {
+    // group tables alternate buffers run by run (each such run has a barrier)
+    const bool has_groups = op.ks > 0;
+    o = pass_diag_run<Real, R>(ops, o, blob, tcs, tid, rg.ar, rg.ai, fi_tab + (rg.irun & 1) * kPassMaxGEntries);
+    rg.irun += has_groups;
+    return o;
+  }
+  if (kind == kPassRGen || kind == kPassRPerm) {
+    const uint32_t tc = tcs[o];
+    if (!(tc >> 31)) {
+      if (kind == kPassRPerm) reg_gen_dispatch<Real, R, true>(op, blob, tc, tid, rg.ar, rg.ai);
+      else reg_gen_dispatch<Real, R, false>(op, blob, tc, tid, rg.ar, rg.ai);
+    }
+    return o + 1;
+  }
+  // SGen / SPerm: through shared memory
+  if (!rg.in_smem) {
+    regs_to_smem<Real, R>(xr, xi, rg.at, rg.ar, rg.ai, rg.vb);
+    rg.in_smem = true;
+  }
+  consumer_bar();
+  // the skip is tile-uniform, so a row-split op's internal barrier stays uniform
+  const uint32_t tc = tcs[o];
+  if (!(tc >> 31)) pass_gen_dispatch<Real, M, L>(op, blob, tc, xr, xi, tid);
+  ++o;
+  if (o < n_ops && ops[o].kind != kPassSGen && ops[o].kind != kPassSPerm && ops[o].kind != kPassLayout) {
+    consumer_bar();  // back to the registers of the current layout
+    smem_to_regs<Real, R>(xr, xi, rg.at, rg.ar, rg.ai, rg.vb);
+    rg.in_smem = false;
+  }
+  return o;
+}
+
+// Op interpreter over the blob's op table (the generic k_pass).
+struct PassInterp {
+  template <typename Real, int M, int L, typename RG>
+  static __device__ __forceinline__ void run(const PassOp* ops, int n_ops, const unsigned char* blob,
+                                             const uint32_t* tcs, int tid, Real* xr, Real* xi,
+                                             typename Real2Of<Real>::T* fi_tab, RG& rg) {
+    for (int o = 0; o < n_ops;) o = pass_step<Real, M, L>(ops, o, n_ops, blob, tcs, tid, xr, xi, fi_tab, rg);
+  }
+};
+
+// The tile pipeline; EXEC applies the op list to a tile (PassInterp, or a
+// generated straight-line sequence in a JIT-compiled pass).
+template <typename Real, int M, int L, int STAGES, typename EXEC>
+__device__ __forceinline__ void k_pass_body(const PassParams& p) {
   using S = PassShape<Real, M, L>;
   using C = PassCopy<Real, M, L>;
   using R2 = typename Real2Of<Real>::T;
@@ -718,11 +829,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
   for (int s = 0; s < STAGES - 1; ++s) prefetch(s);
 
   constexpr int R = S::kIter;  // amplitudes per thread (register layout)
-  Real ar[R], ai[R];
-  uint32_t at[R];      // padded shared-memory offsets of the registers (current layout)
-  int vb = 0;          // vector width (log2) of the current layout's register <-> smem moves
-  uint32_t xt = 0;     // tile coordinate of the thread part of the current layout
-  uint32_t irun = 0;   // runs with diagonal groups so far (table double-buffering)
+  PassRegs<Real, R> rg;
   uint32_t j = 0;
   for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
     const int s = static_cast<int>(j % STAGES);
@@ -743,67 +850,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
     prefetch(static_cast<int>((j + STAGES - 1) % STAGES));
     Real* xr = buf + (2 * s) * S::kStageElems;
     Real* xi = xr + S::kStageElems;
-    // The op list starts with a LAYOUT op; registers hold the tile from then
-    // on.  `in_smem`: the registers have been stored (shared memory is current).
-    bool in_smem = true;
-    for (int o = 0; o < p.n_ops;) {
-      const PassOp& op = ops[o];
-      const int kind = op.kind;
-      if (kind == kPassLayout) {
-        if (!in_smem) {
-          regs_to_smem<Real, R>(xr, xi, at, ar, ai, vb);
-          consumer_bar();  // the tile is in shared memory in full
-        } else if (o > 0) {
-          consumer_bar();  // after shared-memory ops: their writes are visible
-        }
-        xt = reinterpret_cast<const uint32_t*>(blob + op.aux_off)[tid];  // host-built per-thread coordinate
-        const uint32_t at0 = pass_addr<L, S::kStride>(xt);
-        constexpr int kBits = __builtin_ctz(R);
-        uint32_t pd[kBits];  // padded offset of each register position (additive over disjoint bits)
-#pragma unroll
-        for (int k = 0; k < kBits; ++k) pd[k] = op.dep[k];
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-          uint32_t a = at0;
-#pragma unroll
-          for (int k = 0; k < kBits; ++k)
-            if ((i >> k) & 1) a += pd[k];
-          at[i] = a;
-        }
-        vb = op.ks;  // vector width of this layout (host: lowest register positions = lowest tile positions)
-        smem_to_regs<Real, R>(xr, xi, at, ar, ai, vb);
-        in_smem = false;
-        ++o;
-      } else if (kind == kPassRun) {
-        // group tables alternate buffers run by run (each such run has a barrier)
-        const bool has_groups = op.ks > 0;
-        o = pass_diag_run<Real, R>(ops, o, blob, tcs, tid, ar, ai, fi_tab + (irun & 1) * kPassMaxGEntries);
-        irun += has_groups;
-      } else if (kind == kPassRGen || kind == kPassRPerm) {
-        const uint32_t tc = tcs[o];
-        if (!(tc >> 31)) {
-          if (kind == kPassRPerm) reg_gen_dispatch<Real, R, true>(op, blob, tc, tid, ar, ai);
-          else reg_gen_dispatch<Real, R, false>(op, blob, tc, tid, ar, ai);
-        }
-        ++o;
-      } else {  // SGen / SPerm: through shared memory
-        if (!in_smem) {
-          regs_to_smem<Real, R>(xr, xi, at, ar, ai, vb);
-          in_smem = true;
-        }
-        consumer_bar();
-        // the skip is tile-uniform, so a row-split op's internal barrier stays uniform
-        const uint32_t tc = tcs[o];
-        if (!(tc >> 31)) pass_gen_dispatch<Real, M, L>(op, blob, tc, xr, xi, tid);
-        ++o;
-        if (o < p.n_ops && ops[o].kind != kPassSGen && ops[o].kind != kPassSPerm && ops[o].kind != kPassLayout) {
-          consumer_bar();  // back to the registers of the current layout
-          smem_to_regs<Real, R>(xr, xi, at, ar, ai, vb);
-          in_smem = false;
-        }
-      }
-    }
-    if (!in_smem) regs_to_smem<Real, R>(xr, xi, at, ar, ai, vb);
+    // The op list starts with a LAYOUT op; registers hold the tile from then on.
+    rg.in_smem = true;
+    EXEC::template run<Real, M, L>(ops, p.n_ops, blob, tcs, tid, xr, xi, fi_tab, rg);
+    if (!rg.in_smem) regs_to_smem<Real, R>(xr, xi, rg.at, rg.ar, rg.ai, rg.vb);
     consumer_bar();  // all ops done: write the tile back
     const Real* st = buf + (2 * s) * S::kStageElems;
 #pragma unroll
@@ -811,6 +861,11 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant_
       *reinterpret_cast<uint4*>(c_arr[q] + tbase + c_gofs[q]) = *reinterpret_cast<const uint4*>(st + c_off[q]);
   }
   cp_async_wait<0>();
+}
+
+template <typename Real, int M, int L, int STAGES>
+__global__ void __launch_bounds__(kPassThreads, 2) k_pass(const __grid_constant__ PassParams p) {
+  k_pass_body<Real, M, L, STAGES, PassInterp>(p);
 }
 
 }  // namespace tsg

@@ -27,9 +27,11 @@
 // their FMA in the SPARSE variant, which is exactly zero-skipping).
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
 
 #include <cuda_runtime.h>
+#endif
 
 #include "gate_launch.hpp"
 

@@ -38,6 +38,17 @@ int launch_pass_impl(const PassLaunch& pl, cudaStream_t s, int num_sms) {
   p.n_tmask = insertion_masks(hp, nh, tile_bits, p.tmask);
   if (p.n_tmask > kMaxMasks) throw std::runtime_error("pass tile masks");
   const size_t smem = S::smem_bytes(pl.blob_bytes, kStages);
+  if (pl.jit) {  // the JIT-compiled kernel of this op table: same geometry, two CTAs per SM
+    pass_check(cudaFuncSetAttribute(pl.jit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "k_pass_jit smem attribute");
+    int per_sm = 1;
+    pass_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.jit, kPassThreads, smem), "k_pass_jit occupancy");
+    const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * std::max(per_sm, 1));
+    void* args[] = {&p};
+    pass_check(cudaLaunchKernel(pl.jit, dim3(static_cast<unsigned>(blocks)), dim3(kPassThreads), args, smem, s),
+               "k_pass_jit launch");
+    return 1;
+  }
   auto kern = k_pass<Real, M, L, kStages>;
   static size_t configured = 0;
   if (configured < smem) {

@@ -14,12 +14,14 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
 
 #include "../host/handles.hpp"
 #include "gate_launch.hpp"
+#include "pass_jit.hpp"
 #include "tilesim/pass.hpp"
 #include "tilesim/plan.hpp"
 
@@ -1306,17 +1308,68 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
   }
 }
 
+// JIT-compile the program's tile passes (pass_jit.cu), every distinct op
+// table once, in parallel; a pass whose compile fails keeps the interpreter.
+void jit_passes(tsg_program* prog, const std::vector<unsigned char>& arena) {
+  if (prog->passes.empty() || !tsg::pass_jit_enabled(prog->n)) return;
+  const int runs = prog->prec == 64 ? (1 << (11 - 5)) : (1 << (12 - 6));
+  std::vector<std::string> src(prog->passes.size()), name(prog->passes.size());
+  for (size_t i = 0; i < prog->passes.size(); ++i) {
+    const ProgramPass& pp = prog->passes[i];
+    const auto* ops = reinterpret_cast<const tsg::PassOp*>(arena.data() + pp.blob_offset + runs * sizeof(uint64_t));
+    src[i] = tsg::pass_jit_source(prog->prec, ops, pp.launch.n_ops, &name[i]);
+  }
+  std::vector<const void*> kern(prog->passes.size(), nullptr);
+  std::vector<std::string> err(prog->passes.size());
+  std::vector<std::thread> pool;
+  for (size_t i = 0; i < prog->passes.size(); ++i)
+    pool.emplace_back([&, i] {
+      try {
+        cudaSetDevice(prog->ctx->device);
+        kern[i] = tsg::pass_jit_kernel(src[i], name[i]);
+      } catch (const std::exception& e) {
+        err[i] = e.what();
+      }
+    });
+  for (std::thread& t : pool) t.join();
+  for (size_t i = 0; i < prog->passes.size(); ++i) {
+    prog->passes[i].launch.jit = kern[i];
+    if (!kern[i]) {
+      static std::once_flag warned;
+      std::call_once(warned, [&] { std::fprintf(stderr, "tilesim: pass JIT unavailable, interpreting (%s)\n", err[i].c_str()); });
+    }
+  }
+}
+
 // run_circuit's planning: plan every gate, group the launches into steps
 // (tile passes, block splits), upload matrices and pass blobs once.
+// host half: plans, steps, arena contents (no device work)
+std::unique_ptr<tsg_program> plan_program(tsg_ctx* ctx, const Circuit& fused, double zero_tol, double one_tol,
+                                          int precision_bits, std::vector<unsigned char>& arena);
+
 std::unique_ptr<tsg_program> build_program(tsg_ctx* ctx, const Circuit& fused, double zero_tol, double one_tol,
                                            int precision_bits) {
   use_device(ctx);
   const auto t0 = std::chrono::steady_clock::now();
+  std::vector<unsigned char> arena;
+  auto prog = plan_program(ctx, fused, zero_tol, one_tol, precision_bits, arena);
+  if (!arena.empty()) {
+    ck(cudaMalloc(&prog->arena, arena.size()), "cudaMalloc program arena");
+    ck(cudaMemcpy(prog->arena, arena.data(), arena.size(), cudaMemcpyHostToDevice), "program arena upload");
+  }
+  jit_passes(prog.get(), arena);
+  ck(cudaEventCreate(&prog->ev0), "event");
+  ck(cudaEventCreate(&prog->ev1), "event");
+  prog->planning_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return prog;
+}
+
+std::unique_ptr<tsg_program> plan_program(tsg_ctx* ctx, const Circuit& fused, double zero_tol, double one_tol,
+                                          int precision_bits, std::vector<unsigned char>& arena) {
   auto prog = std::make_unique<tsg_program>();
   prog->ctx = ctx;
   prog->n = fused.n_qubits;
   prog->prec = precision_bits;
-  std::vector<unsigned char> arena;
   const uint64_t amp = precision_bits == 64 ? 16 : 8;
   for (const Gate& g : fused.gates) {
     ProgramGate pg;
@@ -1353,18 +1406,11 @@ std::unique_ptr<tsg_program> build_program(tsg_ctx* ctx, const Circuit& fused, d
     }
     prog->touched_bytes += static_cast<uint64_t>(2.0 * std::ldexp(1.0, prog->n) * amp * frac);
   }
-  if (!arena.empty()) {
-    ck(cudaMalloc(&prog->arena, arena.size()), "cudaMalloc program arena");
-    ck(cudaMemcpy(prog->arena, arena.data(), arena.size(), cudaMemcpyHostToDevice), "program arena upload");
-  }
   // the host snapped matrices referenced by launch.m_re/m_im must follow the moved vectors
   for (ProgramGate& pg : prog->gates) {
     pg.launch.m_re = pg.ls.sub_re.data();
     pg.launch.m_im = pg.ls.sub_im.data();
   }
-  ck(cudaEventCreate(&prog->ev0), "event");
-  ck(cudaEventCreate(&prog->ev1), "event");
-  prog->planning_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return prog;
 }
 
@@ -1372,6 +1418,35 @@ std::unique_ptr<tsg_program> build_program(tsg_ctx* ctx, const Circuit& fused, d
 
 // ================================================================ C ABI ===
 extern "C" {
+
+int tsc_pass_jit_precompile(const tsc_circuit* fused, int precision_bits, double zero_tol, double one_tol,
+                            int* n_passes) {
+  TSG_TRY({
+    require(fused && n_passes, "null argument");
+    require(precision_bits == 64 || precision_bits == 32, "precision_bits must be 64 or 32");
+    std::vector<unsigned char> arena;
+    auto prog = plan_program(nullptr, fused->c, zero_tol, one_tol, precision_bits, arena);
+    const int runs = precision_bits == 64 ? (1 << (11 - 5)) : (1 << (12 - 6));
+    std::vector<std::thread> pool;
+    std::vector<std::string> err(prog->passes.size());
+    for (size_t i = 0; i < prog->passes.size(); ++i)
+      pool.emplace_back([&, i] {
+        try {
+          const ProgramPass& pp = prog->passes[i];
+          const auto* ops = reinterpret_cast<const tsg::PassOp*>(arena.data() + pp.blob_offset + runs * sizeof(uint64_t));
+          std::string name;
+          const std::string src = tsg::pass_jit_source(precision_bits, ops, pp.launch.n_ops, &name);
+          tsg::pass_jit_cubin(src, name);
+        } catch (const std::exception& e) {
+          err[i] = e.what();
+        }
+      });
+    for (std::thread& t : pool) t.join();
+    for (const std::string& e : err)
+      if (!e.empty()) throw SimError(e);
+    *n_passes = static_cast<int>(prog->passes.size());
+  })
+}
 
 int tsg_device_count(int* out) {
   int n = 0;
@@ -1952,7 +2027,7 @@ int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* ou
       const ProgramPass& pp = prog->passes[st.index];
       out->n_high = pp.launch.tile_log2 - pp.launch.run_log2;
       for (int h = 0; h < out->n_high; ++h) out->high[h] = pp.launch.high[h];
-      name = "k_pass";
+      name = pp.launch.jit ? "k_pass_jit" : "k_pass";
     } else if (st.kind == kStepBatch) {
       name = "k_diag_batch";
     } else if (!prog->gates[st.gate].subs.empty()) {  // block split: "<part kernel> xN split"

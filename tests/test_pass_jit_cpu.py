@@ -1,0 +1,18 @@
+"""The JIT tile-pass code generator on CPU: NVRTC compiles every pass of the
+bench circuits for sm_100a (no device needed), and the disk cache is keyed by
+the op table (a second precompile compiles nothing new)."""
+import paper_2503_19894_b200 as ts
+
+
+def test_precompile_bench_circuits(tmp_path, monkeypatch):
+    monkeypatch.setenv("TSG_JIT_CACHE_DIR", str(tmp_path))
+    total = 0
+    for kind, n, depth, seed, prec in (("qft", 24, 1, 0, "f64"), ("rqc", 24, 8, 42, "f64"), ("hes", 24, 3, 1, "f32")):
+        fused, _ = ts.run_fusion(ts.gen_benchmark(kind, n, depth, seed), ts.FusionConfig(k_max=5))
+        total += ts.pass_jit_precompile(fused, prec)
+    files = sorted(p.name for p in tmp_path.glob("*.cubin"))
+    assert total > 0 and 0 < len(files) <= total
+    stamp = {p.name: p.stat().st_mtime_ns for p in tmp_path.glob("*.cubin")}
+    fused, _ = ts.run_fusion(ts.gen_benchmark("qft", 24), ts.FusionConfig(k_max=5))
+    ts.pass_jit_precompile(fused, "f64")
+    assert {p.name: p.stat().st_mtime_ns for p in tmp_path.glob("*.cubin")} == stamp
