@@ -48,8 +48,13 @@ struct PassConfig {
   bool force = false;
 };
 
-// Defaults per state precision (64: complex128, 32: complex64).
-PassConfig pass_config(int precision_bits);
+// Whether a program over n qubits gets JIT-compiled passes (the runtime's
+// rule: TSG_PASS_JIT=0 disables, TSG_PASS_JIT_MIN_N, default 24).
+bool pass_jit_expected(int n_qubits);
+// Defaults per state precision (64: complex128, 32: complex64); the op costs
+// are those of the kernel the passes of an n-qubit program will run (the JIT
+// pass or the interpreter; n_qubits = 0: the interpreter's).
+PassConfig pass_config(int precision_bits, int n_qubits = 0);
 
 enum class PassRole : int { Standalone = 0, Diag = 1, Gen = 2 };
 

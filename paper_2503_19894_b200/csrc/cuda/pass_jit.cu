@@ -37,6 +37,7 @@
 
 #include "gate_launch.hpp"
 #include "pass_jit.hpp"
+#include "tilesim/pass.hpp"
 
 #include "jit_headers.inc"
 
@@ -228,12 +229,7 @@ Cache& cache() {
 
 }  // namespace
 
-bool pass_jit_enabled(int n_qubits) {
-  const char* off = std::getenv("TSG_PASS_JIT");
-  if (off && std::strcmp(off, "0") == 0) return false;
-  const char* e = std::getenv("TSG_PASS_JIT_MIN_N");
-  return n_qubits >= (e ? std::atoi(e) : 24);
-}
+bool pass_jit_enabled(int n_qubits) { return tilesim::pass_jit_expected(n_qubits); }
 
 std::string pass_jit_source(int precision_bits, const PassOp* ops, int n_ops, std::string* name) {
   std::ostringstream os;

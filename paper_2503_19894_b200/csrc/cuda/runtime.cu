@@ -1237,7 +1237,7 @@ ProgramPermute compose_permutation(const tsg_program* prog, const std::vector<in
 // Steps of a program: tile passes (tilesim/pass.hpp) when the state holds at
 // least one tile, else per-gate launches with diagonal batches.
 void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
-  const PassConfig cfg = pass_config(prog->prec);
+  const PassConfig cfg = pass_config(prog->prec, prog->n);
   const bool use_pass = !std::getenv("TSG_NO_PASS") && prog->n >= cfg.tile_log2;
   if (use_pass) {
     std::vector<LaunchStructure> ls;

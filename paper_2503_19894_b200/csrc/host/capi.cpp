@@ -216,7 +216,7 @@ int tsc_plan_passes(const tsc_circuit* fused, int precision_bits, double zero_to
       const KernelPlan plan = plan_kernel(g, n, 0, zero_tol, one_tol, false);
       ls.push_back(precision_bits == 64 ? plan.launch : derive_launch(plan, nullptr, precision_bits));
     }
-    const auto steps = plan_passes(ls, n, pass_config(precision_bits));
+    const auto steps = plan_passes(ls, n, pass_config(precision_bits, n));
     if (step_of_gate)
       for (size_t g = 0; g < ls.size(); ++g) step_of_gate[g] = -1;
     for (size_t s = 0; s < steps.size(); ++s) {

@@ -8,14 +8,26 @@
 
 namespace tilesim {
 
-PassConfig pass_config(int precision_bits) {
+bool pass_jit_expected(int n_qubits) {
+  const char* off = std::getenv("TSG_PASS_JIT");
+  if (off && off[0] == '0' && off[1] == '\0') return false;
+  const char* e = std::getenv("TSG_PASS_JIT_MIN_N");
+  return n_qubits >= (e ? std::atoi(e) : 24);
+}
+
+PassConfig pass_config(int precision_bits, int n_qubits) {
   PassConfig c;
+  const bool jit = n_qubits > 0 && pass_jit_expected(n_qubits);
   if (precision_bits == 64) {
     c.tile_log2 = 11;  // 32 KiB of complex128 per tile
     c.run_log2 = 5;    // 256-byte runs per array
     c.max_gen_ks = 4;  // dense ks = 5 complex128 is FP64-bound: own DMMA kernel
     c.amp_real_bytes = 8;
     c.reg_bits = 3;
+    // JIT passes keep the interpreter's complex128 table: the per-op micro
+    // costs measured lower (profiles/r02/pass_bench_jit_f64.txt), but QFT-30 and
+    // RQC-30 planned with them ran slower (76.7 / 395 ms vs 73.3 / 388 ms)
+    (void)jit;
   } else {
     c.tile_log2 = 12;
     c.run_log2 = 6;
@@ -29,6 +41,14 @@ PassConfig pass_config(int precision_bits) {
     c.perm_sweeps_reg = 0.45;
     c.perm_sweeps_smem = 0.6;
     c.standalone_sweeps = 1.1;
+    if (jit) {  // JIT passes (r02 scripts/pass_bench.py PB_FORCE=1, profiles/r02/pass_bench_jit_f32.txt)
+      c.base_sweeps = 1.04;
+      c.diag_sweeps = 0.01;
+      const double gen32j[6] = {0.0, 0.05, 0.12, 0.45, 1.1, 2.1};
+      std::copy(gen32j, gen32j + 6, c.gen_sweeps);
+      c.perm_sweeps_reg = 0.25;
+      c.perm_sweeps_smem = 0.5;
+    }
   }
   const char* f = std::getenv("TSG_PASS_FORCE");
   c.force = f && f[0] == '1';

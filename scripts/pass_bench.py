@@ -40,8 +40,11 @@ def case(name, gates):
     for no_pass in (False, True):
         if no_pass:
             os.environ["TSG_NO_PASS"] = "1"
+        elif os.environ.get("PB_FORCE") == "1":  # every eligible gate joins the pass (cost calibration)
+            os.environ["TSG_PASS_FORCE"] = "1"
         prog = ts.Program(c, PREC)
         os.environ.pop("TSG_NO_PASS", None)
+        os.environ.pop("TSG_PASS_FORCE", None)
         sv = ts.Statevector(N, PREC).init_basis(3)
         prog.run(sv)
         best = min(prog.run(sv)["execution_s"] for _ in range(3))
@@ -79,6 +82,12 @@ cases = {
     "4x gen ks3 same": [([6, 7, 8], "dense")] * 4,
     "4x gen ks3 diff": [([6, 7, 8], "dense"), ([9, 10, 11], "dense"), ([6, 7, 8], "dense"), ([9, 10, 11], "dense")],
     "4x gen ks1 same-layout": [([6], "dense"), ([7], "dense"), ([8], "dense"), ([6], "dense")],
+    "2x gen ks4 smem": [([5, 6, 7, 8], "dense"), ([7, 8, 9, 10], "dense")],
+    "1x gen ks4 smem": [([5, 6, 7, 8], "dense")],
+    "1x gen ks4 smem low": [([0, 1, 2, 3], "dense")],
+    "1x gen ks5 smem": [([5, 6, 7, 8, 9], "dense")],
+    "1x gen ks3": [([6, 7, 8], "dense")],
+    "1x gen ks3 low": [([1, 2, 3], "dense")],
     "4x gen ks4 smem": [([5, 6, 7, 8], "dense"), ([7, 8, 9, 10], "dense"), ([5, 6, 9, 10], "dense"), ([6, 7, 8, 9], "dense")],
     "4x perm ks2": [([6, 7], "perm"), ([8, 9], "perm"), ([1, 7], "perm"), ([2, 9], "perm")],
     "4x perm ks4": [([0, 1, 9, 10], "perm"), ([2, 3, 7, 8], "perm"), ([0, 2, 9, 7], "perm"), ([5, 6, 7, 8], "perm")],
