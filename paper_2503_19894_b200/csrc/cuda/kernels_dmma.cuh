@@ -106,10 +106,21 @@ struct DmmaParams {
   uint32_t nzblk[3];       // bit (rb * KST + ks): block of Mr / Mi / Ms is nonzero
 };
 
+// A pure function of its operands (no volatile): the compiler may schedule
+// the fragment loads around it freely.
+#ifndef TSG_DMMA_VOLATILE
+#define TSG_DMMA_VOLATILE 0
+#endif
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+#if TSG_DMMA_VOLATILE
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
+#else
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+#endif
 }
 
 // in-run position of group g (low targets zero, low controls at their value)

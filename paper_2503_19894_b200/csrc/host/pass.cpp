@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 namespace tilesim {
@@ -50,6 +51,17 @@ PassConfig pass_config(int precision_bits, int n_qubits) {
       c.perm_sweeps_smem = 0.5;
     }
   }
+  // calibration experiments: TSG_PASS_COSTS="base,diag,g1,g2,g3,g4,g5,max_gen_ks"
+  if (const char* e = std::getenv("TSG_PASS_COSTS")) {
+    double v[8];
+    if (std::sscanf(e, "%lf,%lf,%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6], &v[7]) == 8) {
+      c.base_sweeps = v[0];
+      c.diag_sweeps = v[1];
+      for (int k = 1; k <= 5; ++k) c.gen_sweeps[k] = v[1 + k];
+      c.max_gen_ks = static_cast<int>(v[7]);
+    }
+  }
+  if (const char* e = std::getenv("TSG_PASS_GEOM")) std::sscanf(e, "%d,%d", &c.tile_log2, &c.run_log2);  // planner experiments only
   const char* f = std::getenv("TSG_PASS_FORCE");
   c.force = f && f[0] == '1';
   if (std::getenv("TSG_NO_PERMUTE")) c.min_permute_run = 0;
