@@ -478,7 +478,19 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
       p.nzblk[1] |= static_cast<uint32_t>(nzi) << bit;
       p.nzblk[2] |= static_cast<uint32_t>(nzs) << bit;
     }
-  const bool sparse = (p.nzblk[0] & p.nzblk[1] & p.nzblk[2]) != (S::RB * S::KST >= 32 ? ~0u : ((1u << (S::RB * S::KST)) - 1));
+  // The sparse variant (per-tile predicates) pays only when it skips at least
+  // a quarter of the DMMAs: RQC-30's 5-qubit gates with 28/32 nonzero tiles ran
+  // 8-10 ms sparse, 7.7-8.4 ms dense (scripts/ks5_rqc_sparse.py); skipped zero
+  // tiles would only have added exact zeros.
+  const int n_dmma_tiles = 3 * S::RB * S::KST;
+  const int nonzero = __builtin_popcount(p.nzblk[0]) + __builtin_popcount(p.nzblk[1]) + __builtin_popcount(p.nzblk[2]);
+  static const bool any_zero_rule = std::getenv("TSG_DMMA_SPARSE_ANY") != nullptr;  // round-1 rule (A/B runs)
+  bool sparse = any_zero_rule ? nonzero < n_dmma_tiles : 4 * (n_dmma_tiles - nonzero) >= n_dmma_tiles;
+  static const int force_sparse = [] {  // experiments: TSG_DMMA_SPARSE=0|1 forces the variant
+    const char* e = std::getenv("TSG_DMMA_SPARSE");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (force_sparse >= 0) sparse = force_sparse == 1;
   const int most = std::max({__builtin_popcount(p.nzblk[0]), __builtin_popcount(p.nzblk[1]), __builtin_popcount(p.nzblk[2])});
   if (!dmma_geometry<Real, KS>(g, p, &smem, &stages, simt, 2 * most <= S::RB * S::KST)) return false;
   p.re = static_cast<Real*>(g.re);
