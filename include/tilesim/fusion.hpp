@@ -55,6 +55,15 @@ struct FusionConfig {
   double zero_tol = 1e-8, one_tol = 1e-8;
   int max_traversals = 64;
   int threads = 1;  // thread/CTA column used for cost lookups
+  // Shard-aware fusion (B200 extension): with the top
+  // n_global qubits sharded across GPUs, a fusion is refused when the fused
+  // gate mixes (acts non-block-diagonally on) more of those qubits than the
+  // wider-mixing of its two parts -- such a product would need an exchange
+  // its parts did not.  0: the reference's fusion, unchanged (the default:
+  // measured on RQC-33 / TFIM-36 / ALA-30 / IQP-30 over 8 ranks, the
+  // restriction leaves more, smaller gates and MORE exchanges -- 4 -> 5,
+  // 5 -> 14, 7 -> 9, 1 -> 4).
+  int n_global = 0;
 };
 
 // Preset "paper-cpu": k_max 7, op cap 4096, adaptive.

@@ -56,6 +56,7 @@ int tsg_device_count(int* out);
  * One context per GPU (one process per GPU in multi-GPU runs). */
 int tsg_ctx_create(int device, tsg_ctx** out);
 int tsg_ctx_destroy(tsg_ctx* ctx);
+int tsg_ctx_info(const tsg_ctx* ctx, int* device, int* num_sms);
 
 /* ----------------------------------------------------------------- state
  * Statevector / init_zero_state.  precision_bits: 64 for
@@ -204,7 +205,8 @@ typedef struct tsc_fusion_config {
   int multi_traversal;
   double zero_tol, one_tol;
   int max_traversals;
-  int threads;           /* cost-model thread/CTA column */
+  int threads;           /* cost-model thread/CTA column (GPU: SMs) */
+  int n_global;          /* shard-aware fusion over the top n_global qubits (0: off) */
 } tsc_fusion_config;
 
 typedef struct tsc_fusion_stats {
@@ -292,15 +294,26 @@ int tsg_dist_run_local_only(tsg_dist* d, const tsc_shard_plan* plan, tsg_run_rep
 /* this rank's 2^(n-n_global) amplitudes (physical order of the last plan) */
 int tsg_dist_download_local(tsg_dist* d, double* re, double* im);
 int tsg_dist_local_sumsq(tsg_dist* d, double* out);
+/* sharded QSV1: <path>.r<rank> = this shard as a QSV1 dump,
+ * <path>.layout (rank 0) = n, n_global, precision and the qubit map pos[n]
+ * (logical qubit q at physical position pos[q], e.g. ShardPlan final_pos);
+ * load reads this rank's shard back and returns the map */
+int tsg_dist_dump(tsg_dist* d, const char* path, const int* pos);
+int tsg_dist_load(tsg_dist* d, const char* path, int* pos);
 /* host-only check of the rendezvous (no device): `iters` rounds of
  * write-slot / barrier / sum-all-slots; *checksum = sum over rounds */
 int tsg_rendezvous_selftest(const unsigned char id[128], int rank, int world, int iters, uint64_t* checksum);
 
 /* bench_cost_model on the GPU: for k in [1, k_max] and
- * densities {dense, half, quarter}, times the real kernel on a 2^bench_n
- * scratch state, median of `repetitions`, threads = CTA size. */
+ * densities {diagonal, quarter, half, dense}, times the real kernel on a
+ * 2^bench_n scratch state, median of `repetitions`.  `threads`
+ * is the number of SMs the kernels' persistent grids span: the plain call
+ * records the full device (threads = its SM count), the _sms form one record
+ * set per entry of sm_counts (each in [1, SM count]). */
 int tsg_bench_cost_model(tsg_ctx* ctx, int bench_n, int k_max, int precision_bits, int repetitions, uint64_t seed,
                          tsc_cost_model** out);
+int tsg_bench_cost_model_sms(tsg_ctx* ctx, int bench_n, int k_max, int precision_bits, int repetitions, uint64_t seed,
+                             const int* sm_counts, int n_sm_counts, tsc_cost_model** out);
 
 #ifdef __cplusplus
 }

@@ -98,7 +98,7 @@ STEP_KINDS = ("gate", "diag_batch", "pass", "permute")
 class _FusionConfigC(C.Structure):
     _fields_ = [("mode", C.c_int), ("k_max", C.c_int), ("max_op_count", _i64), ("agglomerative", C.c_int),
                 ("multi_traversal", C.c_int), ("zero_tol", C.c_double), ("one_tol", C.c_double),
-                ("max_traversals", C.c_int), ("threads", C.c_int)]
+                ("max_traversals", C.c_int), ("threads", C.c_int), ("n_global", C.c_int)]
 
 
 class _FusionStatsC(C.Structure):
@@ -150,7 +150,9 @@ _sig("tsg_program_gate_info", [_vp, _u64, C.POINTER(PlanInfo)])
 _sig("tsg_program_step_count", [_vp, C.POINTER(_u64)])
 _sig("tsg_program_step_info", [_vp, _u64, C.POINTER(StepInfo)])
 _sig("tsc_plan_passes", [_vp, C.c_int, C.c_double, C.c_double, _ip, _ip, _ip, C.POINTER(_u64)])
+_sig("tsg_ctx_info", [_vp, _ip, _ip])
 _sig("tsg_bench_cost_model", [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _u64, C.POINTER(_vp)])
+_sig("tsg_bench_cost_model_sms", [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _u64, _ip, C.c_int, C.POINTER(_vp)])
 _sig("tsc_circuit_create", [C.c_int, C.POINTER(_vp)])
 _sig("tsc_circuit_destroy", [_vp])
 _sig("tsc_circuit_copy", [_vp, C.POINTER(_vp)])
@@ -311,6 +313,7 @@ class FusionConfig:
     one_tol: float = 1e-8
     max_traversals: int = 64
     threads: int = 1
+    n_global: int = 0  # shard-aware fusion over the top n_global qubits (0: the reference's fusion)
 
     @staticmethod
     def paper_cpu() -> "FusionConfig":
@@ -322,7 +325,7 @@ class FusionConfig:
             raise ConfigError(f"unknown fusion mode {self.mode!r}")
         return _FusionConfigC(modes[self.mode], self.k_max, -1 if self.max_op_count is None else self.max_op_count,
                               int(self.agglomerative), int(self.multi_traversal), self.zero_tol, self.one_tol,
-                              self.max_traversals, self.threads)
+                              self.max_traversals, self.threads, self.n_global)
 
 
 class CostModel:
@@ -380,6 +383,9 @@ class Context:
         _check(_lib.tsg_ctx_create(device, C.byref(h)))
         self._h = h.value
         self.device = device
+        sms = C.c_int()
+        _check(_lib.tsg_ctx_info(self._h, None, C.byref(sms)))
+        self.num_sms = sms.value
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -640,11 +646,17 @@ def run_circuit(c: Circuit, sv: Statevector, zero_tol=1e-8, one_tol=1e-8, use_gr
 
 
 def bench_cost_model(bench_n: int = 28, k_max: int = 6, precision: str = "f64", repetitions: int = 5,
-                     seed: int = 1, ctx: Context | None = None) -> CostModel:
+                     seed: int = 1, ctx: Context | None = None, sm_counts=None) -> CostModel:
+    """GPU bench_cost_model.  `threads` of the records = SMs
+    the kernels span: the full device by default, or each of sm_counts."""
     ctx = ctx or default_context()
     h = _vp()
-    _check(_lib.tsg_bench_cost_model(ctx._h, bench_n, k_max, 64 if precision in ("f64", "c128") else 32,
-                                     repetitions, seed, C.byref(h)))
+    bits = 64 if precision in ("f64", "c128") else 32
+    if sm_counts is None:
+        _check(_lib.tsg_bench_cost_model(ctx._h, bench_n, k_max, bits, repetitions, seed, C.byref(h)))
+    else:
+        _check(_lib.tsg_bench_cost_model_sms(ctx._h, bench_n, k_max, bits, repetitions, seed, _ints(sm_counts),
+                                             len(sm_counts), C.byref(h)))
     return CostModel(_handle=h.value)
 
 
@@ -664,6 +676,8 @@ _sig("tsg_dist_init_basis", [_vp, _u64])
 _sig("tsg_dist_run", [_vp, _vp, C.POINTER(RunReport)])
 _sig("tsg_dist_run_local_only", [_vp, _vp, C.POINTER(RunReport)])
 _sig("tsg_dist_upload_local", [_vp, _dp, _dp])
+_sig("tsg_dist_dump", [_vp, C.c_char_p, _ip])
+_sig("tsg_dist_load", [_vp, C.c_char_p, _ip])
 _sig("tsg_rendezvous_selftest", [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(_u64)])
 _sig("tsg_dist_download_local", [_vp, _dp, _dp])
 _sig("tsg_dist_local_sumsq", [_vp, _dp])
@@ -812,6 +826,16 @@ class DistState:
         out = C.c_double()
         _check(_lib.tsg_dist_local_sumsq(self._h, C.byref(out)))
         return out.value
+
+    def dump(self, path: str, final_pos) -> None:
+        """Sharded QSV1: this rank's shard to <path>.r<rank>, the layout (rank 0) to <path>.layout."""
+        _check(_lib.tsg_dist_dump(self._h, os.fsencode(path), _ints(list(final_pos))))
+
+    def load(self, path: str) -> list:
+        """Read this rank's shard of a sharded QSV1 dump; returns the qubit map it is laid out in."""
+        pos = (C.c_int * self.n)()
+        _check(_lib.tsg_dist_load(self._h, os.fsencode(path), pos))
+        return list(pos)
 
 
 def rendezvous_selftest(uid: bytes, rank: int, world: int, iters: int = 100) -> int:

@@ -1458,6 +1458,14 @@ int tsg_device_count(int* out) {
   return TSG_OK;
 }
 
+int tsg_ctx_info(const tsg_ctx* ctx, int* device, int* num_sms) {
+  TSG_TRY({
+    require(ctx != nullptr, "null handle");
+    if (device) *device = ctx->device;
+    if (num_sms) *num_sms = ctx->num_sms;
+  })
+}
+
 int tsg_ctx_create(int device, tsg_ctx** out) {
   TSG_TRY({
     require(out != nullptr, "null output handle");
@@ -2053,8 +2061,24 @@ int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* ou
 // (one device); the host string names the device and clocks.
 int tsg_bench_cost_model(tsg_ctx* ctx, int bench_n, int k_max, int precision_bits, int repetitions, uint64_t seed,
                          tsc_cost_model** out) {
+  if (!ctx) {
+    tsg_detail::set_error("null argument");
+    return TSG_ERR_CONFIG;
+  }
+  const int full = ctx->num_sms;
+  return tsg_bench_cost_model_sms(ctx, bench_n, k_max, precision_bits, repetitions, seed, &full, 1, out);
+}
+
+// The B200 form of SPEC's `threads` axis (kernels timed per
+// worker count): the number of SMs the persistent grids of the gate kernels
+// span.  Every (k, density) point is timed once per SM count; records carry
+// threads = that SM count (the full device: ctx's SM count).
+int tsg_bench_cost_model_sms(tsg_ctx* ctx, int bench_n, int k_max, int precision_bits, int repetitions, uint64_t seed,
+                             const int* sm_counts, int n_sm_counts, tsc_cost_model** out) {
   TSG_TRY({
-    require(ctx && out, "null argument");
+    require(ctx && out && sm_counts && n_sm_counts >= 1, "null argument");
+    for (int i = 0; i < n_sm_counts; ++i)
+      require(sm_counts[i] >= 1 && sm_counts[i] <= ctx->num_sms, "SM counts must be in [1, the device's SM count]");
     require(bench_n >= 8 && bench_n <= 34, "bench_n must be in [8, 34]");
     require(k_max >= 1 && k_max <= 6 && k_max < bench_n, "k_max must be in [1, 6]");
     require(repetitions >= 1, "repetitions must be >= 1");
@@ -2074,7 +2098,7 @@ int tsg_bench_cost_model(tsg_ctx* ctx, int bench_n, int k_max, int precision_bit
     ck(cudaMalloc(&dev_mat, 3 * 4096 * sizeof(double)), "cudaMalloc bench matrix");
     for (int k = 1; k <= k_max; ++k) {
       for (int level = 0; level < 4; ++level) {  // 0 diag, 1 quarter, 2 half, 3 dense
-        std::vector<double> times;
+        std::vector<std::vector<double>> times(n_sm_counts);
         uint64_t ops = 0;
         for (int trial = 0; trial < 2; ++trial) {
           std::vector<int> pool(bench_n);
@@ -2105,25 +2129,34 @@ int tsg_bench_cost_model(tsg_ctx* ctx, int bench_n, int k_max, int precision_bit
             g.dev_mat = dev_mat;
           }
           ops = std::max(ops, plan.profile.op_count);
-          launch(st, g);  // warm-up (first-use kernel attributes)
-          for (int r = 0; r < repetitions; ++r) {
-            ck(cudaEventRecord(e0, st->stream), "event");
-            launch(st, g);
-            ck(cudaEventRecord(e1, st->stream), "event");
-            ck(cudaEventSynchronize(e1), "event sync");
-            float ms = 0.f;
-            ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
-            times.push_back(ms * 1e-3);
+          for (int t = 0; t < n_sm_counts; ++t) {
+            // the same state and stream, launches sized for sm_counts[t] SMs
+            tsg_ctx sub = *ctx;
+            sub.num_sms = sm_counts[t];
+            tsg_state view = *st;
+            view.ctx = &sub;
+            launch(&view, g);  // warm-up (first-use kernel attributes)
+            for (int r = 0; r < repetitions; ++r) {
+              ck(cudaEventRecord(e0, st->stream), "event");
+              launch(&view, g);
+              ck(cudaEventRecord(e1, st->stream), "event");
+              ck(cudaEventSynchronize(e1), "event sync");
+              float ms = 0.f;
+              ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+              times[t].push_back(ms * 1e-3);
+            }
           }
         }
-        std::sort(times.begin(), times.end());
-        const double med = times[times.size() / 2];
-        CostRecord rec;
-        rec.k = k;
-        rec.op_count = ops;
-        rec.threads = 1;
-        rec.seconds_per_group = std::max(med, 1e-9) / std::ldexp(1.0, bench_n - k);
-        cm.records.push_back(rec);
+        for (int t = 0; t < n_sm_counts; ++t) {
+          std::sort(times[t].begin(), times[t].end());
+          const double med = times[t][times[t].size() / 2];
+          CostRecord rec;
+          rec.k = k;
+          rec.op_count = ops;
+          rec.threads = sm_counts[t];
+          rec.seconds_per_group = std::max(med, 1e-9) / std::ldexp(1.0, bench_n - k);
+          cm.records.push_back(rec);
+        }
       }
     }
     cudaFree(dev_mat);

@@ -611,6 +611,48 @@ int tsg_dist_run_local_only(tsg_dist* d, const tsc_shard_plan* plan, tsg_run_rep
   return dist_run_impl(d, plan, 1, report);
 }
 
+// Sharded QSV1 (SPEC.md:565 per shard): <path>.r<rank> is a plain QSV1 dump
+// of this rank's 2^n_local amplitudes in physical order; rank 0 also writes
+// <path>.layout -- n, n_global, precision and the qubit map (logical qubit q
+// at physical position pos[q]) the shards are laid out in.  A resumed run
+// loads the shards and continues with plans made for the same layout.
+int tsg_dist_dump(tsg_dist* d, const char* path, const int* pos) {
+  TSG_TRY({
+    require(d && path && pos, "null argument");
+    std::vector<int> seen(d->n, 0);
+    for (int q = 0; q < d->n; ++q) {
+      require(pos[q] >= 0 && pos[q] < d->n && !seen[pos[q]], "qubit map is not a permutation");
+      seen[pos[q]] = 1;
+    }
+    const std::string base(path);
+    if (tsg_state_dump(d->st, (base + ".r" + std::to_string(d->rank)).c_str())) throw SimError(tsg_last_error());
+    if (d->rank == 0) {
+      std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen((base + ".layout").c_str(), "w"), std::fclose);
+      if (!f) throw SimError("cannot open " + base + ".layout for writing");
+      std::fprintf(f.get(), "qsv1-sharded 1\nn %d\nn_global %d\nprecision %d\npos", d->n, d->n_global, d->st->prec);
+      for (int q = 0; q < d->n; ++q) std::fprintf(f.get(), " %d", pos[q]);
+      std::fprintf(f.get(), "\n");
+    }
+  })
+}
+
+int tsg_dist_load(tsg_dist* d, const char* path, int* pos) {
+  TSG_TRY({
+    require(d && path && pos, "null argument");
+    const std::string base(path);
+    std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen((base + ".layout").c_str(), "r"), std::fclose);
+    if (!f) throw SimError("cannot open " + base + ".layout");
+    int version = 0, n = 0, g = 0, prec = 0;
+    if (std::fscanf(f.get(), "qsv1-sharded %d n %d n_global %d precision %d pos", &version, &n, &g, &prec) != 4 ||
+        version != 1)
+      throw SimError(base + ".layout: not a sharded QSV1 layout");
+    require(n == d->n && g == d->n_global && prec == d->st->prec, "sharded dump does not match the distributed state");
+    for (int q = 0; q < n; ++q)
+      if (std::fscanf(f.get(), "%d", &pos[q]) != 1) throw SimError(base + ".layout: truncated qubit map");
+    if (tsg_state_load(d->st, (base + ".r" + std::to_string(d->rank)).c_str())) throw SimError(tsg_last_error());
+  })
+}
+
 int tsg_dist_download_local(tsg_dist* d, double* re, double* im) {
   if (!d) {
     tsg_detail::set_error("null handle");

@@ -45,6 +45,8 @@ FusionConfig to_config(const tsc_fusion_config* c) {
   f.one_tol = c->one_tol;
   f.max_traversals = c->max_traversals;
   f.threads = c->threads;
+  f.n_global = c->n_global;
+  require(f.n_global >= 0, "n_global must be >= 0");
   require(f.zero_tol >= 0 && f.one_tol >= 0, "tolerances must be >= 0");
   return f;
 }

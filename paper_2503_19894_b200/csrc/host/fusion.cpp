@@ -13,6 +13,7 @@
 //  * flatten: rows top to bottom, ascending min-wire; fused matrix = left
 //    fold of fuse_matrices over the constituent gates.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <fstream>
@@ -186,16 +187,46 @@ int64_t CircuitTile::ops_of(GateBlock& b) {
   return b.ops;
 }
 
+// Global qubits (>= n - n_global) a gate acts on non-block-diagonally: some
+// nonzero entry (zero_tol) differs between row and column in that bit.
+static int global_mixed(const Gate& g, int n, int n_global, double zt, double ot) {
+  int count = 0;
+  const uint64_t D = g.matrix.dim();
+  for (int b = 0; b < g.k(); ++b) {
+    if (g.targets[b] < n - n_global) continue;
+    bool mixes = false;
+    for (uint64_t r = 0; r < D && !mixes; ++r)
+      for (uint64_t c = 0; c < D && !mixes; ++c) {
+        if (!(((r ^ c) >> b) & 1u)) continue;
+        const cplx& v = g.matrix.at(r, c);
+        mixes = classify_scalar(v.real(), zt, ot) != ScalarKind::Zero || classify_scalar(v.imag(), zt, ot) != ScalarKind::Zero;
+      }
+    count += mixes;
+  }
+  return count;
+}
+
 bool CircuitTile::fusible(int first, int second, int k, Gate* product) {
   GateBlock& a = blocks_[first];
   GateBlock& b = blocks_[second];
   if (!fusible_size_only(a.wires, b.wires, k)) return false;
-  if (cfg_.mode != FusionMode::Adaptive) return true;
+  if (cfg_.mode != FusionMode::Adaptive && cfg_.n_global <= 0) return true;
   // fusible_adaptive: the fused profile is taken on the
   // materialized product = fold(first.gates ++ second.gates).
   materialize(a);
   Gate p = a.fused;
   for (int gi : b.gates) p = fuse_matrices(p, src_.gates[gi]);
+  if (cfg_.n_global > 0) {
+    materialize(b);
+    const int gp = global_mixed(p, n_, cfg_.n_global, cfg_.zero_tol, cfg_.one_tol);
+    const int ga = global_mixed(a.fused, n_, cfg_.n_global, cfg_.zero_tol, cfg_.one_tol);
+    const int gb = global_mixed(b.fused, n_, cfg_.n_global, cfg_.zero_tol, cfg_.one_tol);
+    if (gp > std::max(ga, gb)) return false;
+    if (cfg_.mode != FusionMode::Adaptive) {
+      *product = std::move(p);
+      return true;
+    }
+  }
   const uint64_t ops = sparsity_profile(p.matrix, cfg_.zero_tol, cfg_.one_tol).op_count;
   if (cfg_.max_op_count && ops > *cfg_.max_op_count) return false;
   if (!cm_) throw ConfigError("adaptive fusion needs a cost model");

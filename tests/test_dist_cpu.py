@@ -97,3 +97,17 @@ def test_pipeline_counts_on_the_c4_c5_configs():
         out[kind] = (info["exchanges"], info["pipelined_exchanges"])
         assert info["exchanges"] > 0
     print(out)
+
+
+def test_shard_aware_fusion_option():
+    """FusionConfig.n_global: the fused gates never mix more of the top
+    n_global qubits than their parts did; n_global = 0 is the reference's
+    fusion bit for bit."""
+    c = ts.gen_benchmark("qaoa", 16, 2, 3)
+    base, _ = ts.run_fusion(c, ts.FusionConfig(k_max=5))
+    same, _ = ts.run_fusion(c, ts.FusionConfig(k_max=5, n_global=0))
+    assert [g.targets for g in base.gates()] == [g.targets for g in same.gates()]
+    assert all(np.array_equal(a.matrix, b.matrix) for a, b in zip(base.gates(), same.gates()))
+    aware, st = ts.run_fusion(c, ts.FusionConfig(k_max=5, n_global=2))
+    assert st["fused_block_count"] >= len(base)
+    assert max(len(g.targets) for g in aware.gates()) <= 5
