@@ -10,7 +10,7 @@
  * Conventions
  *  - Return value: TSG_OK (0) or an error class mirroring the CLI exit codes
  *    of SPEC.md:587: 1 parse (ParseError), 2 config (ConfigError or
- *    std::invalid_argument), 3 sim (SimError, CUDA, NCCL).  The message of the
+ *    std::invalid_argument), 3 sim (SimError, CUDA).  The message of the
  *    last failure on the calling thread is tsg_last_error().  C++ exceptions
  *    never cross this boundary.
  *  - Matrices: 2 * 4^k doubles, interleaved (re, im), row-major, index bit j
