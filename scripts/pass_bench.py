@@ -88,6 +88,9 @@ cases = {
     "1x gen ks5 smem": [([5, 6, 7, 8, 9], "dense")],
     "1x gen ks3": [([6, 7, 8], "dense")],
     "1x gen ks3 low": [([1, 2, 3], "dense")],
+    "2x ks5 dense": [([5, 6, 7, 8, 9], "dense"), ([7, 8, 9, 10, 11], "dense")],
+    "ks5+ks4 dense": [([5, 6, 7, 8, 9], "dense"), ([7, 8, 9, 10], "dense")],
+    "3x gen ks4 smem": [([5, 6, 7, 8], "dense"), ([7, 8, 9, 10], "dense"), ([5, 6, 9, 10], "dense")],
     "4x gen ks4 smem": [([5, 6, 7, 8], "dense"), ([7, 8, 9, 10], "dense"), ([5, 6, 9, 10], "dense"), ([6, 7, 8, 9], "dense")],
     "4x perm ks2": [([6, 7], "perm"), ([8, 9], "perm"), ([1, 7], "perm"), ([2, 9], "perm")],
     "4x perm ks4": [([0, 1, 9, 10], "perm"), ([2, 3, 7, 8], "perm"), ([0, 2, 9, 7], "perm"), ([5, 6, 7, 8], "perm")],
