@@ -415,8 +415,9 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   // Two CTAs per SM beat deeper pipelines (measured): 3 stages when two CTAs
   // still fit in shared memory, else 2.
   const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(Real);
-  size_t fixed = 128;  // (6-qubit geometries serve k_stream_umma, which sizes its own shared memory)
+  size_t fixed = 128;  // (complex64 6-qubit geometries serve k_stream_umma, which sizes its own shared memory)
   if constexpr (KS <= 5) fixed += simt ? dmma_m_smem_bytes<Real, KS, true>() : dmma_m_smem_bytes<Real, KS>();
+  if constexpr (KS == 6 && sizeof(Real) == 8) fixed += dmma_m_smem_bytes<Real, KS>();
   const size_t per_cta = 110 * 1024;
   *stages = 3 * stage + fixed <= per_cta ? 3 : 2;
   *smem = *stages * stage + fixed;
@@ -444,7 +445,8 @@ void launch_dmma_pick(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s
   if constexpr (sizeof(Real) == 4 && KS <= 3) {
     if (simt) return launch_dmma<Real, KS, STAGES, false, true>(p, smem, s, num_sms);  // SIMT evaluates densely
   }
-  launch_dmma<Real, KS, STAGES, SP, false>(p, smem, s, num_sms);
+  if constexpr (KS >= 6) launch_dmma<Real, KS, STAGES, false, false>(p, smem, s, num_sms);
+  else launch_dmma<Real, KS, STAGES, SP, false>(p, smem, s, num_sms);
 }
 
 template <typename Real, int KS>
@@ -464,7 +466,7 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   const bool simt = sizeof(Real) == 4 && KS <= 3 && lowest >= 5;
   constexpr int D = S::D;
   for (int rb = 0; rb < S::RB; ++rb)
-    for (int k = 0; k < S::KST; ++k) {
+    for (int k = 0; k < S::KST && KS <= 5; ++k) {  // (ks = 6: dense only)
       bool nzr = false, nzi = false, nzs = false;
       for (int r = 8 * rb; r < 8 * rb + 8; ++r)
         for (int c = 4 * k; c < 4 * k + 4; ++c) {
@@ -485,12 +487,12 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   const int n_dmma_tiles = 3 * S::RB * S::KST;
   const int nonzero = __builtin_popcount(p.nzblk[0]) + __builtin_popcount(p.nzblk[1]) + __builtin_popcount(p.nzblk[2]);
   static const bool any_zero_rule = std::getenv("TSG_DMMA_SPARSE_ANY") != nullptr;  // round-1 rule (A/B runs)
-  bool sparse = any_zero_rule ? nonzero < n_dmma_tiles : 4 * (n_dmma_tiles - nonzero) >= n_dmma_tiles;
+  bool sparse = KS <= 5 && (any_zero_rule ? nonzero < n_dmma_tiles : 4 * (n_dmma_tiles - nonzero) >= n_dmma_tiles);
   static const int force_sparse = [] {  // experiments: TSG_DMMA_SPARSE=0|1 forces the variant
     const char* e = std::getenv("TSG_DMMA_SPARSE");
     return e ? std::atoi(e) : -1;
   }();
-  if (force_sparse >= 0) sparse = force_sparse == 1;
+  if (force_sparse >= 0 && KS <= 5) sparse = force_sparse == 1;
   const int most = std::max({__builtin_popcount(p.nzblk[0]), __builtin_popcount(p.nzblk[1]), __builtin_popcount(p.nzblk[2])});
   if (!dmma_geometry<Real, KS>(g, p, &smem, &stages, simt, 2 * most <= S::RB * S::KST)) return false;
   p.re = static_cast<Real*>(g.re);
@@ -703,6 +705,7 @@ bool launch_stream_if(const GateLaunch& g, cudaStream_t s, int num_sms) {
       case 3: return direct ? try_dmma_direct<3>(g, s, num_sms) : try_dmma<double, 3>(g, s, num_sms);
       case 4: return direct ? try_dmma_direct<4>(g, s, num_sms) : try_dmma<double, 4>(g, s, num_sms);
       case 5: return direct ? try_dmma_direct<5>(g, s, num_sms) : try_dmma<double, 5>(g, s, num_sms);
+      case 6: return try_dmma<double, 6>(g, s, num_sms);
       default: return false;
     }
   } else {
@@ -797,6 +800,11 @@ bool dmma_fits(const GateLaunch& g) {
       DmmaParams<Real, 5> p{};
       return dmma_geometry<Real, 5>(g, p, &smem, &stages, false);
     }
+    case 6: {
+      if constexpr (sizeof(Real) != 8) return false;
+      DmmaParams<Real, 6> p{};
+      return dmma_geometry<Real, 6>(g, p, &smem, &stages, false);
+    }
     default:
       return false;
   }
@@ -810,8 +818,9 @@ std::string kernel_name_impl(const GateLaunch& g) {
   if (klass == 0) return "none";
   if (klass == 1 && g.ks > kMaxSub) return "k_diag_wide" + ks + ">";
   if ((klass == 2 || klass == 3) && sizeof(Real) == 4 && umma_takes(g)) return "k_stream_umma" + ks + ">";
-  if (g.full_range && (klass == 2 || klass == 3) && g.ks >= 3 && g.ks <= 5 && g.dev_mat) {
-    if (dmma_mode() == 1 && sizeof(Real) == 8) return "k_dmma_direct" + ks + ">";
+  if (g.full_range && (klass == 2 || klass == 3) && g.ks >= 3 && (g.ks <= 5 || (g.ks == 6 && sizeof(Real) == 8)) &&
+      g.dev_mat) {
+    if (dmma_mode() == 1 && sizeof(Real) == 8 && g.ks <= 5) return "k_dmma_direct" + ks + ">";
     if (dmma_fits<Real>(g)) return "k_stream_dmma" + ks + ">";
   }
   if (klass == 1 && !g.full_range) klass = g.ks <= DM ? 2 : 3;

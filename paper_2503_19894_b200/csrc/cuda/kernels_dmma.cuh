@@ -1,4 +1,4 @@
-// k_stream_dmma: complex128 sub-gates of 3..5 qubits on the FP64 tensor pipe.
+// k_stream_dmma: complex128 sub-gates of 3..6 qubits on the FP64 tensor pipe.
 //
 // Same tile pipeline as k_stream (kernels_stream.cuh: runs of 2^L contiguous
 // amplitudes, cp.async.bulk global<->shared, mbarrier stages, persistent CTAs)
@@ -72,10 +72,17 @@ struct DmmaShape {
 #ifndef TSG_D5_NRB
 #define TSG_D5_NRB 4
 #endif
+// complex128 6-qubit products: 2048-amplitude tiles (32 groups), 2 n-blocks
+// per warp, so 16 consumer warps share the SM's one CTA (the M fragments take
+// 96 KB of shared memory)
+#ifndef TSG_D6_NRB
+#define TSG_D6_NRB 2
+#endif
 template <typename Real, int KS>
 using DShape = DmmaShape<KS, sizeof(Real) == 8 ? (KS == 5 ? TSG_D5_AMPS : 11) : 12,
-                         (sizeof(Real) == 8 && KS == 5) ? TSG_D5_NRB
-                                                        : ((KS >= 5 || (sizeof(Real) == 4 && KS >= 4)) ? 4 : 8)>;
+                         (sizeof(Real) == 8 && KS == 5)   ? TSG_D5_NRB
+                         : (sizeof(Real) == 8 && KS == 6) ? TSG_D6_NRB
+                                                          : ((KS >= 5 || (sizeof(Real) == 4 && KS >= 4)) ? 4 : 8)>;
 
 // Real = storage type of the state (double: complex128, float: complex64);
 // the product always runs in FP64 on the DMMA pipe (complex64 amplitudes are
@@ -139,9 +146,11 @@ __device__ __forceinline__ uint32_t dmma_pad(const DmmaParams<Real, KS>& p, uint
   return (w >> p.chunk_log2) * p.chunk_stride + (w & ((1u << p.chunk_log2) - 1));
 }
 
-// M fragments live in registers for ks <= 4; for ks = 5 they are staged in
+// M fragments live in registers for ks <= 4; for ks = 5, 6 they are staged in
 // shared memory in fragment order ([3][KST][RB][32 lanes], conflict-free
-// LDS.64) so the consumer warps fit 2 CTAs per SM.
+// LDS.64): 24 KB for ks = 5 (the consumer warps fit 2 CTAs per SM), 96 KB for
+// ks = 6 (one CTA per SM).  ks = 6 runs dense only: its 128 tiles per matrix
+// do not fit nzblk's 32-bit masks.
 template <int KS>
 __host__ __device__ constexpr bool dmma_m_in_regs() {
   return KS <= 4;
@@ -154,7 +163,7 @@ __host__ __device__ constexpr bool dmma_m_in_regs() {
 template <typename Real, int KS, bool SIMT = false>
 __host__ __device__ constexpr size_t dmma_m_smem_bytes() {
   if (SIMT) return size_t{8} << (2 * KS);
-  return dmma_m_in_regs<KS>() ? 0 : size_t{3} * DmmaShape<KS>::KST * DmmaShape<KS>::RB * 32 * sizeof(double);
+  return dmma_m_in_regs<KS>() ? 0 : size_t{3} * ((1 << KS) / 4) * ((1 << KS) / 8) * 32 * sizeof(double);
 }
 
 template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT = false>

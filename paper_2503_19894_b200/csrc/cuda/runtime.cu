@@ -1099,6 +1099,18 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
       bool fits = true;
       for (int p : mixed[i]) fits = fits && g.reg_bit(p) >= 0;
       if (!fits) {
+        if (std::getenv("TSG_PASS_DEBUG")) {
+          const std::vector<int> Pn = choose_layout(mixed[i], upcoming(i + 1), g.r, M, L);
+          int m = 0, in_lane = 0;
+          for (int p : Pn)
+            if (g.reg_bit(p) < 0) {
+              ++m;
+              const int tb = g.thread_bit(p);
+              in_lane += tb >= 0 && tb < 5;
+            }
+          const bool regs_current = !ops.empty() && ops.back().kind != tsg::kPassSGen && ops.back().kind != tsg::kPassSPerm;
+          std::fprintf(stderr, "  layout change m=%d lanes=%d regs=%d\n", m, in_lane, regs_current ? 1 : 0);
+        }
         g.P = choose_layout(mixed[i], upcoming(i + 1), g.r, M, L);
         ops.push_back(build_layout_op<Real>(g, data));
       }
