@@ -174,6 +174,10 @@ typedef struct tsg_step_info {
 } tsg_step_info;
 int tsg_program_step_count(const tsg_program* prog, uint64_t* out);
 int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* out);
+/* B200 addition: a tile-pass step's register layouts -- loaded through shared
+ * memory, or reached from the previous one with warp shuffles (register <->
+ * lane swaps); both 0 for other steps */
+int tsg_program_pass_layouts(const tsg_program* prog, uint64_t i, int* smem_layouts, int* shuffle_layouts);
 
 /* --------------------------------------------------- circuit IR (host) ---
  * C exports of the kept C++ surface (include/tilesim/ir.hpp, fusion.hpp). */

@@ -149,6 +149,7 @@ _sig("tsg_program_run_profiled", [_vp, _vp, _dp, C.POINTER(RunReport)])
 _sig("tsg_program_gate_info", [_vp, _u64, C.POINTER(PlanInfo)])
 _sig("tsg_program_step_count", [_vp, C.POINTER(_u64)])
 _sig("tsg_program_step_info", [_vp, _u64, C.POINTER(StepInfo)])
+_sig("tsg_program_pass_layouts", [_vp, _u64, C.POINTER(C.c_int), C.POINTER(C.c_int)])
 _sig("tsc_plan_passes", [_vp, C.c_int, C.c_double, C.c_double, _ip, _ip, _ip, C.POINTER(_u64)])
 _sig("tsg_ctx_info", [_vp, _ip, _ip])
 _sig("tsg_bench_cost_model", [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _u64, C.POINTER(_vp)])
@@ -598,6 +599,18 @@ class Program:
             _check(_lib.tsg_program_step_info(self._h, i, C.byref(si)))
             out.append({"kind": STEP_KINDS[si.kind], "first_gate": si.first_gate, "n_gates": si.n_gates,
                         "high": list(si.high[:si.n_high]), "kernel": si.kernel.decode()})
+        return out
+
+    def pass_layouts(self) -> list:
+        """Per step: (register layouts loaded through shared memory, layouts reached
+        with warp shuffles) -- (0, 0) for steps that are not tile passes."""
+        cnt = _u64()
+        _check(_lib.tsg_program_step_count(self._h, C.byref(cnt)))
+        out = []
+        for i in range(cnt.value):
+            a, b = C.c_int(), C.c_int()
+            _check(_lib.tsg_program_pass_layouts(self._h, i, C.byref(a), C.byref(b)))
+            out.append((a.value, b.value))
         return out
 
     def gate_info(self, i: int) -> dict:

@@ -165,7 +165,11 @@ struct PassOp {  // 192 bytes, built on the host, read from shared memory
   int32_t n_xmask;
   int32_t thr_off;  // RGen / RPerm: per-thread u8 table (block bits from thread positions, 0xff: thread
                     // controls inactive), -1 when the op has neither
-  uint8_t reserved[28];
+  // LAYOUT in registers (warp shuffles): the new layout swaps register bit
+  // swap_k[s] with lane bit swap_l[s], s < n_swap (0: through shared memory)
+  int32_t n_swap;
+  uint8_t swap_k[4], swap_l[4];
+  uint8_t reserved[16];
 };
 static_assert(sizeof(PassOp) == 192, "PassOp layout");
 

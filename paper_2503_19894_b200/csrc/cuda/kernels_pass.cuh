@@ -660,6 +660,42 @@ __device__ __forceinline__ void smem_to_regs(const Real* xr, const Real* xi, con
   }
 }
 
+// Layout change in registers: register bit K trades places with lane bit l
+// (warp shuffles, no shared memory, no barrier).  For each register pair
+// {i, i | 2^K} a thread keeps the element whose bit K equals its own lane
+// bit; the other one comes from its partner lane (lane ^ 2^l), which sends
+// its element with bit K equal to the receiver's lane bit: one shuffle per
+// pair and array, the data moved unchanged (bit-identical to the
+// shared-memory change).
+template <int K, typename Real, int R>
+__device__ __forceinline__ void shfl_swap_bit(Real (&ar)[R], Real (&ai)[R], int l, int lane) {
+  const bool lb = (lane >> l) & 1;
+  const int mask = 1 << l;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    if (i & (1 << K)) continue;  // compile time
+    const int j = i | (1 << K);
+    const Real sr = lb ? ar[i] : ar[j], si = lb ? ai[i] : ai[j];
+    const Real rr = __shfl_xor_sync(0xffffffffu, sr, mask), ri = __shfl_xor_sync(0xffffffffu, si, mask);
+    if (lb) {
+      ar[i] = rr;
+      ai[i] = ri;
+    } else {
+      ar[j] = rr;
+      ai[j] = ri;
+    }
+  }
+}
+
+template <typename Real, int R>
+__device__ __forceinline__ void shfl_swap(Real (&ar)[R], Real (&ai)[R], int k, int l, int lane) {
+  constexpr int kBits = cx_ctz(R);
+  if constexpr (kBits > 0) if (k == 0) return shfl_swap_bit<0>(ar, ai, l, lane);
+  if constexpr (kBits > 1) if (k == 1) return shfl_swap_bit<1>(ar, ai, l, lane);
+  if constexpr (kBits > 2) if (k == 2) return shfl_swap_bit<2>(ar, ai, l, lane);
+  if constexpr (kBits > 3) if (k == 3) return shfl_swap_bit<3>(ar, ai, l, lane);
+}
+
 // Per-thread interpreter state of one tile: the registers of the current
 // layout, their shared-memory offsets, and what carries across ops.
 template <typename Real, int R>
@@ -686,7 +722,12 @@ __device__ __forceinline__ int pass_step(const PassOp* ops, int o, int n_ops, co
   const PassOp& op = ops[o];
   const int kind = op.kind;
   if (kind == kPassLayout) {
-    if (!rg.in_smem) {
+    if (op.n_swap > 0 && !rg.in_smem) {
+      // register <-> lane bit swaps within each warp; the new layout's
+      // shared-memory offsets (for a later store) from its table as below
+      TSG_JIT_UNROLL
+      for (int q = 0; q < op.n_swap; ++q) shfl_swap<Real, R>(rg.ar, rg.ai, op.swap_k[q], op.swap_l[q], tid & 31);
+    } else if (!rg.in_smem) {
       regs_to_smem<Real, R>(xr, xi, rg.at, rg.ar, rg.ai, rg.vb);
       consumer_bar();  // the tile is in shared memory in full
     } else if (o > 0) {
@@ -707,7 +748,7 @@ __device__ __forceinline__ int pass_step(const PassOp* ops, int o, int n_ops, co
       rg.at[i] = a;
     }
     rg.vb = op.ks;  // vector width of this layout (host: lowest register positions = lowest tile positions)
-    smem_to_regs<Real, R>(xr, xi, rg.at, rg.ar, rg.ai, rg.vb);
+    if (op.n_swap == 0 || rg.in_smem) smem_to_regs<Real, R>(xr, xi, rg.at, rg.ar, rg.ai, rg.vb);
     rg.in_smem = false;
     return o + 1;
   }

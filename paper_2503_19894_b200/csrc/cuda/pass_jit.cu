@@ -197,7 +197,11 @@ void emit_op(std::ostringstream& os, const PassOp& op) {
   arr(op.tb_pos, 8);
   os << ',';
   arr(op.tb_jbit, 8);
-  os << ',' << op.n_tb << ',' << op.n_xmask << ',' << op.thr_off << ",{}}";
+  os << ',' << op.n_tb << ',' << op.n_xmask << ',' << op.thr_off << ',' << op.n_swap << ',';
+  arr(op.swap_k, 4);
+  os << ',';
+  arr(op.swap_l, 4);
+  os << ",{}}";
 }
 
 // indices of the ops the interpreter visits (a RUN consumes its groups,

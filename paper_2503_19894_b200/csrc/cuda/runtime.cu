@@ -219,6 +219,8 @@ struct ProgramPass {
   tsg::PassLaunch launch;  // re/im/blob filled per run
   size_t blob_offset = 0;  // into the device arena
   std::vector<int> gates;
+  int layouts_smem = 0;     // register layouts loaded through shared memory
+  int layouts_shuffle = 0;  // ... reached with warp shuffles
 };
 
 // A run of qubit-permutation gates as one qubit permutation of the state:
@@ -605,15 +607,35 @@ tsg::PassOp blank_op(int kind) {
   return op;
 }
 
+// Shared-memory wavefronts of one register <-> tile move of a warp whose
+// lanes sit on tile positions lanes[0..4] (scalar moves; 8-byte elements
+// take at least 2)
 template <typename Real>
-tsg::PassOp build_layout_op(PassGeom& g, std::vector<unsigned char>& data) {
+int layout_wavefronts(const int* lanes, int L) {
+  int words[32] = {0}, worst = 0;
+  for (uint32_t l = 0; l < 32; ++l) {
+    uint32_t x = 0;
+    for (int b = 0; b < 5; ++b) x |= ((l >> b) & 1u) << lanes[b];
+    const uint32_t w = static_cast<uint32_t>(padded_offset<Real>(x, L)) * (sizeof(Real) / 4);
+    for (uint32_t k = 0; k < sizeof(Real) / 4; ++k) worst = std::max(worst, ++words[(w + k) % 32]);
+  }
+  return worst;
+}
+
+// LAYOUT op for g.P / g.tpos as set by the caller (tpos: thread-id bit ->
+// tile position, lanes first).  n_swap > 0: the kernel reaches it from the
+// previous layout with register <-> lane swaps (warp shuffles).
+template <typename Real>
+tsg::PassOp build_layout_op(PassGeom& g, std::vector<unsigned char>& data, int n_swap = 0, const int* swap_k = nullptr,
+                            const int* swap_l = nullptr) {
   tsg::PassOp op = blank_op(tsg::kPassLayout);
   if (g.r + 1 > 6) throw SimError("pass: too many register positions");
-  std::vector<int> free_pos;
-  for (int p = 0; p < g.M; ++p)
-    if (g.reg_bit(p) < 0) free_pos.push_back(p);
-  if (static_cast<int>(free_pos.size()) != tsg::kPassLogThreads) throw SimError("pass: thread positions");
-  g.tpos = free_pos;  // ascending: lanes on the lowest free positions
+  if (static_cast<int>(g.tpos.size()) != tsg::kPassLogThreads) throw SimError("pass: thread positions");
+  op.n_swap = n_swap;
+  for (int q = 0; q < n_swap; ++q) {
+    op.swap_k[q] = static_cast<uint8_t>(swap_k[q]);
+    op.swap_l[q] = static_cast<uint8_t>(swap_l[q]);
+  }
   // per-thread tile coordinate of the thread part, looked up instead of
   // recomputed every tile
   pad16(data);
@@ -632,7 +654,95 @@ tsg::PassOp build_layout_op(PassGeom& g, std::vector<unsigned char>& data) {
   int vb = 0;
   while (vb < vmax && vb < g.r && g.P[vb] == vb) ++vb;
   op.ks = vb;
+  if (std::getenv("TSG_PASS_DEBUG")) {
+    std::fprintf(stderr, "  layout%s P={", n_swap ? " (shuffles)" : "");
+    for (int p : g.P) std::fprintf(stderr, " %d", p);
+    std::fprintf(stderr, " } lanes={");
+    for (int b = 0; b < 5; ++b) std::fprintf(stderr, " %d", g.tpos[b]);
+    std::fprintf(stderr, " } warps={");
+    for (int b = 5; b < tsg::kPassLogThreads; ++b) std::fprintf(stderr, " %d", g.tpos[b]);
+    std::fprintf(stderr, " } wavefronts/move %d\n", layout_wavefronts<Real>(g.tpos.data(), g.L));
+  }
   return op;
+}
+
+// Thread positions for a layout loaded through shared memory with register
+// positions P: 5 lanes + 3 warp positions out of the others.  A warp owns
+// the amplitudes its lanes and registers span, so a later layout whose
+// register positions avoid the warp positions is reached with warp shuffles
+// (register <-> lane swaps: no shared-memory round trip, no barrier).  The
+// lanes then drift onto other positions, and a later store of the registers
+// (the end of the tile, a shared-memory op, the next shared-memory layout)
+// pays the bank conflicts of where they are.  Cost model in shared-memory
+// wavefronts per warp: moving the R registers of both arrays once costs
+// 2 R wf (wf: wavefronts of one warp access, layout_wavefronts), a barrier
+// ~32, a shuffle change of m bits 1.5 m R (8-byte elements twice that: one
+// SHFL per 32-bit word and pair member).  Picks the warp positions and the
+// number of the following register-current layouts (`next`) to reach with
+// shuffles that save the most against the default (lanes on the lowest
+// free positions, every change through shared memory); *n_shuffle = 0 and
+// the default when nothing is saved.
+template <typename Real>
+std::vector<int> pick_thread_positions(const PassGeom& g, const std::vector<int>& P,
+                                       const std::vector<std::vector<int>>& next, int* n_shuffle) {
+  *n_shuffle = 0;
+  std::vector<int> free_pos;
+  for (int p = 0; p < g.M; ++p)
+    if (std::find(P.begin(), P.end(), p) == P.end()) free_pos.push_back(p);
+  if (static_cast<int>(free_pos.size()) != tsg::kPassLogThreads) throw SimError("pass: thread positions");
+  std::vector<int> best = free_pos;  // lanes on the lowest free positions
+  const char* shfl_env = std::getenv("TSG_PASS_SHFL");  // "0": every layout through shared memory
+  if ((shfl_env && std::string(shfl_env) == "0") || next.empty()) return best;
+  const int R = 1 << g.r;
+  const double words = sizeof(Real) / 4;
+  const int wf_min = layout_wavefronts<Real>(best.data(), g.L);
+  const double smem_change = 2.0 * R * 2 * wf_min + 32.0;  // store + load at the best banks, barrier
+  double best_gain = 0.0;
+  const int nf = static_cast<int>(free_pos.size());
+  for (int a = 0; a < nf; ++a)
+    for (int b = a + 1; b < nf; ++b)
+      for (int c = b + 1; c < nf; ++c) {
+        const int W[3] = {free_pos[a], free_pos[b], free_pos[c]};
+        auto in_w = [&](int p) { return p == W[0] || p == W[1] || p == W[2]; };
+        std::vector<int> lanes;
+        for (int p : free_pos)
+          if (!in_w(p)) lanes.push_back(p);
+        std::vector<int> cur = P;
+        double gain = -2.0 * R * (layout_wavefronts<Real>(lanes.data(), g.L) - wf_min);  // this load
+        double best_here = -1e30;
+        int best_len = 0;
+        for (int j = 0; j <= static_cast<int>(next.size()); ++j) {
+          // stop after j shuffle changes: the next store sees these lanes
+          const double total = gain - 2.0 * R * (layout_wavefronts<Real>(lanes.data(), g.L) - wf_min);
+          if (total > best_here) {
+            best_here = total;
+            best_len = j;
+          }
+          if (j == static_cast<int>(next.size())) break;
+          const std::vector<int>& Pn = next[j];
+          bool ok = true;
+          for (int p : Pn) ok = ok && !in_w(p);
+          if (!ok) break;
+          std::vector<int> out, in;
+          for (int p : cur)
+            if (std::find(Pn.begin(), Pn.end(), p) == Pn.end()) out.push_back(p);
+          for (int p : Pn)
+            if (std::find(cur.begin(), cur.end(), p) == cur.end()) in.push_back(p);
+          if (in.size() > 4) break;
+          for (size_t q = 0; q < in.size(); ++q) *std::find(lanes.begin(), lanes.end(), in[q]) = out[q];
+          cur = Pn;
+          gain += smem_change - 1.5 * static_cast<double>(in.size()) * R * words;
+        }
+        if (best_len > 0 && best_here > best_gain) {
+          best_gain = best_here;
+          *n_shuffle = best_len;
+          best = lanes.empty() ? best : std::vector<int>();
+          for (int p : free_pos)
+            if (!in_w(p)) best.push_back(p);
+          best.insert(best.end(), W, W + 3);
+        }
+      }
+  return best;
 }
 
 // out-of-tile controls into cout, the rest returned as (tile position, value)
@@ -1007,15 +1117,83 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
     return u;
   };
 
-  std::vector<tsg::PassOp> ops;
-  std::vector<unsigned char> data;
+  // The register layouts the op loop below will set, in order (layout 0 is
+  // the first load from shared memory), and whether the registers hold the
+  // tile when each later one is needed (not right after a shared-memory op)
+  // -- the thread positions of a shared-memory layout are picked so that
+  // the following register-current ones can be reached with warp shuffles.
+  std::vector<std::vector<int>> lay_P;
+  std::vector<bool> lay_regs;
   {
     size_t first = 0;
     while (first < ng && !reg_ok[first]) ++first;
-    g.P = first < ng ? choose_layout(mixed[first], upcoming(first + 1), g.r, M, L)
-                     : choose_layout({}, {}, g.r, M, L);
-    ops.push_back(build_layout_op<Real>(g, data));
+    lay_P.push_back(first < ng ? choose_layout(mixed[first], upcoming(first + 1), g.r, M, L)
+                               : choose_layout({}, {}, g.r, M, L));
+    lay_regs.push_back(false);
+    bool after_smem = false, pending_diag = false;
+    for (size_t i = 0; i < ng; ++i) {
+      const LaunchStructure& ls = prog->gates[step.gates[i]].ls;
+      if (ls.klass == KernelClass::Diagonal) {
+        pending_diag = true;
+        continue;
+      }
+      if (pending_diag) after_smem = false;  // a RUN in between: the kernel reloaded the registers
+      pending_diag = false;
+      if (reg_ok[i]) {
+        bool fits = true;
+        for (int p : mixed[i]) fits = fits && std::find(lay_P.back().begin(), lay_P.back().end(), p) != lay_P.back().end();
+        if (!fits) {
+          lay_P.push_back(choose_layout(mixed[i], upcoming(i + 1), g.r, M, L));
+          lay_regs.push_back(!after_smem);
+        }
+        after_smem = false;
+      } else {
+        after_smem = true;
+      }
+    }
   }
+  size_t lay = 0;      // next layout
+  int shuffle_left = 0;  // following layouts the current thread positions plan to reach with shuffles
+  // the layouts after `e` that could follow it with shuffles (registers current)
+  auto shuffle_chain = [&](size_t e) {
+    std::vector<std::vector<int>> nx;
+    for (size_t f = e + 1; f < lay_P.size() && lay_regs[f]; ++f) nx.push_back(lay_P[f]);
+    return nx;
+  };
+  std::vector<tsg::PassOp> ops;
+  std::vector<unsigned char> data;
+  auto set_layout = [&](bool regs_current) {
+    const std::vector<int>& Pn = lay_P[lay];
+    if (regs_current && shuffle_left > 0) {
+      // register positions that leave / enter; shuffles when every entering
+      // one is a lane position now
+      std::vector<int> out, in;
+      for (int p : g.P)
+        if (std::find(Pn.begin(), Pn.end(), p) == Pn.end()) out.push_back(p);
+      for (int p : Pn)
+        if (g.reg_bit(p) < 0) in.push_back(p);
+      bool lanes = in.size() <= 4;
+      for (int p : in) lanes = lanes && g.thread_bit(p) >= 0 && g.thread_bit(p) < 5;
+      if (lanes && !in.empty()) {
+        int sk[4], sl[4];
+        for (size_t q = 0; q < in.size(); ++q) {
+          sk[q] = g.reg_bit(out[q]);
+          sl[q] = g.thread_bit(in[q]);
+          g.P[sk[q]] = in[q];
+          g.tpos[sl[q]] = out[q];
+        }
+        ops.push_back(build_layout_op<Real>(g, data, static_cast<int>(in.size()), sk, sl));
+        ++lay;
+        --shuffle_left;
+        return;
+      }
+    }
+    g.P = Pn;
+    g.tpos = pick_thread_positions<Real>(g, g.P, shuffle_chain(lay), &shuffle_left);
+    ops.push_back(build_layout_op<Real>(g, data));
+    ++lay;
+  };
+  set_layout(false);
   std::vector<const LaunchStructure*> run;  // the open run of diagonal gates
   auto flush_run = [&]() {
     if (run.empty()) return;
@@ -1099,20 +1277,12 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
       bool fits = true;
       for (int p : mixed[i]) fits = fits && g.reg_bit(p) >= 0;
       if (!fits) {
-        if (std::getenv("TSG_PASS_DEBUG")) {
-          const std::vector<int> Pn = choose_layout(mixed[i], upcoming(i + 1), g.r, M, L);
-          int m = 0, in_lane = 0;
-          for (int p : Pn)
-            if (g.reg_bit(p) < 0) {
-              ++m;
-              const int tb = g.thread_bit(p);
-              in_lane += tb >= 0 && tb < 5;
-            }
-          const bool regs_current = !ops.empty() && ops.back().kind != tsg::kPassSGen && ops.back().kind != tsg::kPassSPerm;
-          std::fprintf(stderr, "  layout change m=%d lanes=%d regs=%d\n", m, in_lane, regs_current ? 1 : 0);
-        }
-        g.P = choose_layout(mixed[i], upcoming(i + 1), g.r, M, L);
-        ops.push_back(build_layout_op<Real>(g, data));
+        bool planned = lay < lay_P.size();
+        for (int p : mixed[i])
+          planned = planned && std::find(lay_P[lay].begin(), lay_P[lay].end(), p) != lay_P[lay].end();
+        if (!planned) throw SimError("pass: layout plan out of step");
+        const bool regs_current = !ops.empty() && ops.back().kind != tsg::kPassSGen && ops.back().kind != tsg::kPassSPerm;
+        set_layout(regs_current);
       }
       ops.push_back(build_reg_op<Real>(ls, g, data));
     } else {
@@ -1157,6 +1327,8 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
 
   ProgramPass pp;
   pp.gates = step.gates;
+  for (const tsg::PassOp& op : ops)
+    if (op.kind == tsg::kPassLayout) ++(op.n_swap > 0 ? pp.layouts_shuffle : pp.layouts_smem);
   tsg::PassLaunch& pl = pp.launch;
   pl.n = n;
   pl.tile_log2 = M;
@@ -2028,6 +2200,19 @@ int tsg_program_step_count(const tsg_program* prog, uint64_t* out) {
     require(prog && out, "null argument");
     *out = prog->steps.size();
   })
+}
+
+int tsg_program_pass_layouts(const tsg_program* prog, uint64_t i, int* smem_layouts, int* shuffle_layouts) {
+  TSG_TRY({
+    require(prog && smem_layouts && shuffle_layouts, "null argument");
+    require(i < prog->steps.size(), "step index out of range");
+    const ProgramStep& st = prog->steps[i];
+    *smem_layouts = *shuffle_layouts = 0;
+    if (st.kind == kStepPass) {
+      *smem_layouts = prog->passes[st.index].layouts_smem;
+      *shuffle_layouts = prog->passes[st.index].layouts_shuffle;
+    }
+  });
 }
 
 int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* out) {

@@ -1,11 +1,13 @@
 """Dense 6-qubit gates at n = 30 on several target sets (device time per
 gate, median of 6): complex128 on k_stream_dmma<ks=6> (or k_tile with
 TSG_NO_DMMA6=1 in the environment of a build that honours it), complex64 on
-k_stream_umma<ks=6>.  usage: d6_bench.py [f64|f32]"""
+k_stream_umma<ks=6>.  usage: d6_bench.py [f64|f32] [VARIANT_ROOT]"""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if len(sys.argv) > 2:  # a variant build's root (scripts/build_variant.sh)
+    sys.path.insert(0, sys.argv[2])
 import paper_2503_19894_b200 as ts  # noqa: E402
 from tests._util import random_gate_matrix  # noqa: E402
 

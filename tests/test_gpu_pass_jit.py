@@ -53,3 +53,38 @@ def test_precompile_warms_the_cache(tmp_path, monkeypatch):
     assert n > 0 and len(list(tmp_path.glob("*.cubin"))) >= 1
     prog = ts.Program(fused, "f64")
     assert sum(s["kernel"] == "k_pass_jit" for s in prog.steps()) == n
+
+
+@pytest.mark.parametrize("kind,n,depth,kmax,prec", [("qft", 18, 1, 5, "f64"), ("hes", 16, 4, 5, "f32"),
+                                                    ("rqc", 16, 8, 5, "f64"), ("qaoa", 16, 4, 5, "f32")])
+def test_shuffle_layouts(kind, n, depth, kmax, prec, monkeypatch):
+    """Register layouts reached with warp shuffles (register <-> lane swaps)
+    against every layout through shared memory (TSG_PASS_SHFL=0), the
+    interpreter against the JIT with shuffles, and the oracle."""
+    monkeypatch.setenv("TSG_PASS_FORCE", "1")
+    monkeypatch.setenv("TSG_PASS_JIT_MIN_N", "1")
+    fused, _ = ts.run_fusion(ts.gen_benchmark(kind, n, depth, 3), ts.FusionConfig(k_max=kmax))
+    ps = ts.Program(fused, prec)
+    monkeypatch.setenv("TSG_PASS_JIT", "0")
+    pi = ts.Program(fused, prec)
+    monkeypatch.setenv("TSG_PASS_SHFL", "0")
+    p0 = ts.Program(fused, prec)
+    lay_s, lay_0 = ps.pass_layouts(), p0.pass_layouts()
+    assert sum(b for _, b in lay_s) > 0, lay_s  # some layouts are shuffles
+    assert sum(b for _, b in lay_0) == 0
+    # same layouts in all: a shuffle replaces a shared-memory change one for one
+    assert [a + b for a, b in lay_s] == [a + b for a, b in lay_0]
+    a = ts.Statevector(n, prec).init_random(8)
+    b = ts.Statevector(n, prec).copy_from(a)
+    c = ts.Statevector(n, prec).copy_from(a)
+    re0, im0 = a.download()
+    ps.run(a)
+    pi.run(b)
+    p0.run(c)
+    assert ts.compare_states(a, b) == 0.0  # JIT == interpreter, both with shuffles
+    bar = 1e-12 if prec == "f64" else 1e-6  # thread positions change the order of diagonal factors only
+    assert ts.compare_states(a, c) <= bar
+    dt = np.float64 if prec == "f64" else np.float32
+    ore, oim = re0.astype(dt), im0.astype(dt)
+    ob.run_circuit(to_oracle(fused), ore, oim, threads=4)
+    assert ts.compare_states(a, (ore.astype(np.float64), oim.astype(np.float64))) <= (1e-10 if prec == "f64" else 1e-5)
