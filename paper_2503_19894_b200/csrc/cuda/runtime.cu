@@ -666,6 +666,36 @@ tsg::PassOp build_layout_op(PassGeom& g, std::vector<unsigned char>& data, int n
   return op;
 }
 
+// Shared-memory cost (wavefronts per warp) of moving a layout's registers
+// of both arrays once, as regs_to_smem / smem_to_regs do: complex64 layouts
+// whose lowest register positions are tile positions 0, 1 move 2^vb
+// registers per 16-byte-or-narrower vector access (build_layout_op's vb).
+template <typename Real>
+double layout_move_cost(const std::vector<int>& P, const int* lanes, int L) {
+  const int R = 1 << static_cast<int>(P.size());
+  int vb = 0;
+  if (sizeof(Real) == 4)
+    while (vb < 2 && vb < static_cast<int>(P.size()) && P[vb] == vb) ++vb;
+  const uint32_t words = (sizeof(Real) / 4) << vb;  // 32-bit words per lane access
+  int cnt[32] = {0}, worst = 0;
+  for (uint32_t l = 0; l < 32; ++l) {
+    uint32_t x = 0;
+    for (int b = 0; b < 5; ++b) x |= ((l >> b) & 1u) << lanes[b];
+    const uint32_t w = static_cast<uint32_t>(padded_offset<Real>(x, L)) * (sizeof(Real) / 4);
+    for (uint32_t k = 0; k < words; ++k) worst = std::max(worst, ++cnt[(w + k) % 32]);
+  }
+  return 2.0 * (R >> vb) * worst;
+}
+
+// Widest layout change done with shuffles: complex64 changes of two and more
+// bits measured slower than the shared-memory round trip (HES-30's block
+// pass 25.1 -> 27.0 ms; the selects around each SHFL cost issue slots),
+// complex128 one- and two-bit changes faster (QFT-30 73.5 -> 72.3 ms).
+template <typename Real>
+constexpr int shuffle_max_bits() {
+  return sizeof(Real) == 8 ? 2 : 1;
+}
+
 // Thread positions for a layout loaded through shared memory with register
 // positions P: 5 lanes + 3 warp positions out of the others.  A warp owns
 // the amplitudes its lanes and registers span, so a later layout whose
@@ -674,29 +704,36 @@ tsg::PassOp build_layout_op(PassGeom& g, std::vector<unsigned char>& data, int n
 // lanes then drift onto other positions, and a later store of the registers
 // (the end of the tile, a shared-memory op, the next shared-memory layout)
 // pays the bank conflicts of where they are.  Cost model in shared-memory
-// wavefronts per warp: moving the R registers of both arrays once costs
-// 2 R wf (wf: wavefronts of one warp access, layout_wavefronts), a barrier
-// ~32, a shuffle change of m bits 1.5 m R (8-byte elements twice that: one
-// SHFL per 32-bit word and pair member).  Picks the warp positions and the
-// number of the following register-current layouts (`next`) to reach with
-// shuffles that save the most against the default (lanes on the lowest
-// free positions, every change through shared memory); *n_shuffle = 0 and
-// the default when nothing is saved.
+// wavefronts per warp (layout_move_cost; a barrier ~32; a shuffle change of
+// m bits 3 m R per 32-bit word of an element: a SHFL and the selects around
+// it per pair member, issue slots rather than wavefronts -- measured: two-
+// and three-bit changes of complex64 layouts ran slower than the shared-memory
+// round trip they replaced): this load, the shuffles and the store after the last of
+// them, against the default (sorted registers, lanes on the lowest free
+// positions, every change a store and a load through shared memory).  Picks the warp
+// positions and the number of the following register-current layouts
+// (`next`) to reach with shuffles that save the most; *n_shuffle = 0 and the
+// default when nothing is saved.  The simulated swaps are set_layout's.
 template <typename Real>
 std::vector<int> pick_thread_positions(const PassGeom& g, const std::vector<int>& P,
                                        const std::vector<std::vector<int>>& next, int* n_shuffle) {
   *n_shuffle = 0;
-  std::vector<int> free_pos;
-  for (int p = 0; p < g.M; ++p)
-    if (std::find(P.begin(), P.end(), p) == P.end()) free_pos.push_back(p);
+  auto default_lanes = [&](const std::vector<int>& regs) {
+    std::vector<int> f;
+    for (int p = 0; p < g.M; ++p)
+      if (std::find(regs.begin(), regs.end(), p) == regs.end()) f.push_back(p);
+    return f;
+  };
+  const std::vector<int> free_pos = default_lanes(P);
   if (static_cast<int>(free_pos.size()) != tsg::kPassLogThreads) throw SimError("pass: thread positions");
   std::vector<int> best = free_pos;  // lanes on the lowest free positions
   const char* shfl_env = std::getenv("TSG_PASS_SHFL");  // "0": every layout through shared memory
   if ((shfl_env && std::string(shfl_env) == "0") || next.empty()) return best;
-  const int R = 1 << g.r;
-  const double words = sizeof(Real) / 4;
-  const int wf_min = layout_wavefronts<Real>(best.data(), g.L);
-  const double smem_change = 2.0 * R * 2 * wf_min + 32.0;  // store + load at the best banks, barrier
+  auto default_cost = [&](std::vector<int> regs) {
+    std::sort(regs.begin(), regs.end());
+    return layout_move_cost<Real>(regs, default_lanes(regs).data(), g.L);
+  };
+  const double R = static_cast<double>(1 << g.r), words = sizeof(Real) / 4;
   double best_gain = 0.0;
   const int nf = static_cast<int>(free_pos.size());
   for (int a = 0; a < nf; ++a)
@@ -708,12 +745,13 @@ std::vector<int> pick_thread_positions(const PassGeom& g, const std::vector<int>
         for (int p : free_pos)
           if (!in_w(p)) lanes.push_back(p);
         std::vector<int> cur = P;
-        double gain = -2.0 * R * (layout_wavefronts<Real>(lanes.data(), g.L) - wf_min);  // this load
+        // this load against the default one
+        double gain = default_cost(cur) - layout_move_cost<Real>(cur, lanes.data(), g.L);
         double best_here = -1e30;
         int best_len = 0;
         for (int j = 0; j <= static_cast<int>(next.size()); ++j) {
           // stop after j shuffle changes: the next store sees these lanes
-          const double total = gain - 2.0 * R * (layout_wavefronts<Real>(lanes.data(), g.L) - wf_min);
+          const double total = gain - (layout_move_cost<Real>(cur, lanes.data(), g.L) - default_cost(cur));
           if (total > best_here) {
             best_here = total;
             best_len = j;
@@ -728,15 +766,18 @@ std::vector<int> pick_thread_positions(const PassGeom& g, const std::vector<int>
             if (std::find(Pn.begin(), Pn.end(), p) == Pn.end()) out.push_back(p);
           for (int p : Pn)
             if (std::find(cur.begin(), cur.end(), p) == cur.end()) in.push_back(p);
-          if (in.size() > 4) break;
-          for (size_t q = 0; q < in.size(); ++q) *std::find(lanes.begin(), lanes.end(), in[q]) = out[q];
-          cur = Pn;
-          gain += smem_change - 1.5 * static_cast<double>(in.size()) * R * words;
+          if (static_cast<int>(in.size()) > shuffle_max_bits<Real>()) break;
+          // the shared-memory change it replaces (default layouts on both sides)
+          gain += default_cost(cur) + default_cost(Pn) + 32.0 - 3.0 * static_cast<double>(in.size()) * R * words;
+          for (size_t q = 0; q < in.size(); ++q) {
+            *std::find(lanes.begin(), lanes.end(), in[q]) = out[q];
+            *std::find(cur.begin(), cur.end(), out[q]) = in[q];
+          }
         }
         if (best_len > 0 && best_here > best_gain) {
           best_gain = best_here;
           *n_shuffle = best_len;
-          best = lanes.empty() ? best : std::vector<int>();
+          best.clear();
           for (int p : free_pos)
             if (!in_w(p)) best.push_back(p);
           best.insert(best.end(), W, W + 3);
@@ -936,7 +977,14 @@ void append_blocks(const LaunchStructure& ls, const BlockForm& f, std::vector<un
 // RGen / RPerm: every mixed qubit is a register position of the layout
 template <typename Real>
 tsg::PassOp build_reg_op(const LaunchStructure& ls, const PassGeom& g, std::vector<unsigned char>& data) {
-  const BlockForm f = block_form(ls);
+  BlockForm f = block_form(ls);
+  // the kernel's block element index takes the mixed register bits in
+  // ascending register order (reg_gen: deposit into rmask); after shuffle
+  // changes the register positions need not ascend with the qubits, so the
+  // blocks are laid out in that order
+  std::stable_sort(f.ebits.begin(), f.ebits.end(), [&](int a, int b) {
+    return g.reg_bit(g.pos[ls.sub_targets[a]]) < g.reg_bit(g.pos[ls.sub_targets[b]]);
+  });
   tsg::PassOp op = blank_op(f.perm ? tsg::kPassRPerm : tsg::kPassRGen);
   op.ks = f.ke;
   for (int b : f.ebits) {
@@ -1172,7 +1220,7 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
         if (std::find(Pn.begin(), Pn.end(), p) == Pn.end()) out.push_back(p);
       for (int p : Pn)
         if (g.reg_bit(p) < 0) in.push_back(p);
-      bool lanes = in.size() <= 4;
+      bool lanes = static_cast<int>(in.size()) <= shuffle_max_bits<Real>();
       for (int p : in) lanes = lanes && g.thread_bit(p) >= 0 && g.thread_bit(p) < 5;
       if (lanes && !in.empty()) {
         int sk[4], sl[4];

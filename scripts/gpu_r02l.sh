@@ -1,0 +1,15 @@
+#!/bin/bash
+# shuffle layouts (capped width): tests, A/B; ks6 DMMA NRB A/B; fusion sweep with ks6 DMMA
+cd ${GRAFT_REPO_ROOT:-.}
+O=gpurun_out/r02l; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_pass_jit.py tests/test_pass.py tests/test_gpu_fuzz.py -q -x -p no:cacheprovider > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+for c in "qft 30 5 f64" "qaoa 30 5 f32 4" "hes 30 5 f32 6"; do
+  f=$(echo $c | tr ' ' '_')
+  timeout 600 python scripts/prof_pass.py $c > "$O/steps_$f.txt" 2>&1
+  TSG_PASS_SHFL=0 timeout 600 python scripts/prof_pass.py $c > "$O/steps_${f}_noshfl.txt" 2>&1
+done
+bash scripts/ab_bench.sh "TSG_PASS_SHFL=0" "TSG_PASS_SHFL=1" > $O/ab.txt 2>&1
+timeout 300 python scripts/d6_bench.py f64 > $O/d6_nrb2.txt 2>&1
+timeout 300 python scripts/d6_bench.py f64 abvar/d6nrb4 > $O/d6_nrb4.txt 2>&1
+timeout 2400 python scripts/calibrate.py --out $O --tag _r02 > $O/calibrate.log 2>&1
+echo done

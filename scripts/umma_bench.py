@@ -4,6 +4,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("PB_ROOT"):  # a variant build (A/B)
+    sys.path.insert(0, os.environ["PB_ROOT"])
 import paper_2503_19894_b200 as ts  # noqa: E402
 from tests._util import random_gate_matrix  # noqa: E402
 
