@@ -19,11 +19,21 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2503_19894_b200 as ts  # noqa: E402
 
 
+def model_threads(cm):
+    """The threads axis value the device bench recorded (its SM count)."""
+    for line in cm.serialize().splitlines():
+        for tok in line.split():
+            if tok.startswith("threads="):
+                return int(tok.split("=")[1])
+    return 1
+
+
 def predicted(cm, fused, n):
     tot = 0.0
+    threads = model_threads(cm)
     for g in fused.gates():
         kp = ts.KernelPlan(g, n)
-        tot += cm.estimate(g.k, kp.info()["op_count"], 1, n)
+        tot += cm.estimate(g.k, kp.info()["op_count"], threads, n)
     return tot
 
 
@@ -54,9 +64,12 @@ def main():
         cm = models[prec]
         sv = ts.Statevector(n, prec).init_zero()
         configs = [(f"size-only k={k}", ts.FusionConfig(k_max=k)) for k in range(1, 7)]
-        configs += [("adaptive k_max=5", ts.FusionConfig(k_max=5, mode="adaptive")),
-                    ("adaptive k_max=6", ts.FusionConfig(k_max=6, mode="adaptive")),
-                    ("paper-cpu (adaptive k7 cap4096)", ts.FusionConfig.paper_cpu())]
+        th = model_threads(cm)  # the device bench's threads axis (its SM count)
+        pc = ts.FusionConfig.paper_cpu()
+        pc.threads = th
+        configs += [("adaptive k_max=5", ts.FusionConfig(k_max=5, mode="adaptive", threads=th)),
+                    ("adaptive k_max=6", ts.FusionConfig(k_max=6, mode="adaptive", threads=th)),
+                    ("paper-cpu (adaptive k7 cap4096)", pc)]
         for name, cfg in configs:
             try:
                 fused, st = ts.run_fusion(c, cfg, cm)
