@@ -467,7 +467,8 @@ def run_ours(args):
         cpu = cpu_baseline(n, args.kmax, args.cpu_seconds)
 
     # auxiliary (not the headline), device seconds, median of 3 after warm-up:
-    #   BASELINE.json configs[2]: QAOA-30 (p = 4) complex64, fusion k <= 5
+    #   BASELINE.json configs[2]: QAOA-30 (p = 4) complex64, fusion k <= 5, and
+    #                             its size-only fusion sweep k = 1..6
     #   SURVEY §8(d) C2b dense class: ALA-30 (depth 20, seed 42) complex128, k <= 5
     #   configs[0] / C1: QFT-20 complex128, fusion k <= 3, against the CPU oracle
     #                    run in full on this host (parity and CPU seconds)
@@ -486,6 +487,17 @@ def run_ours(args):
         aux["qaoa30_c64_k5"] = {"seconds": dev_seconds(pqa, sq32),
                                 "gates": f"{sqa['original_gate_count']}->{sqa['fused_block_count']}",
                                 "steps": len(pqa.steps())}
+        # configs[2]'s fusion sweep k = 1..6 (size-only) on the same circuit: the
+        # tile passes take the small-k gate streams, so the best k is not the widest
+        sweep = {}
+        for k in range(1, 7):
+            qk, sqk = ts.run_fusion(ts.gen_benchmark("qaoa", n, 4, 7), ts.FusionConfig(k_max=k))
+            pk = ts.Program(qk, "f32", ctx=ctx)
+            sweep[f"k={k}"] = {"seconds": dev_seconds(pk, sq32), "gates": sqk["fused_block_count"],
+                               "steps": len(pk.steps())}
+            del pk
+        best = min(sweep, key=lambda kk: sweep[kk]["seconds"])
+        aux["qaoa30_c64_sweep"] = dict(sweep, best=best)
         del pqa, sq32
         al, sal = ts.run_fusion(ts.gen_benchmark("ala", n, 20, 42), ts.FusionConfig(k_max=args.kmax))
         pal = ts.Program(al, "f64", ctx=ctx)
