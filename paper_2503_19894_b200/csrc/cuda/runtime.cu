@@ -1372,6 +1372,7 @@ ProgramPass build_pass(const tsg_program* prog, const PassStep& step, const Pass
   blob.insert(blob.end(), data.begin(), data.end());
   pad16(blob);
   if (blob.size() > static_cast<size_t>(tsg::kPassMaxBlob)) throw SimError("pass: blob exceeds shared-memory budget");
+  if (std::getenv("TSG_PASS_DEBUG")) std::fprintf(stderr, "  blob %zu bytes, %zu ops\n", blob.size(), ops.size());
 
   ProgramPass pp;
   pp.gates = step.gates;

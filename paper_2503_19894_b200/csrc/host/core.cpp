@@ -282,15 +282,33 @@ Gate fuse_matrices(const Gate& first, const Gate& second, int hard_cap) {
   GateMatrix out(m);
   const GateMatrix& F = first.matrix;
   const GateMatrix& S = second.matrix;
+  // per-row / per-column local indices once (the product loop below keeps
+  // the reference's accumulation order: w ascending, real and imaginary
+  // sums separately -- bit-exact)
+  const uint64_t dF = F.dim(), dS = S.dim();
+  // (fused blocks are small: stack tables up to 6 qubits)
+  uint64_t tab_small[4 * 64];
+  std::vector<uint64_t> tab_big(dim > 64 ? 4 * dim : 0);
+  uint64_t* const tab = dim > 64 ? tab_big.data() : tab_small;
+  uint64_t *srow = tab, *frow = tab + dim, *fcol = tab + 2 * dim, *scol = tab + 3 * dim;
+  for (uint64_t x = 0; x < dim; ++x) {
+    srow[x] = extract(x, spos.data(), ks) * dS;
+    frow[x] = extract(x, fpos.data(), kf) & f_only_local;
+    fcol[x] = extract(x, fpos.data(), kf);
+    scol[x] = extract(x, spos.data(), ks) & s_only_local;
+  }
+  for (uint64_t w = 0; w < nw; ++w) wf[w] *= dF;  // row offsets in F
+  const cplx* fe = &F.at(0, 0);
+  const cplx* se = &S.at(0, 0);
   for (uint64_t r = 0; r < dim; ++r) {
-    const uint64_t srow = extract(r, spos.data(), ks);
-    const uint64_t frow = extract(r, fpos.data(), kf) & f_only_local;
+    const cplx* srow_p = se + srow[r];
+    const cplx* frow_p = fe + frow[r] * dF;
     for (uint64_t c = 0; c < dim; ++c) {
-      const uint64_t fcol = extract(c, fpos.data(), kf);
-      const uint64_t scol = extract(c, spos.data(), ks) & s_only_local;
+      const cplx* sp = srow_p + scol[c];
+      const cplx* fp = frow_p + fcol[c];
       double acc_re = 0.0, acc_im = 0.0;
       for (uint64_t w = 0; w < nw; ++w) {
-        const cplx p = mul(S.at(srow, scol | ws[w]), F.at(frow | wf[w], fcol));
+        const cplx p = mul(sp[ws[w]], fp[wf[w]]);
         acc_re += p.real();
         acc_im += p.imag();
       }
