@@ -353,26 +353,6 @@ std::vector<unsigned char> tile_matrix_bytes(const LaunchStructure& ls, const ts
   return out;
 }
 
-// Nonzero 8 x 4 tiles of [Mr | Mi | Mr + Mi] (the DMMA kernels skip the
-// others) with rows / columns in element order P.
-int dmma_tiles(const LaunchStructure& ls, const int* P) {
-  const int D = 1 << ls.ks;
-  int tiles = 0;
-  for (int m = 0; m < 3; ++m)
-    for (int rb = 0; rb < D / 8; ++rb)
-      for (int k = 0; k < D / 4; ++k) {
-        bool nz = false;
-        for (int r = 8 * rb; r < 8 * rb + 8 && !nz; ++r)
-          for (int c = 4 * k; c < 4 * k + 4 && !nz; ++c) {
-            const size_t e = static_cast<size_t>(P[r]) * D + P[c];
-            const double v = m == 0 ? ls.sub_re[e] : (m == 1 ? ls.sub_im[e] : ls.sub_re[e] + ls.sub_im[e]);
-            nz = v != 0.0;
-          }
-        tiles += nz;
-      }
-  return tiles;
-}
-
 // Element order of a launch: identity, except for full-range sub-gates of
 // 3..5 qubits (the DMMA stream kernels), which take the qubit order with the
 // fewest nonzero DMMA tiles (<= 5! orders; ties keep the sorted order).
@@ -383,16 +363,46 @@ void choose_dmma_perm(tsg::GateLaunch& g, const LaunchStructure& ls) {
   if (!g.full_range || (g.klass != 2 && g.klass != 3) || g.ks < 3 || g.ks > 5) return;
   static const bool disabled = std::getenv("TSG_NO_DMMA_PERM") != nullptr;
   if (disabled) return;
+  // nonzero pattern of [Mr | Mi | Mr + Mi] as one column bitmask per row
+  // (D <= 32); a tile (row block rb, k-step k) of an element order P is
+  // nonzero when a row P[r] of the block has a nonzero among the columns
+  // P[4k .. 4k+3] -- the count dmma_tiles takes, from masks
+  uint32_t nz[3][32] = {};
+  bool dense = true;
+  for (int r = 0; r < D; ++r)
+    for (int c = 0; c < D; ++c) {
+      const size_t e = static_cast<size_t>(r) * D + c;
+      const double v[3] = {ls.sub_re[e], ls.sub_im[e], ls.sub_re[e] + ls.sub_im[e]};
+      for (int m = 0; m < 3; ++m) {
+        nz[m][r] |= static_cast<uint32_t>(v[m] != 0.0) << c;
+        dense = dense && v[m] != 0.0;
+      }
+    }
+  if (dense) return;  // every order has every tile nonzero
+  auto tiles = [&](const int* P, int bound) {
+    int t = 0;
+    for (int k = 0; k < D / 4; ++k) {
+      const uint32_t cols = (1u << P[4 * k]) | (1u << P[4 * k + 1]) | (1u << P[4 * k + 2]) | (1u << P[4 * k + 3]);
+      for (int m = 0; m < 3; ++m)
+        for (int rb = 0; rb < D / 8; ++rb) {
+          bool any = false;
+          for (int r = 8 * rb; r < 8 * rb + 8 && !any; ++r) any = (nz[m][P[r]] & cols) != 0;
+          t += any;
+        }
+      if (t >= bound) return t;  // cannot beat the best so far
+    }
+    return t;
+  };
   int bits[5] = {0, 1, 2, 3, 4}, P[32], best[32];
   for (int j = 0; j < D; ++j) best[j] = j;
-  int best_tiles = dmma_tiles(ls, best);
+  int best_tiles = tiles(best, 1 << 30);
   do {
     for (int j = 0; j < D; ++j) {
       int x = 0;
       for (int b = 0; b < g.ks; ++b) x |= ((j >> b) & 1) << bits[b];
       P[j] = x;
     }
-    const int t = dmma_tiles(ls, P);
+    const int t = tiles(P, best_tiles);
     if (t < best_tiles) {
       best_tiles = t;
       std::copy(P, P + D, best);
