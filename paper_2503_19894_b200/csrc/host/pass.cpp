@@ -258,24 +258,75 @@ bool qubit_permutation(const LaunchStructure& ls, std::vector<int>* sigma) {
   return true;
 }
 
+// Qubits a gate touches and the ones it mixes (as bit masks), for the
+// commutation test of the lookahead planner: two gates commute when every
+// qubit they share is a block (non-mixed) qubit of both -- for each value of
+// the shared qubits the two act on disjoint qubits.  Exact for the snapped
+// matrices the kernels apply (mixed_bits uses the same structural zeros).
+struct GateQubits {
+  uint64_t all = 0, mix = 0;
+};
+static GateQubits gate_qubits(const LaunchStructure& ls) {
+  GateQubits q;
+  for (int t : ls.sub_targets) q.all |= uint64_t{1} << t;
+  for (int c : ls.controls) q.all |= uint64_t{1} << c;
+  if (ls.klass != KernelClass::Diagonal && ls.klass != KernelClass::Identity)
+    for (int b : mixed_bits(ls)) q.mix |= uint64_t{1} << ls.sub_targets[b];
+  return q;
+}
+
 std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int n, const PassConfig& cfg) {
   std::vector<PassStep> steps;
   const int L = cfg.run_log2, M = cfg.tile_log2;
   const int hmax = M - L;
   const bool passes_possible = n >= M;
   const int run_table = 8 << hmax;
+  const int G = static_cast<int>(gates.size());
 
-  std::vector<int> cur;      // gates of the open pass
-  std::vector<int> cur_high; // mixed qubits >= L of the open pass
-  int cur_bytes = run_table + 4 * 1024;  // room for a few LAYOUT records + per-thread tables (1 KiB each)
+  // per gate: pass role, mixed qubits at or above L, blob bytes, qubit masks
+  std::vector<PassRole> role(G, PassRole::Standalone);
+  std::vector<std::vector<int>> mixed_hi(G);
+  std::vector<int> bytes(G, 0);
+  std::vector<GateQubits> qb(G);
+  std::vector<char> perm(G, 0);  // in a run of >= min_permute_run consecutive qubit permutations
+  for (int i = 0; i < G; ++i) {
+    const LaunchStructure& ls = gates[i];
+    if (ls.klass == KernelClass::Identity) continue;
+    qb[i] = gate_qubits(ls);
+    perm[i] = passes_possible && cfg.min_permute_run > 0 && qubit_permutation(ls, nullptr);
+    PassRole r = passes_possible ? pass_role(ls, cfg) : PassRole::Standalone;
+    if (r != PassRole::Standalone && !cfg.force && pass_op_sweeps(ls, cfg) >= standalone_sweeps(ls, cfg))
+      r = PassRole::Standalone;  // cheaper on its own kernel
+    role[i] = r;
+    if (r == PassRole::Gen)
+      for (int b : mixed_bits(ls))
+        if (ls.sub_targets[b] >= L) mixed_hi[i].push_back(ls.sub_targets[b]);
+    bytes[i] = r == PassRole::Standalone ? 0 : pass_op_bytes(ls, cfg);
+  }
+  for (int i = 0; i < G;) {  // keep only the permutations inside long enough runs (identities ignored)
+    if (!perm[i]) {
+      ++i;
+      continue;
+    }
+    std::vector<int> run;
+    int j = i;
+    for (; j < G; ++j) {
+      if (gates[j].klass == KernelClass::Identity) continue;
+      if (!perm[j]) break;
+      run.push_back(j);
+    }
+    if (static_cast<int>(run.size()) < cfg.min_permute_run)
+      for (int g : run) perm[g] = 0;
+    i = j;
+  }
 
   auto emit_standalone = [&](int g) {
     PassStep s;
     s.gates.push_back(g);
     steps.push_back(std::move(s));
   };
-  auto flush = [&]() {
-    if (cur.empty()) return;
+  // a finished pass: kept when it beats launching its gates one by one
+  auto emit_pass = [&](const std::vector<int>& cur, const std::vector<int>& cur_high) {
     double alone = 0.0, inside = cfg.base_sweeps;
     for (int g : cur) {
       alone += standalone_sweeps(gates[g], cfg);
@@ -294,62 +345,80 @@ std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int
     } else {
       for (int g : cur) emit_standalone(g);
     }
-    cur.clear();
-    cur_high.clear();
-    cur_bytes = run_table + 4 * 1024;
   };
 
-  for (int i = 0; i < static_cast<int>(gates.size()); ++i) {
-    const LaunchStructure& ls = gates[i];
-    if (ls.klass == KernelClass::Identity) continue;
-    if (passes_possible && cfg.min_permute_run > 0 && qubit_permutation(ls, nullptr)) {
+  // Lookahead (commutation-aware) grouping: a pass opened at the first
+  // remaining gate takes later gates that fit it AND commute with every gate
+  // passed over so far (those keep their order and come later); gates that
+  // do not fit, standalone gates and permutations are passed over.  Gates of
+  // a pass keep program order among themselves.  TSG_PASS_LOOKAHEAD=<window>
+  // (0: the in-order greedy planner).
+  static const int window = [] {
+    const char* e = std::getenv("TSG_PASS_LOOKAHEAD");
+    return e ? std::max(0, std::atoi(e)) : 256;
+  }();
+  std::vector<char> done(G, 0);
+  for (int i = 0; i < G; ++i) done[i] = gates[i].klass == KernelClass::Identity;
+  int head = 0;
+  while (true) {
+    while (head < G && done[head]) ++head;
+    if (head >= G) break;
+    const int i = head;
+    if (perm[i]) {
       // a run of consecutive qubit permutations (identity gates in between ignored)
       std::vector<int> run;
       int j = i;
-      for (; j < static_cast<int>(gates.size()); ++j) {
-        if (gates[j].klass == KernelClass::Identity) continue;
-        if (!qubit_permutation(gates[j], nullptr)) break;
+      for (; j < G; ++j) {
+        if (done[j]) continue;
+        if (!perm[j]) break;
         run.push_back(j);
       }
-      if (static_cast<int>(run.size()) >= cfg.min_permute_run) {
-        flush();
-        PassStep s;
-        s.is_permute = true;
-        s.gates = std::move(run);
-        steps.push_back(std::move(s));
-        i = j - 1;
-        continue;
-      }
-    }
-    PassRole role = passes_possible ? pass_role(ls, cfg) : PassRole::Standalone;
-    if (role != PassRole::Standalone && !cfg.force && pass_op_sweeps(ls, cfg) >= standalone_sweeps(ls, cfg))
-      role = PassRole::Standalone;  // cheaper on its own kernel
-    if (role == PassRole::Standalone) {
-      flush();
-      emit_standalone(i);
+      PassStep s;
+      s.is_permute = true;
+      s.gates = run;
+      for (int g : run) done[g] = 1;
+      steps.push_back(std::move(s));
       continue;
     }
-    std::vector<int> mixed;  // qubits the gate mixes (must be tile qubits)
-    if (role == PassRole::Gen)
-      for (int b : mixed_bits(ls)) mixed.push_back(ls.sub_targets[b]);
-    std::vector<int> need = cur_high;
-    for (int q : mixed)
-      if (q >= L && std::find(need.begin(), need.end(), q) == need.end()) need.push_back(q);
-    const int bytes = pass_op_bytes(ls, cfg);
-    // ops + RUN headers must stay within kPassMaxOps (128): at most 2 records per gate
-    const bool fits = static_cast<int>(need.size()) <= hmax && 2 * (static_cast<int>(cur.size()) + 1) <= 128 &&
-                      static_cast<int>(cur.size()) < cfg.max_ops && cur_bytes + bytes <= cfg.max_blob;
-    if (!fits) {
-      flush();
-      need.clear();
-      for (int q : mixed)
-        if (q >= L) need.push_back(q);
+    if (role[i] == PassRole::Standalone) {
+      emit_standalone(i);
+      done[i] = 1;
+      continue;
     }
-    cur.push_back(i);
-    cur_high = need;
-    cur_bytes += bytes;
+    std::vector<int> cur{i};
+    std::vector<int> cur_high = mixed_hi[i];
+    int cur_bytes = run_table + 4 * 1024 + bytes[i];  // room for a few LAYOUT records + per-thread tables
+    done[i] = 1;
+    uint64_t skip_all = 0, skip_mix = 0;  // qubits of the gates passed over / the qubits they mix
+    int scanned = 0;
+    for (int j = i + 1; j < G && scanned < (window > 0 ? window : 1 << 30); ++j) {
+      if (done[j]) continue;
+      ++scanned;
+      bool take = role[j] != PassRole::Standalone && !perm[j] && (qb[j].all & skip_mix) == 0 &&
+                  (qb[j].mix & skip_all) == 0;
+      std::vector<int> need;
+      if (take) {
+        need = cur_high;
+        for (int q : mixed_hi[j])
+          if (std::find(need.begin(), need.end(), q) == need.end()) need.push_back(q);
+        // ops + RUN headers must stay within kPassMaxOps (128): at most 2 records per gate
+        take = static_cast<int>(need.size()) <= hmax && 2 * (static_cast<int>(cur.size()) + 1) <= 128 &&
+               static_cast<int>(cur.size()) < cfg.max_ops && cur_bytes + bytes[j] <= cfg.max_blob;
+      }
+      if (take) {
+        cur.push_back(j);
+        cur_high = need;
+        cur_bytes += bytes[j];
+        done[j] = 1;
+      } else {
+        if (window == 0) break;  // in-order greedy: the pass ends at the first gate it cannot take
+        skip_all |= qb[j].all;
+        skip_mix |= qb[j].mix;
+        if (skip_mix == (n >= 64 ? ~uint64_t{0} : (uint64_t{1} << n) - 1)) break;  // nothing can commute past
+      }
+    }
+    emit_pass(cur, cur_high);
   }
-  flush();
   return steps;
 }
 
