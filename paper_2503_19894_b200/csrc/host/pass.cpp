@@ -275,7 +275,8 @@ static GateQubits gate_qubits(const LaunchStructure& ls) {
   return q;
 }
 
-std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int n, const PassConfig& cfg) {
+static std::vector<PassStep> plan_passes_window(const std::vector<LaunchStructure>& gates, int n,
+                                                const PassConfig& cfg, int window) {
   std::vector<PassStep> steps;
   const int L = cfg.run_log2, M = cfg.tile_log2;
   const int hmax = M - L;
@@ -351,12 +352,8 @@ std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int
   // remaining gate takes later gates that fit it AND commute with every gate
   // passed over so far (those keep their order and come later); gates that
   // do not fit, standalone gates and permutations are passed over.  Gates of
-  // a pass keep program order among themselves.  TSG_PASS_LOOKAHEAD=<window>
-  // (0: the in-order greedy planner).
-  static const int window = [] {
-    const char* e = std::getenv("TSG_PASS_LOOKAHEAD");
-    return e ? std::max(0, std::atoi(e)) : 256;
-  }();
+  // a pass keep program order among themselves.  window 0: the in-order
+  // greedy planner (a pass ends at the first gate it cannot take).
   std::vector<char> done(G, 0);
   for (int i = 0; i < G; ++i) done[i] = gates[i].klass == KernelClass::Identity;
   int head = 0;
@@ -420,6 +417,40 @@ std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int
     emit_pass(cur, cur_high);
   }
   return steps;
+}
+
+// Estimated sweeps of a plan with the planner's own cost model.
+static double plan_sweeps(const std::vector<PassStep>& steps, const std::vector<LaunchStructure>& gates,
+                          const PassConfig& cfg) {
+  double t = 0.0;
+  for (const PassStep& s : steps) {
+    if (s.is_permute) {
+      t += 1.0;
+    } else if (s.is_pass) {
+      t += cfg.base_sweeps;
+      for (int g : s.gates) t += pass_op_sweeps(gates[g], cfg);
+    } else {
+      t += standalone_sweeps(gates[s.gates.front()], cfg);
+    }
+  }
+  return t;
+}
+
+// Both planners; the lookahead plan is taken when the cost model says it
+// saves at least a third of a sweep (B200: RQC-30 k <= 2 57 -> 35 sweeps,
+// 551 -> 452 ms; QAOA-30 c64 k = 1 71 -> 31, 310 -> 243 ms), else the
+// in-order plan -- on equal sweep counts the hoisted gates made QFT-30's
+// passes ~3% slower (profiles/r02/planner_ab.txt).  TSG_PASS_LOOKAHEAD=<window>
+// sets the window (default 256; 0: in-order only).
+std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int n, const PassConfig& cfg) {
+  static const int window = [] {
+    const char* e = std::getenv("TSG_PASS_LOOKAHEAD");
+    return e ? std::max(0, std::atoi(e)) : 256;
+  }();
+  std::vector<PassStep> in_order = plan_passes_window(gates, n, cfg, 0);
+  if (window == 0 || cfg.force) return in_order;
+  std::vector<PassStep> ahead = plan_passes_window(gates, n, cfg, window);
+  return plan_sweeps(ahead, gates, cfg) + 0.34 <= plan_sweeps(in_order, gates, cfg) ? ahead : in_order;
 }
 
 }  // namespace tilesim
