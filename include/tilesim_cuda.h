@@ -178,6 +178,10 @@ int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* ou
  * memory, or reached from the previous one with warp shuffles (register <->
  * lane swaps); both 0 for other steps */
 int tsg_program_pass_layouts(const tsg_program* prog, uint64_t i, int* smem_layouts, int* shuffle_layouts);
+/* B200 addition: how many of the program's tile passes run JIT-compiled
+ * kernels (NVRTC, op table compiled in) and how many standalone launches run
+ * a JIT-compiled DMMA product (zero 8x4 tiles compiled out) */
+int tsg_program_jit_kernels(const tsg_program* prog, int* jit_passes, int* jit_gate_launches);
 
 /* --------------------------------------------------- circuit IR (host) ---
  * C exports of the kept C++ surface (include/tilesim/ir.hpp, fusion.hpp). */

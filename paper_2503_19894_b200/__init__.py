@@ -150,6 +150,7 @@ _sig("tsg_program_gate_info", [_vp, _u64, C.POINTER(PlanInfo)])
 _sig("tsg_program_step_count", [_vp, C.POINTER(_u64)])
 _sig("tsg_program_step_info", [_vp, _u64, C.POINTER(StepInfo)])
 _sig("tsg_program_pass_layouts", [_vp, _u64, C.POINTER(C.c_int), C.POINTER(C.c_int)])
+_sig("tsg_program_jit_kernels", [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)])
 _sig("tsc_plan_passes", [_vp, C.c_int, C.c_double, C.c_double, _ip, _ip, _ip, C.POINTER(_u64)])
 _sig("tsg_ctx_info", [_vp, _ip, _ip])
 _sig("tsg_bench_cost_model", [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _u64, C.POINTER(_vp)])
@@ -612,6 +613,13 @@ class Program:
             _check(_lib.tsg_program_pass_layouts(self._h, i, C.byref(a), C.byref(b)))
             out.append((a.value, b.value))
         return out
+
+    def jit_kernels(self) -> dict:
+        """JIT-compiled kernels the program runs: {"passes": tile passes, "gates":
+        standalone launches with a JIT DMMA product}."""
+        a, b = C.c_int(), C.c_int()
+        _check(_lib.tsg_program_jit_kernels(self._h, C.byref(a), C.byref(b)))
+        return {"passes": a.value, "gates": b.value}
 
     def gate_info(self, i: int) -> dict:
         pi = PlanInfo()

@@ -1,7 +1,29 @@
 // complex128 instantiations of the gate kernels (see kernels*.cuh).
 #include "apply_impl.cuh"
+#include "pass_jit.hpp"
 
 namespace tsg {
+namespace {
+template <int KS>
+bool dmma_jit_spec_ks(const GateLaunch& g, std::string* source, std::string* name) {
+  DmmaSetup<double, KS> st;
+  if (!dmma_setup<double, KS>(g, st)) return false;
+  if (st.nonzero == 3 * DShape<double, KS>::RB * DShape<double, KS>::KST) return false;  // dense: nothing to compile in
+  *source = dmma_jit_source(KS, st.stages, st.p.nzblk, name);
+  return true;
+}
+}  // namespace
+
+bool dmma_jit_spec(const GateLaunch& g, std::string* source, std::string* name) {
+  if (!g.full_range || (g.klass != 2 && g.klass != 3) || !g.m_re || dmma_mode() == 1) return false;
+  switch (g.ks) {
+    case 3: return dmma_jit_spec_ks<3>(g, source, name);
+    case 4: return dmma_jit_spec_ks<4>(g, source, name);
+    case 5: return dmma_jit_spec_ks<5>(g, source, name);
+    default: return false;
+  }
+}
+
 int launch_gate_f64(const GateLaunch& g, cudaStream_t s, int num_sms) { return launch_gate_impl<double>(g, s, num_sms); }
 int launch_diag_batch_f64(const DiagBatchLaunch& b, cudaStream_t s, int num_sms) {
   return launch_diag_batch_impl<double>(b, s, num_sms);

@@ -449,21 +449,29 @@ void launch_dmma_pick(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s
   else launch_dmma<Real, KS, STAGES, SP, false>(p, smem, s, num_sms);
 }
 
+// Host half of a k_stream_dmma launch: nonzero tile masks, variant,
+// geometry (no device pointers needed).
 template <typename Real, int KS>
-bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
-  using S = DShape<Real, KS>;
-  if (!g.dev_mat) return false;
+struct DmmaSetup {
   DmmaParams<Real, KS> p;
-  std::memset(&p, 0, sizeof p);
   size_t smem = 0;
   int stages = 3;
+  bool simt = false, sparse = false;
+  int nonzero = 0;  // nonzero 8 x 4 tiles of [Mr | Mi | Ms]
+};
+
+template <typename Real, int KS>
+bool dmma_setup(const GateLaunch& g, DmmaSetup<Real, KS>& st) {
+  using S = DShape<Real, KS>;
+  DmmaParams<Real, KS>& p = st.p;
+  std::memset(&p, 0, sizeof p);
   // complex64, 3 qubits, every target and control at bit 5 or above: FP32
   // SIMT consumer (measured faster there; slower than the FP64-widened DMMA
   // product for 4-5 qubits and for low targets -- scripts/pass_bench.py)
   int lowest = 64;
   for (int b = 0; b < g.ks; ++b) lowest = std::min(lowest, g.sub_targets[b]);
   for (int c = 0; c < g.n_ctrl; ++c) lowest = std::min(lowest, g.ctrl[c]);
-  const bool simt = sizeof(Real) == 4 && KS <= 3 && lowest >= 5;
+  st.simt = sizeof(Real) == 4 && KS <= 3 && lowest >= 5;
   constexpr int D = S::D;
   for (int rb = 0; rb < S::RB; ++rb)
     for (int k = 0; k < S::KST && KS <= 5; ++k) {  // (ks = 6: dense only)
@@ -483,34 +491,67 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   // The sparse variant (per-tile predicates) pays only when it skips at least
   // a quarter of the DMMAs: RQC-30's 5-qubit gates with 28/32 nonzero tiles ran
   // 8-10 ms sparse, 7.7-8.4 ms dense (scripts/ks5_rqc_sparse.py); skipped zero
-  // tiles would only have added exact zeros.
+  // tiles would only have added exact zeros.  (A JIT kernel with the masks
+  // compiled in skips every zero tile at no cost: dmma_jit_spec.)
   const int n_dmma_tiles = 3 * S::RB * S::KST;
-  const int nonzero = __builtin_popcount(p.nzblk[0]) + __builtin_popcount(p.nzblk[1]) + __builtin_popcount(p.nzblk[2]);
+  st.nonzero = KS <= 5 ? __builtin_popcount(p.nzblk[0]) + __builtin_popcount(p.nzblk[1]) + __builtin_popcount(p.nzblk[2])
+                       : n_dmma_tiles;
   static const bool any_zero_rule = std::getenv("TSG_DMMA_SPARSE_ANY") != nullptr;  // round-1 rule (A/B runs)
-  bool sparse = KS <= 5 && (any_zero_rule ? nonzero < n_dmma_tiles : 4 * (n_dmma_tiles - nonzero) >= n_dmma_tiles);
+  st.sparse = KS <= 5 && (any_zero_rule ? st.nonzero < n_dmma_tiles : 4 * (n_dmma_tiles - st.nonzero) >= n_dmma_tiles);
   static const int force_sparse = [] {  // experiments: TSG_DMMA_SPARSE=0|1 forces the variant
     const char* e = std::getenv("TSG_DMMA_SPARSE");
     return e ? std::atoi(e) : -1;
   }();
-  if (force_sparse >= 0 && KS <= 5) sparse = force_sparse == 1;
+  if (force_sparse >= 0 && KS <= 5) st.sparse = force_sparse == 1;
   const int most = std::max({__builtin_popcount(p.nzblk[0]), __builtin_popcount(p.nzblk[1]), __builtin_popcount(p.nzblk[2])});
-  if (!dmma_geometry<Real, KS>(g, p, &smem, &stages, simt, 2 * most <= S::RB * S::KST)) return false;
+  return dmma_geometry<Real, KS>(g, p, &st.smem, &st.stages, st.simt, KS <= 5 && 2 * most <= S::RB * S::KST);
+}
+
+// a JIT-compiled product (dmma_jit_spec): same parameters and geometry
+template <typename Real, int KS>
+void launch_dmma_jit(const void* kern, const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int num_sms) {
+  using S = DShape<Real, KS>;
+  cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+             "dmma jit smem");
+  int per_sm = 1;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::kThreads + 32, smem), "dmma jit occupancy");
+  const uint64_t blocks = std::min<uint64_t>(p.n_tiles, uint64_t(num_sms) * std::max(per_sm, 1));
+  DmmaParams<Real, KS> arg = p;
+  void* args[] = {&arg};
+  cuda_check(cudaLaunchKernel(kern, dim3(static_cast<unsigned>(blocks)), dim3(S::kThreads + 32), args, smem, s),
+             "k_stream_dmma jit launch");
+}
+
+template <typename Real, int KS>
+bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
+  using S = DShape<Real, KS>;
+  if (!g.dev_mat) return false;
+  DmmaSetup<Real, KS> st;
+  if (!dmma_setup<Real, KS>(g, st)) return false;
+  DmmaParams<Real, KS>& p = st.p;
   p.re = static_cast<Real*>(g.re);
   p.im = static_cast<Real*>(g.im);
   p.mat = static_cast<const double*>(g.dev_mat);
   static const bool debug = std::getenv("TSG_DMMA_DEBUG") != nullptr;
   if (debug)
-    std::fprintf(stderr, "dmma ks=%d L=%d chunk=%d runs=%d stages=%d smem=%zu tiles=%d/%d/%d of %d sparse=%d\n", KS, p.L,
-                 p.chunk_log2, p.n_runs, stages, smem, __builtin_popcount(p.nzblk[0]), __builtin_popcount(p.nzblk[1]),
-                 __builtin_popcount(p.nzblk[2]), S::RB * S::KST, sparse ? 1 : 0);
-  switch (stages) {
+    std::fprintf(stderr, "dmma ks=%d L=%d chunk=%d runs=%d stages=%d smem=%zu tiles=%d/%d/%d of %d sparse=%d jit=%d\n", KS,
+                 p.L, p.chunk_log2, p.n_runs, st.stages, st.smem, __builtin_popcount(p.nzblk[0]),
+                 __builtin_popcount(p.nzblk[1]), __builtin_popcount(p.nzblk[2]), S::RB * S::KST, st.sparse ? 1 : 0,
+                 g.jit ? 1 : 0);
+  if constexpr (sizeof(Real) == 8 && KS <= 5) {
+    if (g.jit) {
+      launch_dmma_jit<Real, KS>(g.jit, p, st.smem, s, num_sms);
+      return true;
+    }
+  }
+  switch (st.stages) {
     case 3:
-      sparse ? launch_dmma_pick<Real, KS, 3, true>(p, smem, s, num_sms, simt)
-             : launch_dmma_pick<Real, KS, 3, false>(p, smem, s, num_sms, simt);
+      st.sparse ? launch_dmma_pick<Real, KS, 3, true>(p, st.smem, s, num_sms, st.simt)
+                : launch_dmma_pick<Real, KS, 3, false>(p, st.smem, s, num_sms, st.simt);
       break;
     default:
-      sparse ? launch_dmma_pick<Real, KS, 2, true>(p, smem, s, num_sms, simt)
-             : launch_dmma_pick<Real, KS, 2, false>(p, smem, s, num_sms, simt);
+      st.sparse ? launch_dmma_pick<Real, KS, 2, true>(p, st.smem, s, num_sms, st.simt)
+                : launch_dmma_pick<Real, KS, 2, false>(p, st.smem, s, num_sms, st.simt);
       break;
   }
   return true;

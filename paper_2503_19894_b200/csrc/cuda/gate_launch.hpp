@@ -59,6 +59,9 @@ struct GateLaunch {
   // that zero structure falls into whole 8x4 DMMA tiles).  Identity unless
   // the full-range DMMA path runs.
   uint8_t perm[1 << kMaxSub] = {};
+  // complex128 DMMA product JIT-compiled with this launch's zero 8 x 4 tiles
+  // compiled in (dmma_jit_spec, pass_jit.hpp); null: the generic kernel
+  const void* jit = nullptr;
 };
 
 // Launch on `stream`; returns the number of kernels enqueued (0 for identity).

@@ -166,9 +166,167 @@ __host__ __device__ constexpr size_t dmma_m_smem_bytes() {
   return dmma_m_in_regs<KS>() ? 0 : size_t{3} * ((1 << KS) / 4) * ((1 << KS) / 8) * 32 * sizeof(double);
 }
 
-template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT = false>
-__global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, KS>::W >= 16 ? 1 : 2)
-    k_stream_dmma(const __grid_constant__ DmmaParams<Real, KS> p) {
+// Tile bases in the persistent order first, first + step, ...: stepped in
+// the masked domain (non-tile bits forced to 1 so the carry crosses them).
+struct DmmaTileStream {
+  uint64_t raw, mask, dstep, ctrl;
+  __device__ uint64_t base() const { return raw | ctrl; }
+  __device__ void advance() { raw = ((raw | ~mask) + dstep) & mask; }
+};
+
+// Which 8 x 4 tiles of Mr / Mi / Ms the product visits: all (dense), the
+// launch's runtime masks (p.nzblk, per-tile predicates), or masks compiled
+// into a JIT kernel (DmmaStaticNz: the skipped DMMAs and loads vanish from
+// the code; per row block the consumer loop is instantiated once).
+struct DmmaDenseNz {
+  static constexpr bool kStatic = true, kDense = true;
+  template <typename P>
+  static __device__ __forceinline__ constexpr bool use(const P&, int, int) { return true; }
+};
+struct DmmaRuntimeNz {
+  static constexpr bool kStatic = false, kDense = false;
+  template <typename P>
+  static __device__ __forceinline__ bool use(const P& p, int m, int bit) { return (p.nzblk[m] >> bit) & 1u; }
+};
+template <uint32_t M0, uint32_t M1, uint32_t M2>
+struct DmmaStaticNz {
+  static constexpr bool kStatic = true, kDense = false;
+  template <typename P>
+  static __device__ __forceinline__ constexpr bool use(const P&, int m, int bit) {
+    return (((m == 0 ? M0 : (m == 1 ? M1 : M2)) >> bit) & 1u) != 0;
+  }
+};
+
+// Consumer warps of k_stream_dmma: Y = M X on the DMMA pipe for row block RB
+// (RBC >= 0: a compile-time row block, RBC < 0: rb at run time).
+template <typename Real, int KS, int STAGES, typename NZ, bool MREG, bool kDirectOut, int RBC>
+__device__ __forceinline__ void dmma_consumer(const DmmaParams<Real, KS>& p, Real* buf, uint64_t* full, uint64_t* empty,
+                                              uint32_t stage_elems, const double* mfrag,
+                                              const DmmaTileStream& stream0, int warp_rb, int wg, int lane) {
+  using S = DShape<Real, KS>;
+  const int rb = RBC >= 0 ? RBC : warp_rb;
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  const int lr = lane >> 2, lc = lane & 3;
+  double amr[MREG ? S::KST : 1], ami[MREG ? S::KST : 1], ams[MREG ? S::KST : 1];
+  if constexpr (MREG) {
+    constexpr int DD = S::D * S::D;
+#pragma unroll
+    for (int k = 0; k < S::KST; ++k) {
+      const int e = (8 * rb + lr) * S::D + 4 * k + lc;
+      amr[k] = p.mat[e];
+      ami[k] = p.mat[DD + e];
+      ams[k] = p.mat[2 * DD + e];
+    }
+  }
+  const double* mf = mfrag + rb * 32 + lane;  // fragment (m, k) at mf[(m * KST + k) * RB * 32]
+  uint32_t offb[S::KST], lbb[S::NR], lbc[S::NR][2];
+#pragma unroll
+  for (int k = 0; k < S::KST; ++k) offb[k] = p.soff[4 * k + lc];
+  // output row 8 rb + lr: shared offset offc (ks <= 4 write-back) and global
+  // offset goffc from the tile base (ks = 5 stores from registers); a
+  // group's base is padded for shared memory (lbb, lbc) and raw for global
+  // memory (gbc)
+  const uint32_t offc = p.soff[8 * rb + lr];
+  const uint64_t goffc = p.goff[8 * rb + lr];
+  uint32_t gbc[S::NR][2];
+#pragma unroll
+  for (int nb = 0; nb < S::NR; ++nb) {
+    const uint32_t g0 = wg * S::GW + nb * 8;
+    lbb[nb] = dmma_pad(p, dmma_group_pos(p, g0 + lr));
+    gbc[nb][0] = dmma_group_pos(p, g0 + 2 * lc);
+    gbc[nb][1] = dmma_group_pos(p, g0 + 2 * lc + 1);
+    lbc[nb][0] = dmma_pad(p, gbc[nb][0]);
+    lbc[nb][1] = dmma_pad(p, gbc[nb][1]);
+  }
+  // no target on bit 0: groups 2c, 2c+1 are adjacent, even-aligned amplitudes
+  const bool pair_store = gbc[0][1] == gbc[0][0] + 1 && (gbc[0][0] & 1u) == 0 && (goffc & 1u) == 0;
+
+  DmmaTileStream cstream = stream0;  // output addresses (ks = 5)
+  uint32_t j = 0;
+  for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
+    const int s = static_cast<int>(j % STAGES);
+    mbar_wait(&full[s], (j / STAGES) & 1u);
+    Real* xr = buf + (2 * s) * stage_elems;
+    Real* xi = xr + stage_elems;
+
+    double t1[S::NR][2], t2[S::NR][2], t3[S::NR][2];
+#pragma unroll
+    for (int nb = 0; nb < S::NR; ++nb) t1[nb][0] = t1[nb][1] = t2[nb][0] = t2[nb][1] = t3[nb][0] = t3[nb][1] = 0.0;
+#pragma unroll
+    for (int k = 0; k < S::KST; ++k) {
+      const int bit = rb * S::KST + k;
+      const bool use_r = NZ::use(p, 0, bit);
+      const bool use_i = NZ::use(p, 1, bit);
+      const bool use_s = NZ::use(p, 2, bit);
+      if (!(use_r || use_i || use_s)) continue;  // zero k-step of this row block: no loads either
+      // (compiled-in masks drop the loads of unused operands too; runtime
+      // masks load every operand of an active k-step)
+      constexpr bool kDrop = NZ::kStatic;
+      double fr = 0.0, fi = 0.0, fs = 0.0;
+      if constexpr (MREG) {
+        fr = amr[k];
+        fi = ami[k];
+        fs = ams[k];
+      } else {
+        if (!kDrop || use_r) fr = mf[(0 * S::KST + k) * S::RB * 32];
+        if (!kDrop || use_i) fi = mf[(1 * S::KST + k) * S::RB * 32];
+        if (!kDrop || use_s) fs = mf[(2 * S::KST + k) * S::RB * 32];
+      }
+#pragma unroll
+      for (int nb = 0; nb < S::NR; ++nb) {
+        const double br = (!kDrop || use_r || use_s) ? static_cast<double>(xr[lbb[nb] + offb[k]]) : 0.0;
+        const double bi = (!kDrop || use_i || use_s) ? static_cast<double>(xi[lbb[nb] + offb[k]]) : 0.0;
+        if (use_r) dmma(t1[nb], fr, br);
+        if (use_i) dmma(t2[nb], fi, bi);
+        if (use_s) dmma(t3[nb], fs, br + bi);
+      }
+    }
+    if constexpr (!kDirectOut) {
+      // all consumer warps have read the stage before anyone overwrites it
+      asm volatile("bar.sync 1, %0;" ::"r"(S::kThreads) : "memory");
+#pragma unroll
+      for (int nb = 0; nb < S::NR; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const uint32_t a = lbc[nb][i] + offc;
+          xr[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
+          xi[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
+        }
+      fence_async_smem();  // generic-proxy writes -> async-proxy bulk store
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+      continue;
+    }
+    // this warp has read the stage: release it to the producer, then write
+    // the results from registers (the stage is not written back)
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+    const uint64_t tb = cstream.base() + goffc;
+    cstream.advance();
+    if (pair_store) {  // the lane's two groups are adjacent amplitudes: one 2-element store per array
+#pragma unroll
+      for (int nb = 0; nb < S::NR; ++nb) {
+        const uint64_t a = tb + gbc[nb][0];
+        using V2 = std::conditional_t<sizeof(Real) == 8, double2, float2>;
+        *reinterpret_cast<V2*>(p.re + a) = V2{static_cast<Real>(t1[nb][0] - t2[nb][0]), static_cast<Real>(t1[nb][1] - t2[nb][1])};
+        *reinterpret_cast<V2*>(p.im + a) = V2{static_cast<Real>(t3[nb][0] - t1[nb][0] - t2[nb][0]),
+                                              static_cast<Real>(t3[nb][1] - t1[nb][1] - t2[nb][1])};
+      }
+    } else {
+#pragma unroll
+      for (int nb = 0; nb < S::NR; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const uint64_t a = tb + gbc[nb][i];
+          p.re[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
+          p.im[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
+        }
+    }
+  }
+}
+
+template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT, typename NZ>
+__device__ __forceinline__ void k_stream_dmma_body(const DmmaParams<Real, KS>& p) {
   using S = DShape<Real, KS>;
   constexpr bool MREG = dmma_m_in_regs<KS>();
   // ks = 5 (FP64-bound): results leave from registers so a stage frees as soon
@@ -227,20 +385,13 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
       if (i < p.n_tmask) b += (tile & p.tmask[i]) << i;
     return b << p.L;
   };
-  // Tile bases in the persistent order first, first + step, ...: stepped in
-  // the masked domain (non-tile bits forced to 1 so the carry crosses them).
-  struct TileStream {
-    uint64_t raw, mask, dstep, ctrl;
-    __device__ uint64_t base() const { return raw | ctrl; }
-    __device__ void advance() { raw = ((raw | ~mask) + dstep) & mask; }
-  };
-  const TileStream stream0{raw_base(first), raw_base(p.n_tiles - 1), raw_base(step), p.ctrl_hi};
+  const DmmaTileStream stream0{raw_base(first), raw_base(p.n_tiles - 1), raw_base(step), p.ctrl_hi};
 
   if (warp == S::W) {
     // ---------------- producer warp: TMA bulk loads and stores ------------
     // Copies are spread over the 32 lanes (lane l owns runs l, l+32, ...);
     // bulk groups are per thread, so every lane waits for its own stores.
-    TileStream lstream = stream0, sstream = stream0;  // next tile to load / to store
+    DmmaTileStream lstream = stream0, sstream = stream0;  // next tile to load / to store
     auto load = [&](uint64_t tile, int s) {
       const uint64_t base = lstream.base();
       lstream.advance();
@@ -353,120 +504,26 @@ __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, 
 
   // ---------------- consumer warps: Y = M X on the DMMA pipe --------------
   const int rb = warp / S::WG, wg = warp % S::WG;
-  const int lr = lane >> 2, lc = lane & 3;
-  double amr[MREG ? S::KST : 1], ami[MREG ? S::KST : 1], ams[MREG ? S::KST : 1];
-  if constexpr (MREG) {
-    constexpr int DD = S::D * S::D;
-#pragma unroll
-    for (int k = 0; k < S::KST; ++k) {
-      const int e = (8 * rb + lr) * S::D + 4 * k + lc;
-      amr[k] = p.mat[e];
-      ami[k] = p.mat[DD + e];
-      ams[k] = p.mat[2 * DD + e];
-    }
+  if constexpr (NZ::kStatic && !NZ::kDense) {
+    // compiled-in masks: one straight-line product per row block
+    static_assert(S::RB <= 8, "row blocks");
+#define TSG_DMMA_RB(R)                                                                                          \
+  if constexpr (S::RB > R)                                                                                      \
+    if (rb == R) return dmma_consumer<Real, KS, STAGES, NZ, MREG, kDirectOut, R>(p, buf, full, empty, stage_elems, \
+                                                                                mfrag, stream0, rb, wg, lane);
+    TSG_DMMA_RB(0) TSG_DMMA_RB(1) TSG_DMMA_RB(2) TSG_DMMA_RB(3) TSG_DMMA_RB(4) TSG_DMMA_RB(5) TSG_DMMA_RB(6)
+    TSG_DMMA_RB(7)
+#undef TSG_DMMA_RB
+  } else {
+    dmma_consumer<Real, KS, STAGES, std::conditional_t<SPARSE, DmmaRuntimeNz, DmmaDenseNz>, MREG, kDirectOut, -1>(
+        p, buf, full, empty, stage_elems, mfrag, stream0, rb, wg, lane);
   }
-  const double* mf = mfrag + rb * 32 + lane;  // fragment (m, k) at mf[(m * KST + k) * RB * 32]
-  uint32_t offb[S::KST], lbb[S::NR], lbc[S::NR][2];
-#pragma unroll
-  for (int k = 0; k < S::KST; ++k) offb[k] = p.soff[4 * k + lc];
-  // output row 8 rb + lr: shared offset offc (ks <= 4 write-back) and global
-  // offset goffc from the tile base (ks = 5 stores from registers); a
-  // group's base is padded for shared memory (lbb, lbc) and raw for global
-  // memory (gbc)
-  const uint32_t offc = p.soff[8 * rb + lr];
-  const uint64_t goffc = p.goff[8 * rb + lr];
-  uint32_t gbc[S::NR][2];
-#pragma unroll
-  for (int nb = 0; nb < S::NR; ++nb) {
-    const uint32_t g0 = wg * S::GW + nb * 8;
-    lbb[nb] = dmma_pad(p, dmma_group_pos(p, g0 + lr));
-    gbc[nb][0] = dmma_group_pos(p, g0 + 2 * lc);
-    gbc[nb][1] = dmma_group_pos(p, g0 + 2 * lc + 1);
-    lbc[nb][0] = dmma_pad(p, gbc[nb][0]);
-    lbc[nb][1] = dmma_pad(p, gbc[nb][1]);
-  }
-  // no target on bit 0: groups 2c, 2c+1 are adjacent, even-aligned amplitudes
-  const bool pair_store = gbc[0][1] == gbc[0][0] + 1 && (gbc[0][0] & 1u) == 0 && (goffc & 1u) == 0;
+}
 
-  TileStream cstream = stream0;  // output addresses (ks = 5)
-  uint32_t j = 0;
-  for (uint64_t tile = first; tile < p.n_tiles; tile += step, ++j) {
-    const int s = static_cast<int>(j % STAGES);
-    mbar_wait(&full[s], (j / STAGES) & 1u);
-    Real* xr = buf + (2 * s) * stage_elems;
-    Real* xi = xr + stage_elems;
-
-    double t1[S::NR][2], t2[S::NR][2], t3[S::NR][2];
-#pragma unroll
-    for (int nb = 0; nb < S::NR; ++nb) t1[nb][0] = t1[nb][1] = t2[nb][0] = t2[nb][1] = t3[nb][0] = t3[nb][1] = 0.0;
-#pragma unroll
-    for (int k = 0; k < S::KST; ++k) {
-      const int bit = rb * S::KST + k;
-      const bool use_r = !SPARSE || ((p.nzblk[0] >> bit) & 1u);
-      const bool use_i = !SPARSE || ((p.nzblk[1] >> bit) & 1u);
-      const bool use_s = !SPARSE || ((p.nzblk[2] >> bit) & 1u);
-      if (SPARSE && !(use_r || use_i || use_s)) continue;  // zero k-step of this row block: no loads either
-      double fr, fi, fs;
-      if constexpr (MREG) {
-        fr = amr[k];
-        fi = ami[k];
-        fs = ams[k];
-      } else {
-        fr = mf[(0 * S::KST + k) * S::RB * 32];
-        fi = mf[(1 * S::KST + k) * S::RB * 32];
-        fs = mf[(2 * S::KST + k) * S::RB * 32];
-      }
-#pragma unroll
-      for (int nb = 0; nb < S::NR; ++nb) {
-        const double br = static_cast<double>(xr[lbb[nb] + offb[k]]);
-        const double bi = static_cast<double>(xi[lbb[nb] + offb[k]]);
-        if (use_r) dmma(t1[nb], fr, br);
-        if (use_i) dmma(t2[nb], fi, bi);
-        if (use_s) dmma(t3[nb], fs, br + bi);
-      }
-    }
-    if constexpr (!kDirectOut) {
-      // all consumer warps have read the stage before anyone overwrites it
-      asm volatile("bar.sync 1, %0;" ::"r"(S::kThreads) : "memory");
-#pragma unroll
-      for (int nb = 0; nb < S::NR; ++nb)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const uint32_t a = lbc[nb][i] + offc;
-          xr[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
-          xi[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
-        }
-      fence_async_smem();  // generic-proxy writes -> async-proxy bulk store
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
-      continue;
-    }
-    // this warp has read the stage: release it to the producer, then write
-    // the results from registers (the stage is not written back)
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
-    const uint64_t tb = cstream.base() + goffc;
-    cstream.advance();
-    if (pair_store) {  // the lane's two groups are adjacent amplitudes: one 2-element store per array
-#pragma unroll
-      for (int nb = 0; nb < S::NR; ++nb) {
-        const uint64_t a = tb + gbc[nb][0];
-        using V2 = std::conditional_t<sizeof(Real) == 8, double2, float2>;
-        *reinterpret_cast<V2*>(p.re + a) = V2{static_cast<Real>(t1[nb][0] - t2[nb][0]), static_cast<Real>(t1[nb][1] - t2[nb][1])};
-        *reinterpret_cast<V2*>(p.im + a) = V2{static_cast<Real>(t3[nb][0] - t1[nb][0] - t2[nb][0]),
-                                              static_cast<Real>(t3[nb][1] - t1[nb][1] - t2[nb][1])};
-      }
-    } else {
-#pragma unroll
-      for (int nb = 0; nb < S::NR; ++nb)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const uint64_t a = tb + gbc[nb][i];
-          p.re[a] = static_cast<Real>(t1[nb][i] - t2[nb][i]);
-          p.im[a] = static_cast<Real>(t3[nb][i] - t1[nb][i] - t2[nb][i]);
-        }
-    }
-  }
+template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT = false>
+__global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, KS>::W >= 16 ? 1 : 2)
+    k_stream_dmma(const __grid_constant__ DmmaParams<Real, KS> p) {
+  k_stream_dmma_body<Real, KS, STAGES, SPARSE, SIMT, std::conditional_t<SPARSE, DmmaRuntimeNz, DmmaDenseNz>>(p);
 }
 
 // --------------------------------------------------------------------------

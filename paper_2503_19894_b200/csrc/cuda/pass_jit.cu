@@ -20,6 +20,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -167,7 +168,8 @@ std::vector<char> cached_cubin(const std::string& src, const std::string& name) 
   }
   std::vector<char> cubin = compile_cubin(src, name);
   mkdir(cache_dir().c_str(), 0777);
-  const std::string tmp = path + ".tmp" + std::to_string(getpid());
+  static std::atomic<unsigned> seq{0};  // unique per writer: threads of one process may compile the same kernel
+  const std::string tmp = path + ".tmp" + std::to_string(getpid()) + "." + std::to_string(seq.fetch_add(1));
   {
     std::ofstream out(tmp, std::ios::binary);
     out.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
@@ -258,6 +260,27 @@ std::string pass_jit_source(int precision_bits, const PassOp* ops, int n_ops, st
     << "(const __grid_constant__ tsg::PassParams p) {\n  tsg::k_pass_body<"
     << (precision_bits == 64 ? "double, 11, 5" : "float, 12, 6") << ", 2, tsg::jit::Exec>(p);\n}\n";
   return k.str();
+}
+
+std::string dmma_jit_source(int ks, int stages, const uint32_t nz[3], std::string* name) {
+  std::ostringstream body;
+  body << "complex128 ks=" << ks << " stages=" << stages << " nz=" << nz[0] << "," << nz[1] << "," << nz[2];
+  const std::string key = hex16(fnv1a(body.str(), fnv1a(std::string(kJitHeaderHash) + "dmma")));
+  *name = "tsg_dmma_jit_" + key;
+  std::ostringstream k;
+  k << kPreamble << "#include \"kernels_dmma.cuh\"\n"
+    << "extern \"C\" __global__ void __launch_bounds__(tsg::DShape<double, " << ks << ">::kThreads + 32, "
+    << "tsg::DShape<double, " << ks << ">::W >= 16 ? 1 : 2) " << *name
+    << "(const __grid_constant__ tsg::DmmaParams<double, " << ks << "> p) {\n"
+    << "  tsg::k_stream_dmma_body<double, " << ks << ", " << stages << ", true, false, tsg::DmmaStaticNz<" << nz[0]
+    << "u, " << nz[1] << "u, " << nz[2] << "u>>(p);\n}\n";
+  return k.str();
+}
+
+bool dmma_jit_enabled(int n_qubits) {
+  const char* e = std::getenv("TSG_DMMA_JIT");
+  if (e && e[0] == '0' && e[1] == '\0') return false;
+  return pass_jit_enabled(n_qubits);
 }
 
 void pass_jit_cubin(const std::string& source, const std::string& name) { cached_cubin(source, name); }

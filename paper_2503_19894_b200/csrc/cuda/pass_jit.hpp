@@ -16,4 +16,13 @@ void pass_jit_cubin(const std::string& source, const std::string& name);
 // compile (or fetch from the caches) and load; returns a cudaKernel_t usable as a launch handle
 const void* pass_jit_kernel(const std::string& source, const std::string& name);
 
+// CUDA source of a complex128 k_stream_dmma product with its nonzero 8 x 4
+// tiles of [Mr | Mi | Mr + Mi] compiled in (DmmaStaticNz); *name = its kernel name
+std::string dmma_jit_source(int ks, int stages, const uint32_t nz[3], std::string* name);
+// The JIT source of a full-range complex128 launch that takes the DMMA
+// stream kernel and has at least one zero tile; false otherwise (apply_f64.cu)
+bool dmma_jit_spec(const GateLaunch& g, std::string* source, std::string* name);
+// JIT DMMA products on (n >= TSG_PASS_JIT_MIN_N, unless TSG_PASS_JIT=0 or TSG_DMMA_JIT=0)
+bool dmma_jit_enabled(int n_qubits);
+
 }  // namespace tsg

@@ -1584,6 +1584,68 @@ void jit_passes(tsg_program* prog, const std::vector<unsigned char>& arena) {
   }
 }
 
+// The standalone complex128 DMMA launches with zero 8 x 4 tiles get a
+// JIT-compiled product with those tiles compiled out (pass_jit.hpp
+// dmma_jit_spec; skipped loads and DMMAs cost nothing, unlike the runtime
+// predicates of the sparse variant).  device = false: compile into the disk
+// cache only (no device).
+// (distinct kernels once; targets[i] = index into the returned specs of the
+// i-th JIT launch, with `launches` its GateLaunch)
+std::vector<std::pair<std::string, std::string>> dmma_jit_specs(tsg_program* prog,
+                                                                 std::vector<tsg::GateLaunch*>* launches,
+                                                                 std::vector<size_t>* targets) {
+  std::vector<std::pair<std::string, std::string>> specs;
+  if (prog->prec != 64 || !tsg::dmma_jit_enabled(prog->n)) return specs;
+  std::map<std::string, size_t> index;
+  auto consider = [&](tsg::GateLaunch& g) {
+    std::string src, name;
+    if (!tsg::dmma_jit_spec(g, &src, &name)) return;
+    auto it = index.find(name);
+    if (it == index.end()) {
+      it = index.emplace(name, specs.size()).first;
+      specs.emplace_back(std::move(src), std::move(name));
+    }
+    if (launches) {
+      launches->push_back(&g);
+      targets->push_back(it->second);
+    }
+  };
+  for (const ProgramStep& step : prog->steps) {
+    if (step.kind != kStepGate) continue;
+    ProgramGate& pg = prog->gates[step.gate];
+    if (pg.subs.empty()) consider(pg.launch);
+    else
+      for (tsg::GateLaunch& g : pg.subs) consider(g);
+  }
+  return specs;
+}
+
+void jit_gates(tsg_program* prog) {
+  std::vector<tsg::GateLaunch*> launches;
+  std::vector<size_t> targets;
+  const auto specs = dmma_jit_specs(prog, &launches, &targets);
+  if (specs.empty()) return;
+  std::vector<const void*> kern(specs.size(), nullptr);
+  std::vector<std::string> err(specs.size());
+  std::vector<std::thread> pool;
+  for (size_t i = 0; i < specs.size(); ++i)
+    pool.emplace_back([&, i] {
+      try {
+        cudaSetDevice(prog->ctx->device);
+        kern[i] = tsg::pass_jit_kernel(specs[i].first, specs[i].second);
+      } catch (const std::exception& e) {
+        err[i] = e.what();
+      }
+    });
+  for (std::thread& t : pool) t.join();
+  for (size_t i = 0; i < launches.size(); ++i) launches[i]->jit = kern[targets[i]];  // null: the generic kernel
+  for (size_t i = 0; i < specs.size(); ++i)
+    if (!kern[i]) {
+      static std::once_flag warned;
+      std::call_once(warned, [&] { std::fprintf(stderr, "tilesim: DMMA JIT unavailable (%s)\n", err[i].c_str()); });
+    }
+}
+
 // run_circuit's planning: plan every gate, group the launches into steps
 // (tile passes, block splits), upload matrices and pass blobs once.
 // host half: plans, steps, arena contents (no device work)
@@ -1601,6 +1663,7 @@ std::unique_ptr<tsg_program> build_program(tsg_ctx* ctx, const Circuit& fused, d
     ck(cudaMemcpy(prog->arena, arena.data(), arena.size(), cudaMemcpyHostToDevice), "program arena upload");
   }
   jit_passes(prog.get(), arena);
+  jit_gates(prog.get());
   ck(cudaEventCreate(&prog->ev0), "event");
   ck(cudaEventCreate(&prog->ev1), "event");
   prog->planning_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1684,8 +1747,21 @@ int tsc_pass_jit_precompile(const tsc_circuit* fused, int precision_bits, double
           err[i] = e.what();
         }
       });
+    // the JIT DMMA products of the program's standalone gates as well
+    const auto specs = dmma_jit_specs(prog.get(), nullptr, nullptr);
+    std::vector<std::string> gerr(specs.size());
+    for (size_t i = 0; i < specs.size(); ++i)
+      pool.emplace_back([&, i] {
+        try {
+          tsg::pass_jit_cubin(specs[i].first, specs[i].second);
+        } catch (const std::exception& e) {
+          gerr[i] = e.what();
+        }
+      });
     for (std::thread& t : pool) t.join();
     for (const std::string& e : err)
+      if (!e.empty()) throw SimError(e);
+    for (const std::string& e : gerr)
       if (!e.empty()) throw SimError(e);
     *n_passes = static_cast<int>(prog->passes.size());
   })
@@ -2259,6 +2335,20 @@ int tsg_program_step_count(const tsg_program* prog, uint64_t* out) {
     require(prog && out, "null argument");
     *out = prog->steps.size();
   })
+}
+
+int tsg_program_jit_kernels(const tsg_program* prog, int* jit_passes, int* jit_gate_launches) {
+  TSG_TRY({
+    require(prog && jit_passes && jit_gate_launches, "null argument");
+    *jit_passes = *jit_gate_launches = 0;
+    for (const ProgramPass& pp : prog->passes) *jit_passes += pp.launch.jit != nullptr;
+    for (const ProgramStep& st : prog->steps) {
+      if (st.kind != kStepGate) continue;
+      const ProgramGate& pg = prog->gates[st.gate];
+      if (pg.subs.empty()) *jit_gate_launches += pg.launch.jit != nullptr;
+      for (const tsg::GateLaunch& g : pg.subs) *jit_gate_launches += g.jit != nullptr;
+    }
+  });
 }
 
 int tsg_program_pass_layouts(const tsg_program* prog, uint64_t i, int* smem_layouts, int* shuffle_layouts) {

@@ -220,3 +220,47 @@ def test_dmma6_complex128(targets):
         ob.apply_kernel(n, targets, m, ore, oim)
         d = ts.compare_states(sv, (ore, oim))
         assert d <= 1e-12, (kind, targets, plan.info(), d)
+
+
+def _tile_sparse_matrix(k, seed, density=0.5):
+    """A random (non-unitary) matrix whose 8x4 DMMA tiles (natural order) are
+    zero with probability 1 - density."""
+    rng = np.random.default_rng(seed)
+    d = 1 << k
+    m = rng.normal(size=(d, d)) + 1j * rng.normal(size=(d, d))
+    for rb in range(d // 8):
+        for kb in range(d // 4):
+            if rng.uniform() > density:
+                m[8 * rb:8 * rb + 8, 4 * kb:4 * kb + 4] = 0
+    m[0, 0] = 1.0  # never all zero
+    return m / np.sqrt(d)
+
+
+@pytest.mark.parametrize("ks", [3, 4, 5])
+def test_dmma_jit_zero_tiles(ks, monkeypatch):
+    """Standalone complex128 DMMA products JIT-compiled with their zero tiles
+    compiled out: bit-identical to the generic kernels (dense or runtime
+    predicates), and against the oracle."""
+    monkeypatch.setenv("TSG_PASS_JIT_MIN_N", "1")
+    monkeypatch.setenv("TSG_NO_PASS", "1")
+    monkeypatch.setenv("TSG_NO_BLOCK_SPLIT", "1")
+    n = 16
+    rng = np.random.default_rng(ks)
+    c = ts.Circuit(n)
+    for i, density in enumerate((0.25, 0.5, 0.75, 0.9, 0.5)):
+        t = sorted(int(q) for q in rng.choice(n, size=ks, replace=False)) if i else list(range(ks))
+        c.add_matrix(t, _tile_sparse_matrix(ks, 10 * ks + i, density))
+    pj = ts.Program(c, "f64")
+    assert pj.jit_kernels()["gates"] >= 4, pj.jit_kernels()
+    monkeypatch.setenv("TSG_DMMA_JIT", "0")
+    p0 = ts.Program(c, "f64")
+    assert p0.jit_kernels()["gates"] == 0
+    a = ts.Statevector(n, "f64").init_random(3)
+    b = ts.Statevector(n, "f64").copy_from(a)
+    re0, im0 = a.download()
+    pj.run(a)
+    p0.run(b)
+    assert ts.compare_states(a, b) == 0.0
+    ore, oim = re0.copy(), im0.copy()
+    ob.run_circuit(to_oracle(c), ore, oim, threads=4)
+    assert ts.compare_states(a, (ore, oim)) <= 1e-12
