@@ -8,7 +8,14 @@ template <int KS>
 bool dmma_jit_spec_ks(const GateLaunch& g, std::string* source, std::string* name) {
   DmmaSetup<double, KS> st;
   if (!dmma_setup<double, KS>(g, st)) return false;
-  if (st.nonzero == 3 * DShape<double, KS>::RB * DShape<double, KS>::KST) return false;  // dense: nothing to compile in
+  // Measured on RQC-30's 5-qubit gates (profiles/r02/dmma_jit_ab.txt): the
+  // compiled-in masks win where a third to two thirds of the tiles are
+  // nonzero (40-48 of 96: 0.1-0.7 ms faster, FP64 work halved without the
+  // runtime predicates), and lose at a quarter (24 of 96, HBM-bound: +0.1-0.5 ms)
+  // and near-dense (88 of 96: +0.9 ms): one code path per row block costs
+  // more than the skipped work saves there.
+  const int all = 3 * DShape<double, KS>::RB * DShape<double, KS>::KST;
+  if (3 * st.nonzero < all || 3 * st.nonzero > 2 * all) return false;
   *source = dmma_jit_source(KS, st.stages, st.p.nzblk, name);
   return true;
 }

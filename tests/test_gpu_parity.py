@@ -228,11 +228,10 @@ def _tile_sparse_matrix(k, seed, density=0.5):
     rng = np.random.default_rng(seed)
     d = 1 << k
     m = rng.normal(size=(d, d)) + 1j * rng.normal(size=(d, d))
-    for rb in range(d // 8):
-        for kb in range(d // 4):
-            if rng.uniform() > density:
-                m[8 * rb:8 * rb + 8, 4 * kb:4 * kb + 4] = 0
-    m[0, 0] = 1.0  # never all zero
+    tiles = [(rb, kb) for rb in range(d // 8) for kb in range(d // 4)][1:]  # tile (0, 0) stays dense
+    zero = [t for t in tiles if rng.uniform() > density] or tiles[-1:]    # at least one zero tile
+    for rb, kb in zero:
+        m[8 * rb:8 * rb + 8, 4 * kb:4 * kb + 4] = 0
     return m / np.sqrt(d)
 
 
@@ -247,11 +246,11 @@ def test_dmma_jit_zero_tiles(ks, monkeypatch):
     n = 16
     rng = np.random.default_rng(ks)
     c = ts.Circuit(n)
-    for i, density in enumerate((0.25, 0.5, 0.75, 0.9, 0.5)):
+    for i, density in enumerate((0.25, 0.5, 0.75, 0.45, 0.55, 0.5)):
         t = sorted(int(q) for q in rng.choice(n, size=ks, replace=False)) if i else list(range(ks))
         c.add_matrix(t, _tile_sparse_matrix(ks, 10 * ks + i, density))
     pj = ts.Program(c, "f64")
-    assert pj.jit_kernels()["gates"] >= 4, pj.jit_kernels()
+    assert pj.jit_kernels()["gates"] >= 2, pj.jit_kernels()  # (the mid-density ones: dmma_jit_spec)
     monkeypatch.setenv("TSG_DMMA_JIT", "0")
     p0 = ts.Program(c, "f64")
     assert p0.jit_kernels()["gates"] == 0
