@@ -19,7 +19,9 @@ for r in rows[1:]:
 agg = collections.defaultdict(lambda: [0.0, 0, 0.0])
 for i, m in per.items():
     k = name[i]
-    k = "tsg_pass_jit_*" if k.startswith("tsg_pass_jit") and len(sys.argv) > 3 else k
+    for fam in ("tsg_pass_jit_", "tsg_dmma_jit_"):  # JIT kernels by family (one name per op table / tile mask)
+        if k.startswith(fam):
+            k = fam + "*"
     t = m.get("gpu__time_duration.sum", 0.0)
     unit_ms = t / 1e6 if t > 1e3 else t  # ns or ms depending on the ncu unit
     agg[k][0] += unit_ms
