@@ -75,6 +75,8 @@ int tsg_state_upload(tsg_state* st, const double* re, const double* im);
 int tsg_state_upload_range(tsg_state* st, uint64_t begin, uint64_t count, const double* re, const double* im);
 int tsg_state_download(tsg_state* st, double* re, double* im);
 int tsg_state_download_range(tsg_state* st, uint64_t begin, uint64_t count, double* re, double* im);
+/* amplitudes at arbitrary indices (a device gather, one copy back) */
+int tsg_state_gather(tsg_state* st, const uint64_t* indices, uint64_t count, double* re, double* im);
 int tsg_state_copy(tsg_state* dst, const tsg_state* src);
 /* QSV1 amplitude dump / load: header "QSV1", u8 precision bits
  * (32 | 64), u8 n, 10 zero bytes; then re[2^n], im[2^n] little-endian in the

@@ -127,6 +127,7 @@ _sig("tsg_state_upload", [_vp, _dp, _dp])
 _sig("tsg_state_upload_range", [_vp, _u64, _u64, _dp, _dp])
 _sig("tsg_state_download", [_vp, _dp, _dp])
 _sig("tsg_state_download_range", [_vp, _u64, _u64, _dp, _dp])
+_sig("tsg_state_gather", [_vp, C.POINTER(_u64), _u64, _dp, _dp])
 _sig("tsg_state_copy", [_vp, _vp])
 _sig("tsg_state_dump", [_vp, C.c_char_p])
 _sig("tsg_state_load", [_vp, C.c_char_p])
@@ -456,6 +457,15 @@ class Statevector:
         re = np.empty(count)
         im = np.empty(count)
         _check(_lib.tsg_state_download_range(self._h, begin, count, re.ctypes.data_as(_dp), im.ctypes.data_as(_dp)))
+        return re, im
+
+    def gather(self, indices):
+        """Amplitudes at arbitrary indices (one device gather, one copy back) -> (re, im)."""
+        idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
+        re = np.empty(idx.size)
+        im = np.empty(idx.size)
+        _check(_lib.tsg_state_gather(self._h, idx.ctypes.data_as(C.POINTER(_u64)), idx.size,
+                                     re.ctypes.data_as(_dp), im.ctypes.data_as(_dp)))
         return re, im
 
     def amplitudes(self) -> np.ndarray:

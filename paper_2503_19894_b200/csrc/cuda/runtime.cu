@@ -119,6 +119,15 @@ __global__ void __launch_bounds__(kRedThreads) k_overlap(const Real* __restrict_
 }
 
 // ------------------------------------------------------- init / convert
+// amplitudes at `count` indices into out[0, count) (re) and out[count, 2 count) (im)
+template <typename Real>
+__global__ void k_gather(const Real* re, const Real* im, const uint64_t* idx, uint64_t count, double* out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count; i += uint64_t(gridDim.x) * blockDim.x) {
+    out[i] = static_cast<double>(re[idx[i]]);
+    out[count + i] = static_cast<double>(im[idx[i]]);
+  }
+}
+
 template <typename Real>
 __global__ void k_set_amp(Real* re, Real* im, uint64_t idx, double vr, double vi) {
   re[idx] = static_cast<Real>(vr);
@@ -1943,6 +1952,28 @@ int tsg_state_download_range(tsg_state* st, uint64_t begin, uint64_t count, doub
       }
     }
     ck(cudaStreamSynchronize(st->stream), "download sync");
+  })
+}
+
+int tsg_state_gather(tsg_state* st, const uint64_t* indices, uint64_t count, double* re, double* im) {
+  TSG_TRY({
+    require(st && indices && re && im, "null argument");
+    require(count <= kStage / 2, "gather: too many indices (at most half the staging buffer)");
+    for (uint64_t i = 0; i < count; ++i) require(indices[i] < st->size(), "gather index outside the state");
+    if (count == 0) return TSG_OK;
+    use_device(st->ctx);
+    // indices in the staging buffer's second half, values into its first 2 count doubles
+    uint64_t* didx = reinterpret_cast<uint64_t*>(st->stage + kStage);
+    ck(cudaMemcpyAsync(didx, indices, count * sizeof(uint64_t), cudaMemcpyHostToDevice, st->stream), "gather indices");
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((count + 255) / 256, 1024));
+    if (st->prec == 64) k_gather<double><<<grid, 256, 0, st->stream>>>((double*)st->re, (double*)st->im, didx, count, st->stage);
+    else k_gather<float><<<grid, 256, 0, st->stream>>>((float*)st->re, (float*)st->im, didx, count, st->stage);
+    ck(cudaGetLastError(), "k_gather");
+    std::vector<double> buf(2 * count);
+    ck(cudaMemcpyAsync(buf.data(), st->stage, 2 * count * sizeof(double), cudaMemcpyDeviceToHost, st->stream), "gather");
+    ck(cudaStreamSynchronize(st->stream), "gather sync");
+    std::copy(buf.begin(), buf.begin() + count, re);
+    std::copy(buf.begin() + count, buf.end(), im);
   })
 }
 

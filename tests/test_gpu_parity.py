@@ -263,3 +263,16 @@ def test_dmma_jit_zero_tiles(ks, monkeypatch):
     ore, oim = re0.copy(), im0.copy()
     ob.run_circuit(to_oracle(c), ore, oim, threads=4)
     assert ts.compare_states(a, (ore, oim)) <= 1e-12
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_state_gather(prec):
+    """tsg_state_gather: amplitudes at arbitrary indices equal the downloaded state's."""
+    n = 14
+    sv = ts.Statevector(n, prec).init_random(5)
+    re, im = sv.download()
+    idx = np.random.default_rng(1).integers(0, 1 << n, size=77)
+    gr, gi = sv.gather(idx)
+    assert np.array_equal(gr, re[idx]) and np.array_equal(gi, im[idx])
+    with pytest.raises(ts.TilesimError):
+        sv.gather([1 << n])
