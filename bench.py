@@ -470,7 +470,7 @@ def run_ours(args):
             del p1, p2
             # one_tol=1e-8 lowering of cos(phi)~1 in tiny CP phases perturbs the norm by ~1e-8 (SPEC semantics)
             assert abs(nrm - 1.0) < 1e-6, nrm
-            assert np.array_equal(got_re, ref_re) and np.array_equal(got_im, ref_im), "e2e step != timed step
+            assert np.array_equal(got_re, ref_re) and np.array_equal(got_im, ref_im), "e2e step != timed step"
         e2e = {"value": dist.max(statistics.median(e2e_times)), "unit": "s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "includes": "generate+fuse+plan+upload+init+run+readback",
                "pipelining": "RQC-30's host front end (generate, fuse, plan, upload) overlaps QFT-30's device run "
