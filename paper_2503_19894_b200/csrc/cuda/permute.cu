@@ -108,7 +108,7 @@ __device__ __forceinline__ void perm_pre_gate(const PermParams& p, const PermPre
 }
 
 template <typename Real, bool PRE>
-__global__ void __launch_bounds__(kPermThreads, PRE ? 3 : 5) k_permute(const __grid_constant__ PermParams p) {
+__global__ void __launch_bounds__(kPermThreads, PRE ? 3 : 1) k_permute(const __grid_constant__ PermParams p) {
   // the pre-gate's sparse rows (a byte without a pre-gate: the plain kernel keeps its occupancy)
   __shared__ std::conditional_t<PRE, PermPreRows, char> pre_rows_storage;
   PermPreRows* pre_rows = reinterpret_cast<PermPreRows*>(&pre_rows_storage);
