@@ -16,7 +16,6 @@
 #include <algorithm>
 #include <stdexcept>
 #include <string>
-#include <type_traits>
 
 #include "gate_launch.hpp"
 
@@ -44,74 +43,68 @@ struct PermParams {
   int tsrc[kPermMaxTileLog2];       // local tile bit i -> local position of P's image
   // pre-gate (PermuteLaunch::pre_*): its qubits as local tile bits
   int pre_k;  // <= 4
-  int pre_lbit[4];       // local tile bit of sub-target bit b
-  int pre_lbit_rank[4];  // the gate bit at the k-th gate position in ascending local order
-  const double* pre_mat;  // [re | im] D x D row-major
+  int pre_lbit[4];
+  const double* pre_mat;
 };
 
-// The pre-gate on the loaded tiles in shared memory.  Work items are (group,
-// row) pairs spread over the CTA: phase 1 computes each item's output from
-// the group's inputs (the row's nonzero entries only, staged in shared memory
-// as a sparse row list), a barrier, phase 2 writes them in place.
-constexpr int kPermPreItems = 2 * kPermMaxTile / kPermThreads;  // items per thread (two tiles)
-
-constexpr int kPermPreMaxNnz = 128;  // nonzero entries of an absorbed gate (static shared memory budget)
-struct PermPreRows {  // the pre-gate's rows, sparse (staged once per CTA)
-  int start[17];      // row r: entries [start[r], start[r + 1])
-  uint8_t col[kPermPreMaxNnz];
-  double mr[kPermPreMaxNnz], mi[kPermPreMaxNnz];
-};
-
-template <typename Real>
-__device__ __forceinline__ void perm_pre_gate(const PermParams& p, const PermPreRows& rows, Real (*tr)[kPermPadded],
-                                              Real (*ti)[kPermPadded], int n_tiles) {
-  const int K = p.pre_k, D = 1 << K, m = p.m;
+// The pre-gate on one loaded tile in shared memory: thread-strided groups of
+// 2^k amplitudes (the gate's local bits), each read into registers, multiplied
+// by the dense sub-matrix (zero entries skipped, uniformly), written back --
+// groups are disjoint, so in place without a barrier.
+template <typename Real, int K>
+__device__ __forceinline__ void perm_pre_gate(const PermParams& p, Real* tr, Real* ti, int tile_log2) {
+  constexpr int D = 1 << K;
   uint32_t gm = 0;  // local bits of the gate
   for (int b = 0; b < K; ++b) gm |= 1u << p.pre_lbit[b];
-  auto local = [&](uint32_t g, uint32_t j) {  // deposit g over the non-gate bits, j over the gate bits
-    uint32_t t = 0;
-    for (int b = 0, kg = 0, kj = 0; b < m; ++b)
-      if ((gm >> b) & 1u) t |= ((j >> p.pre_lbit_rank[kj++]) & 1u) << b;
-      else t |= ((g >> kg++) & 1u) << b;
-    return t;
-  };
-  const uint32_t items = static_cast<uint32_t>(n_tiles) << m;  // (tile, group, row): 2^m per tile
-  Real yr[kPermPreItems], yi[kPermPreItems];
+  const uint32_t n_groups = (1u << tile_log2) >> K;
+  for (uint32_t g = threadIdx.x; g < n_groups; g += blockDim.x) {
+    uint32_t base = 0;  // deposit g over the non-gate local bits
+    for (uint32_t b = 0, k = 0; b < static_cast<uint32_t>(tile_log2); ++b)
+      if (!((gm >> b) & 1u)) base |= ((g >> k++) & 1u) << b;
+    uint32_t off[D];
+    Real vr[D], vi[D];
 #pragma unroll
-  for (int q = 0; q < kPermPreItems; ++q) {
-    const uint32_t it = threadIdx.x + q * kPermThreads;
-    yr[q] = yi[q] = Real(0);
-    if (it >= items) continue;
-    const int tile = static_cast<int>(it >> m);
-    const uint32_t rest = it & ((1u << m) - 1), r = rest & (D - 1), g = rest >> K;
-    for (int e = rows.start[r]; e < rows.start[r + 1]; ++e) {
-      const uint32_t a = perm_pad(local(g, rows.col[e]));
-      const Real mr = static_cast<Real>(rows.mr[e]), mi = static_cast<Real>(rows.mi[e]);
-      const Real xr = tr[tile][a], xi = ti[tile][a];
-      yr[q] = fma(mr, xr, yr[q]);
-      yi[q] = fma(mr, xi, yi[q]);
-      yr[q] = fma(-mi, xi, yr[q]);
-      yi[q] = fma(mi, xr, yi[q]);
+    for (int j = 0; j < D; ++j) {
+      uint32_t t = base;
+#pragma unroll
+      for (int b = 0; b < K; ++b) t |= ((j >> b) & 1u) << p.pre_lbit[b];
+      off[j] = perm_pad(t);
+      vr[j] = tr[off[j]];
+      vi[j] = ti[off[j]];
     }
-  }
-  __syncthreads();  // every item has read its group
 #pragma unroll
-  for (int q = 0; q < kPermPreItems; ++q) {
-    const uint32_t it = threadIdx.x + q * kPermThreads;
-    if (it >= items) continue;
-    const int tile = static_cast<int>(it >> m);
-    const uint32_t rest = it & ((1u << m) - 1), r = rest & (D - 1), g = rest >> K;
-    const uint32_t a = perm_pad(local(g, r));
-    tr[tile][a] = yr[q];
-    ti[tile][a] = yi[q];
+    for (int r = 0; r < D; ++r) {
+      Real yr = Real(0), yi = Real(0);
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const Real mr = static_cast<Real>(__ldg(p.pre_mat + r * D + c));
+        const Real mi = static_cast<Real>(__ldg(p.pre_mat + D * D + r * D + c));
+        if (mr == Real(0) && mi == Real(0)) continue;  // the same for every thread
+        yr = fma(mr, vr[c], yr);
+        yi = fma(mr, vi[c], yi);
+        yr = fma(-mi, vi[c], yr);
+        yi = fma(mi, vr[c], yi);
+      }
+      tr[off[r]] = yr;
+      ti[off[r]] = yi;
+    }
   }
 }
 
+template <typename Real>
+__device__ __forceinline__ void perm_pre_dispatch(const PermParams& p, Real* tr, Real* ti, int tile_log2) {
+  switch (p.pre_k) {
+    case 1: perm_pre_gate<Real, 1>(p, tr, ti, tile_log2); break;
+    case 2: perm_pre_gate<Real, 2>(p, tr, ti, tile_log2); break;
+    case 3: perm_pre_gate<Real, 3>(p, tr, ti, tile_log2); break;
+    case 4: perm_pre_gate<Real, 4>(p, tr, ti, tile_log2); break;
+    default: break;
+  }
+}
+
+
 template <typename Real, bool PRE>
-__global__ void __launch_bounds__(kPermThreads, PRE ? 3 : 1) k_permute(const __grid_constant__ PermParams p) {
-  // the pre-gate's sparse rows (a byte without a pre-gate: the plain kernel keeps its occupancy)
-  __shared__ std::conditional_t<PRE, PermPreRows, char> pre_rows_storage;
-  PermPreRows* pre_rows = reinterpret_cast<PermPreRows*>(&pre_rows_storage);
+__global__ void __launch_bounds__(kPermThreads) k_permute(const __grid_constant__ PermParams p) {
   __shared__ uint64_t dep[kPermMaxTile];   // local index t -> index bits
   __shared__ uint16_t src[kPermMaxTile];   // local index t -> padded smem slot of its source
   __shared__ Real tr[2][kPermPadded], ti[2][kPermPadded];
@@ -126,24 +119,6 @@ __global__ void __launch_bounds__(kPermThreads, PRE ? 3 : 1) k_permute(const __g
       }
     dep[t] = d;
     src[t] = static_cast<uint16_t>(perm_pad(s));
-  }
-  if constexpr (PRE) {  // the pre-gate's nonzero entries, row by row
-    if (threadIdx.x == 0) {
-      const int D = 1 << p.pre_k;
-      int e = 0;
-      for (int r = 0; r < D; ++r) {
-        pre_rows[0].start[r] = e;
-        for (int c = 0; c < D; ++c) {
-          const double mr = p.pre_mat[r * D + c], mi = p.pre_mat[D * D + r * D + c];
-          if ((mr == 0.0 && mi == 0.0) || e >= kPermPreMaxNnz) continue;  // (the host bounds the count)
-          pre_rows[0].col[e] = static_cast<uint8_t>(c);
-          pre_rows[0].mr[e] = mr;
-          pre_rows[0].mi[e] = mi;
-          ++e;
-        }
-      }
-      pre_rows[0].start[D] = e;
-    }
   }
   __syncthreads();
   Real* re = static_cast<Real*>(p.re);
@@ -168,7 +143,8 @@ __global__ void __launch_bounds__(kPermThreads, PRE ? 3 : 1) k_permute(const __g
     __syncthreads();
     if constexpr (PRE) {  // the absorbed gate, on each loaded tile before the permutation
       // (its own instantiation: the plain permutation keeps its registers and occupancy)
-      perm_pre_gate<Real>(p, pre_rows[0], tr, ti, self ? 1 : 2);
+      perm_pre_dispatch<Real>(p, tr[0], ti[0], p.m);
+      if (!self) perm_pre_dispatch<Real>(p, tr[1], ti[1], p.m);
       __syncthreads();
     }
     const int other = self ? 0 : 1;
@@ -256,11 +232,6 @@ int launch_permute_impl(const PermuteLaunch& pl, cudaStream_t s, int num_sms) {
   for (int b = 0; b < pl.pre_k; ++b) {
     if (pl.pre_q[b] < 0 || pl.pre_q[b] >= n || !in_t[pl.pre_q[b]]) throw std::runtime_error("k_permute: pre-gate off the tile");
     p.pre_lbit[b] = lpos[pl.pre_q[b]];
-  }
-  for (int k = 0; k < pl.pre_k; ++k) {  // gate bits by ascending local position
-    int rank = 0;
-    for (int b = 0; b < pl.pre_k; ++b) rank += p.pre_lbit[b] < p.pre_lbit[k];
-    p.pre_lbit_rank[rank] = k;
   }
   p.n_units = uint64_t{1} << (n - m);
   p.n_omask = insertion_masks(tpos, m, n - m, p.omask);

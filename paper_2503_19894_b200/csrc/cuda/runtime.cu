@@ -1529,9 +1529,6 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
           const uint64_t tile = tsg::permute_tile_mask(pp.invs.front().data(), prog->n, want);
           bool ok = ls.controls.empty() && ls.ks >= 1 && ls.ks <= 4 && ls.klass != KernelClass::Identity;
           for (int q : ls.sub_targets) ok = ok && ((tile >> q) & 1u);
-          int nnz = 0;  // the permutation kernel stages at most 128 nonzero entries
-          for (size_t e = 0; e < ls.sub_re.size(); ++e) nnz += ls.sub_re[e] != 0.0 || ls.sub_im[e] != 0.0;
-          ok = ok && nnz <= 128;
           if (ok) {
             const size_t D = size_t{1} << ls.ks;
             pp.pre_gate = prog->steps.back().gate;
