@@ -218,14 +218,13 @@ struct PermuteLaunch {
   int p[64] = {};
   // optional gate applied to every loaded tile before the permutation (the
   // gate right before the permutation run, when its qubits are tile qubits):
-  // D x D sub-matrix (D = 2^pre_k, pre_k <= 4) on qubits pre_q, [re | im] row-major, fp64, device
+  // D x D sub-matrix (D = 2^pre_k) on qubits pre_q, [re | im] row-major, fp64, device
   int pre_k = 0;
-  int pre_q[4] = {};
+  int pre_q[5] = {};
   const double* pre_mat = nullptr;
 };
-// Tile qubits of the k_permute launch for permutation p (bit q set: qubit q),
-// preferring the qubits in `prefer` (a pre-gate's) after the run bits and their images
-uint64_t permute_tile_mask(const int* p, int n, uint64_t prefer = 0);
+// Tile qubits of the k_permute launch for permutation p (bit q set: qubit q)
+uint64_t permute_tile_mask(const int* p, int n);
 int launch_permute_f64(const PermuteLaunch& p, cudaStream_t stream, int num_sms);
 int launch_permute_f32(const PermuteLaunch& p, cudaStream_t stream, int num_sms);
 

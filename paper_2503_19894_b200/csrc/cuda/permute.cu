@@ -42,8 +42,8 @@ struct PermParams {
   uint64_t tdep[kPermMaxTileLog2];  // local tile bit i -> index bit
   int tsrc[kPermMaxTileLog2];       // local tile bit i -> local position of P's image
   // pre-gate (PermuteLaunch::pre_*): its qubits as local tile bits
-  int pre_k;  // <= 4
-  int pre_lbit[4];
+  int pre_k;
+  int pre_lbit[5];
   const double* pre_mat;
 };
 
@@ -98,12 +98,13 @@ __device__ __forceinline__ void perm_pre_dispatch(const PermParams& p, Real* tr,
     case 2: perm_pre_gate<Real, 2>(p, tr, ti, tile_log2); break;
     case 3: perm_pre_gate<Real, 3>(p, tr, ti, tile_log2); break;
     case 4: perm_pre_gate<Real, 4>(p, tr, ti, tile_log2); break;
+    case 5: perm_pre_gate<Real, 5>(p, tr, ti, tile_log2); break;
     default: break;
   }
 }
 
 
-template <typename Real, bool PRE>
+template <typename Real>
 __global__ void __launch_bounds__(kPermThreads) k_permute(const __grid_constant__ PermParams p) {
   __shared__ uint64_t dep[kPermMaxTile];   // local index t -> index bits
   __shared__ uint16_t src[kPermMaxTile];   // local index t -> padded smem slot of its source
@@ -141,8 +142,7 @@ __global__ void __launch_bounds__(kPermThreads) k_permute(const __grid_constant_
       }
     }
     __syncthreads();
-    if constexpr (PRE) {  // the absorbed gate, on each loaded tile before the permutation
-      // (its own instantiation: the plain permutation keeps its registers and occupancy)
+    if (p.pre_k > 0) {  // the absorbed gate, on each loaded tile before the permutation
       perm_pre_dispatch<Real>(p, tr[0], ti[0], p.m);
       if (!self) perm_pre_dispatch<Real>(p, tr[1], ti[1], p.m);
       __syncthreads();
@@ -166,9 +166,8 @@ void perm_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
-// tile bits: the run bits, their images, then the preferred qubits (a
-// pre-gate's) with their images, then further p-closed positions
-int perm_tile_bits(const int* p, int n, bool* in_t, uint64_t prefer = 0) {
+// tile bits: the run bits, their images, then further p-closed positions
+int perm_tile_bits(const int* p, int n, bool* in_t) {
   const int m_target = std::min(kPermMaxTileLog2, n);
   int m = 0;
   for (int q = 0; q < std::min(5, n); ++q) {
@@ -177,13 +176,6 @@ int perm_tile_bits(const int* p, int n, bool* in_t, uint64_t prefer = 0) {
         in_t[r] = true;
         ++m;
       }
-  }
-  for (int q = 0; q < n && m < m_target; ++q) {
-    if (!((prefer >> q) & 1u) || in_t[q]) continue;
-    const int need = p[q] == q ? 1 : 2;
-    if (m + need > m_target) continue;
-    in_t[q] = in_t[p[q]] = true;
-    m += need;
   }
   for (int q = 0; q < n && m < m_target; ++q) {
     if (in_t[q]) continue;
@@ -205,9 +197,7 @@ int launch_permute_impl(const PermuteLaunch& pl, cudaStream_t s, int num_sms) {
   }
   if (!any) return 0;
   bool in_t[64] = {};
-  uint64_t prefer = 0;
-  for (int b = 0; b < pl.pre_k; ++b) prefer |= uint64_t{1} << pl.pre_q[b];
-  const int m = perm_tile_bits(pl.p, n, in_t, prefer);
+  const int m = perm_tile_bits(pl.p, n, in_t);
   if (m > kPermMaxTileLog2) throw std::runtime_error("k_permute: tile too large");
   PermParams p{};
   p.re = pl.re;
@@ -226,7 +216,6 @@ int launch_permute_impl(const PermuteLaunch& pl, cudaStream_t s, int num_sms) {
     p.tdep[i] = uint64_t{1} << tpos[i];
     p.tsrc[i] = lpos[pl.p[tpos[i]]];
   }
-  if (pl.pre_k > 4) throw std::runtime_error("k_permute: pre-gate wider than 4 qubits");
   p.pre_k = pl.pre_k;
   p.pre_mat = pl.pre_mat;
   for (int b = 0; b < pl.pre_k; ++b) {
@@ -242,20 +231,19 @@ int launch_permute_impl(const PermuteLaunch& pl, cudaStream_t s, int num_sms) {
       p.mo_mask |= uint64_t{1} << opos[i];
       ++p.n_mo;
     }
-  auto kern = pl.pre_k > 0 ? k_permute<Real, true> : k_permute<Real, false>;
   int per_sm = 1;
-  perm_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPermThreads, 0), "k_permute occupancy");
+  perm_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_permute<Real>, kPermThreads, 0), "k_permute occupancy");
   const uint64_t blocks = std::min<uint64_t>(p.n_units, uint64_t(num_sms) * std::max(per_sm, 1) * 4);
-  kern<<<static_cast<unsigned>(blocks), kPermThreads, 0, s>>>(p);
+  k_permute<Real><<<static_cast<unsigned>(blocks), kPermThreads, 0, s>>>(p);
   perm_check(cudaGetLastError(), "k_permute launch");
   return 1;
 }
 
 }  // namespace
 
-uint64_t permute_tile_mask(const int* p, int n, uint64_t prefer) {
+uint64_t permute_tile_mask(const int* p, int n) {
   bool in_t[64] = {};
-  perm_tile_bits(p, n, in_t, prefer);
+  perm_tile_bits(p, n, in_t);
   uint64_t mask = 0;
   for (int q = 0; q < n; ++q) mask |= static_cast<uint64_t>(in_t[q]) << q;
   return mask;

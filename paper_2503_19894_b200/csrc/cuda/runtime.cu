@@ -1524,10 +1524,8 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
         if (!no_pre && !prog->steps.empty() && prog->steps.back().kind == kStepGate) {
           ProgramGate& pg = prog->gates[prog->steps.back().gate];
           const LaunchStructure& ls = pg.ls;
-          uint64_t want = 0;
-          for (int q : ls.sub_targets) want |= uint64_t{1} << q;
-          const uint64_t tile = tsg::permute_tile_mask(pp.invs.front().data(), prog->n, want);
-          bool ok = ls.controls.empty() && ls.ks >= 1 && ls.ks <= 4 && ls.klass != KernelClass::Identity;
+          const uint64_t tile = tsg::permute_tile_mask(pp.invs.front().data(), prog->n);
+          bool ok = ls.controls.empty() && ls.ks >= 1 && ls.ks <= 5 && ls.klass != KernelClass::Identity;
           for (int q : ls.sub_targets) ok = ok && ((tile >> q) & 1u);
           if (ok) {
             const size_t D = size_t{1} << ls.ks;
