@@ -1519,8 +1519,7 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
         // fused with two of the bit-reversal swaps) when its qubits are tile
         // qubits of the first launch: the permutation kernel applies it to every
         // tile it loads, one sweep saved.  TSG_NO_PERMUTE_PRE=1 keeps it apart.
-        const char* no_pre_env = std::getenv("TSG_NO_PERMUTE_PRE");
-        const bool no_pre = no_pre_env && *no_pre_env && *no_pre_env != '0';
+        static const bool no_pre = std::getenv("TSG_NO_PERMUTE_PRE") != nullptr;
         if (!no_pre && !prog->steps.empty() && prog->steps.back().kind == kStepGate) {
           ProgramGate& pg = prog->gates[prog->steps.back().gate];
           const LaunchStructure& ls = pg.ls;
