@@ -216,15 +216,7 @@ struct PermuteLaunch {
   void* re = nullptr;
   void* im = nullptr;
   int p[64] = {};
-  // optional gate applied to every loaded tile before the permutation (the
-  // gate right before the permutation run, when its qubits are tile qubits):
-  // D x D sub-matrix (D = 2^pre_k) on qubits pre_q, [re | im] row-major, fp64, device
-  int pre_k = 0;
-  int pre_q[5] = {};
-  const double* pre_mat = nullptr;
 };
-// Tile qubits of the k_permute launch for permutation p (bit q set: qubit q)
-uint64_t permute_tile_mask(const int* p, int n);
 int launch_permute_f64(const PermuteLaunch& p, cudaStream_t stream, int num_sms);
 int launch_permute_f32(const PermuteLaunch& p, cudaStream_t stream, int num_sms);
 

@@ -27,8 +27,6 @@ constexpr int kPermMaxTileLog2 = 10;
 constexpr int kPermMaxTile = 1 << kPermMaxTileLog2;
 constexpr int kPermPadded = kPermMaxTile + kPermMaxTile / 32;
 
-__device__ __forceinline__ uint32_t perm_pad(uint32_t s) { return s + (s >> 5); }
-
 struct PermParams {
   void* re;
   void* im;
@@ -41,68 +39,9 @@ struct PermParams {
   uint64_t mo_mask;
   uint64_t tdep[kPermMaxTileLog2];  // local tile bit i -> index bit
   int tsrc[kPermMaxTileLog2];       // local tile bit i -> local position of P's image
-  // pre-gate (PermuteLaunch::pre_*): its qubits as local tile bits
-  int pre_k;
-  int pre_lbit[5];
-  const double* pre_mat;
 };
 
-// The pre-gate on one loaded tile in shared memory: thread-strided groups of
-// 2^k amplitudes (the gate's local bits), each read into registers, multiplied
-// by the dense sub-matrix (zero entries skipped, uniformly), written back --
-// groups are disjoint, so in place without a barrier.
-template <typename Real, int K>
-__device__ __forceinline__ void perm_pre_gate(const PermParams& p, Real* tr, Real* ti, int tile_log2) {
-  constexpr int D = 1 << K;
-  uint32_t gm = 0;  // local bits of the gate
-  for (int b = 0; b < K; ++b) gm |= 1u << p.pre_lbit[b];
-  const uint32_t n_groups = (1u << tile_log2) >> K;
-  for (uint32_t g = threadIdx.x; g < n_groups; g += blockDim.x) {
-    uint32_t base = 0;  // deposit g over the non-gate local bits
-    for (uint32_t b = 0, k = 0; b < static_cast<uint32_t>(tile_log2); ++b)
-      if (!((gm >> b) & 1u)) base |= ((g >> k++) & 1u) << b;
-    uint32_t off[D];
-    Real vr[D], vi[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      uint32_t t = base;
-#pragma unroll
-      for (int b = 0; b < K; ++b) t |= ((j >> b) & 1u) << p.pre_lbit[b];
-      off[j] = perm_pad(t);
-      vr[j] = tr[off[j]];
-      vi[j] = ti[off[j]];
-    }
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-      Real yr = Real(0), yi = Real(0);
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        const Real mr = static_cast<Real>(__ldg(p.pre_mat + r * D + c));
-        const Real mi = static_cast<Real>(__ldg(p.pre_mat + D * D + r * D + c));
-        if (mr == Real(0) && mi == Real(0)) continue;  // the same for every thread
-        yr = fma(mr, vr[c], yr);
-        yi = fma(mr, vi[c], yi);
-        yr = fma(-mi, vi[c], yr);
-        yi = fma(mi, vr[c], yi);
-      }
-      tr[off[r]] = yr;
-      ti[off[r]] = yi;
-    }
-  }
-}
-
-template <typename Real>
-__device__ __forceinline__ void perm_pre_dispatch(const PermParams& p, Real* tr, Real* ti, int tile_log2) {
-  switch (p.pre_k) {
-    case 1: perm_pre_gate<Real, 1>(p, tr, ti, tile_log2); break;
-    case 2: perm_pre_gate<Real, 2>(p, tr, ti, tile_log2); break;
-    case 3: perm_pre_gate<Real, 3>(p, tr, ti, tile_log2); break;
-    case 4: perm_pre_gate<Real, 4>(p, tr, ti, tile_log2); break;
-    case 5: perm_pre_gate<Real, 5>(p, tr, ti, tile_log2); break;
-    default: break;
-  }
-}
-
+__device__ __forceinline__ uint32_t perm_pad(uint32_t s) { return s + (s >> 5); }
 
 template <typename Real>
 __global__ void __launch_bounds__(kPermThreads) k_permute(const __grid_constant__ PermParams p) {
@@ -142,11 +81,6 @@ __global__ void __launch_bounds__(kPermThreads) k_permute(const __grid_constant_
       }
     }
     __syncthreads();
-    if (p.pre_k > 0) {  // the absorbed gate, on each loaded tile before the permutation
-      perm_pre_dispatch<Real>(p, tr[0], ti[0], p.m);
-      if (!self) perm_pre_dispatch<Real>(p, tr[1], ti[1], p.m);
-      __syncthreads();
-    }
     const int other = self ? 0 : 1;
     for (int t = threadIdx.x; t < tile; t += kPermThreads) {
       const uint64_t d = dep[t];
@@ -166,27 +100,6 @@ void perm_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
-// tile bits: the run bits, their images, then further p-closed positions
-int perm_tile_bits(const int* p, int n, bool* in_t) {
-  const int m_target = std::min(kPermMaxTileLog2, n);
-  int m = 0;
-  for (int q = 0; q < std::min(5, n); ++q) {
-    for (int r : {q, p[q]})
-      if (!in_t[r]) {
-        in_t[r] = true;
-        ++m;
-      }
-  }
-  for (int q = 0; q < n && m < m_target; ++q) {
-    if (in_t[q]) continue;
-    const int need = p[q] == q ? 1 : 2;
-    if (m + need > m_target) continue;
-    in_t[q] = in_t[p[q]] = true;
-    m += need;
-  }
-  return m;
-}
-
 template <typename Real>
 int launch_permute_impl(const PermuteLaunch& pl, cudaStream_t s, int num_sms) {
   const int n = pl.n;
@@ -196,8 +109,24 @@ int launch_permute_impl(const PermuteLaunch& pl, cudaStream_t s, int num_sms) {
     any |= pl.p[q] != q;
   }
   if (!any) return 0;
+  // tile bits: the run bits, their images, then further p-closed positions
+  const int m_target = std::min(kPermMaxTileLog2, n);
   bool in_t[64] = {};
-  const int m = perm_tile_bits(pl.p, n, in_t);
+  int m = 0;
+  for (int q = 0; q < std::min(5, n); ++q) {
+    for (int r : {q, pl.p[q]})
+      if (!in_t[r]) {
+        in_t[r] = true;
+        ++m;
+      }
+  }
+  for (int q = 0; q < n && m < m_target; ++q) {
+    if (in_t[q]) continue;
+    const int need = pl.p[q] == q ? 1 : 2;
+    if (m + need > m_target) continue;
+    in_t[q] = in_t[pl.p[q]] = true;
+    m += need;
+  }
   if (m > kPermMaxTileLog2) throw std::runtime_error("k_permute: tile too large");
   PermParams p{};
   p.re = pl.re;
@@ -215,12 +144,6 @@ int launch_permute_impl(const PermuteLaunch& pl, cudaStream_t s, int num_sms) {
   for (int i = 0; i < m; ++i) {
     p.tdep[i] = uint64_t{1} << tpos[i];
     p.tsrc[i] = lpos[pl.p[tpos[i]]];
-  }
-  p.pre_k = pl.pre_k;
-  p.pre_mat = pl.pre_mat;
-  for (int b = 0; b < pl.pre_k; ++b) {
-    if (pl.pre_q[b] < 0 || pl.pre_q[b] >= n || !in_t[pl.pre_q[b]]) throw std::runtime_error("k_permute: pre-gate off the tile");
-    p.pre_lbit[b] = lpos[pl.pre_q[b]];
   }
   p.n_units = uint64_t{1} << (n - m);
   p.n_omask = insertion_masks(tpos, m, n - m, p.omask);
@@ -240,14 +163,6 @@ int launch_permute_impl(const PermuteLaunch& pl, cudaStream_t s, int num_sms) {
 }
 
 }  // namespace
-
-uint64_t permute_tile_mask(const int* p, int n) {
-  bool in_t[64] = {};
-  perm_tile_bits(p, n, in_t);
-  uint64_t mask = 0;
-  for (int q = 0; q < n; ++q) mask |= static_cast<uint64_t>(in_t[q]) << q;
-  return mask;
-}
 
 int launch_permute_f64(const PermuteLaunch& p, cudaStream_t s, int num_sms) { return launch_permute_impl<double>(p, s, num_sms); }
 int launch_permute_f32(const PermuteLaunch& p, cudaStream_t s, int num_sms) { return launch_permute_impl<float>(p, s, num_sms); }

@@ -237,10 +237,6 @@ struct ProgramPass {
 // permutation is not an involution).
 struct ProgramPermute {
   std::vector<std::vector<int>> invs;  // launch order
-  // the gate right before the run, applied by the first launch to every
-  // loaded tile (its qubits are tile qubits of that launch): -1 if none
-  int pre_gate = -1;
-  size_t pre_mat_offset = 0;  // [re | im] D x D fp64 in the device arena
 };
 
 // One launch of a program: a single gate, a diagonal batch, a tile pass or a
@@ -469,19 +465,12 @@ void run_step(tsg_state* st, tsg_program* prog, const ProgramStep& step) {
     return;
   }
   if (step.kind == kStepPermute) {
-    const ProgramPermute& pp = prog->permutes[step.index];
-    for (const std::vector<int>& inv : pp.invs) {
+    for (const std::vector<int>& inv : prog->permutes[step.index].invs) {
       tsg::PermuteLaunch pl;
       pl.n = prog->n;
       pl.re = st->re;
       pl.im = st->im;
       for (int q = 0; q < prog->n; ++q) pl.p[q] = inv[q];
-      if (pp.pre_gate >= 0 && &inv == &pp.invs.front()) {
-        const LaunchStructure& ls = prog->gates[pp.pre_gate].ls;
-        pl.pre_k = ls.ks;
-        for (int b = 0; b < ls.ks; ++b) pl.pre_q[b] = ls.sub_targets[b];
-        pl.pre_mat = reinterpret_cast<const double*>(arena + pp.pre_mat_offset);
-      }
       st->prec == 64 ? tsg::launch_permute_f64(pl, st->stream, st->ctx->num_sms)
                      : tsg::launch_permute_f32(pl, st->stream, st->ctx->num_sms);
     }
@@ -1513,36 +1502,8 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
       if (st.is_permute) {
         step.kind = kStepPermute;
         step.index = static_cast<int>(prog->permutes.size());
-        ProgramPermute pp = compose_permutation(prog, st.gates);
+        prog->permutes.push_back(compose_permutation(prog, st.gates));
         for (size_t i = 1; i < st.gates.size(); ++i) prog->gates[st.gates[i]].in_batch = true;
-        // Absorb the standalone gate right before the run (QFT-30: the last H
-        // fused with two of the bit-reversal swaps) when its qubits are tile
-        // qubits of the first launch: the permutation kernel applies it to every
-        // tile it loads, one sweep saved.  TSG_NO_PERMUTE_PRE=1 keeps it apart.
-        static const bool no_pre = std::getenv("TSG_NO_PERMUTE_PRE") != nullptr;
-        if (!no_pre && !prog->steps.empty() && prog->steps.back().kind == kStepGate) {
-          ProgramGate& pg = prog->gates[prog->steps.back().gate];
-          const LaunchStructure& ls = pg.ls;
-          const uint64_t tile = tsg::permute_tile_mask(pp.invs.front().data(), prog->n);
-          bool ok = ls.controls.empty() && ls.ks >= 1 && ls.ks <= 5 && ls.klass != KernelClass::Identity;
-          for (int q : ls.sub_targets) ok = ok && ((tile >> q) & 1u);
-          if (ok) {
-            const size_t D = size_t{1} << ls.ks;
-            pp.pre_gate = prog->steps.back().gate;
-            pp.pre_mat_offset = (arena.size() + 255) & ~size_t{255};
-            arena.resize(pp.pre_mat_offset + 2 * D * D * sizeof(double));
-            double* m = reinterpret_cast<double*>(arena.data() + pp.pre_mat_offset);
-            for (size_t e = 0; e < D * D; ++e) {
-              m[e] = ls.sub_re[e];
-              m[D * D + e] = ls.sub_im[e];
-            }
-            step.gate = pp.pre_gate;
-            step.n_gates += 1;
-            pg.in_batch = true;
-            prog->steps.pop_back();
-          }
-        }
-        prog->permutes.push_back(std::move(pp));
       } else if (st.is_pass) {
         step.kind = kStepPass;
         step.index = static_cast<int>(prog->passes.size());
@@ -2447,7 +2408,6 @@ int tsg_program_step_info(const tsg_program* prog, uint64_t i, tsg_step_info* ou
     if (st.kind == kStepPermute) {
       const size_t sweeps = prog->permutes[st.index].invs.size();
       name = sweeps == 1 ? "k_permute" : "k_permute x" + std::to_string(sweeps);
-      if (prog->permutes[st.index].pre_gate >= 0) name += " +gate";  // the absorbed gate before the run
     } else if (st.kind == kStepPass) {
       const ProgramPass& pp = prog->passes[st.index];
       out->n_high = pp.launch.tile_log2 - pp.launch.run_log2;

@@ -131,38 +131,3 @@ def test_qft_with_permute_step_analytic():
     y = np.arange(1 << n)
     want = np.exp(2j * np.pi * ((x * y) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
     assert np.abs(sv.amplitudes() - want).max() <= 1e-10
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("prec", [64, 32])
-@pytest.mark.parametrize("pre_targets,absorbed", [([0, 1, 14, 15], True), ([2, 13], True), ([0, 7, 8, 9], False)])
-def test_permute_step_absorbs_the_gate_before(pre_targets, absorbed, prec):
-    """The standalone gate right before a permutation run, on tile qubits of
-    the permutation launch (the run bits and their images), is applied by the
-    permutation kernel to every tile it loads (one sweep saved); elsewhere it
-    keeps its own launch.  Against the oracle and TSG_NO_PERMUTE_PRE=1."""
-    n = 16
-    pairs = [(i, 15 - i) for i in range(8)]  # bit reversal: tile qubits {0..4} + {11..15}
-    rng = np.random.default_rng(len(pre_targets) + 3)
-    k = len(pre_targets)
-    before = [([3, 8, 9], random_gate_matrix(3, 7, "dense")), (pre_targets, random_gate_matrix(k, 8, "dense"))]
-    c = swap_circuit(n, pairs, (before, []))
-    psi0 = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
-    psi0 /= np.linalg.norm(psi0)
-    dt = np.float64 if prec == 64 else np.float32
-    psi0 = psi0.real.astype(dt).astype(np.float64) + 1j * psi0.imag.astype(dt).astype(np.float64)
-    sv, prog = _run(c, prec, psi0)
-    ref, pref = _run(c, prec, psi0, {"TSG_NO_PERMUTE_PRE": "1"})
-    kinds = [s["kernel"] for s in prog.steps()]
-    # absorbed exactly when the gate is a launch of its own right before the run
-    # (a cheap one may sit in a tile pass instead) and its qubits are tile qubits
-    st = pref.steps()
-    pi = next(i for i, s in enumerate(st) if s["kernel"].startswith("k_permute"))
-    alone = pi > 0 and st[pi - 1]["kind"] == "gate" and st[pi - 1]["first_gate"] == 1
-    assert ("k_permute +gate" in kinds) == (alone and absorbed), (kinds, st)
-    if absorbed and prec == 64:
-        assert alone  # the dense 4-qubit complex128 case always runs on its own
-    ore, oim = psi0.real.astype(dt), psi0.imag.astype(dt)
-    ob.run_circuit(to_oracle(c), ore, oim)
-    assert ts.compare_states(sv, (ore.astype(np.float64), oim.astype(np.float64))) <= BAR[prec]
-    assert ts.compare_states(sv, ref) <= (1e-14 if prec == 64 else 1e-6)
