@@ -46,9 +46,6 @@ struct PassConfig {
   // testing: every eligible gate joins (no cost test, single-gate passes allowed);
   // pass_config() sets it when the environment has TSG_PASS_FORCE=1
   bool force = false;
-  // commutation-aware grouping window (plan_passes; TSG_PASS_LOOKAHEAD, default
-  // 256); 0: the in-order planner only
-  int lookahead = 256;
 };
 
 // Whether a program over n qubits gets JIT-compiled passes (the runtime's
@@ -87,16 +84,6 @@ std::vector<LaunchStructure> split_blocks(const LaunchStructure& ls, int precisi
 // moves bit b of the sub-index to bit sigma[b] (SWAP and products of SWAPs,
 // e.g. QFT's bit-reversal layer after fusion): the gate permutes qubits.
 bool qubit_permutation(const LaunchStructure& ls, std::vector<int>* sigma);
-
-// G = P_sigma . A, with A acting on fewer of G's qubits than G and P_sigma a
-// permutation of G's qubits (bit b of the sub-index moves to bit sigma[b], as
-// in qubit_permutation): A is G's matrix with its rows permuted, so the split
-// is exact.  Tries every non-identity permutation of G's k <= 5 bits and keeps
-// the one whose A touches the fewest qubits (at least one); false when none
-// touches fewer than k.  QFT's last fused block -- an H merged with two of the
-// bit-reversal swaps -- splits into the H (a one-qubit gate a tile pass takes)
-// and the swaps (which join the permutation run).
-bool factor_qubit_permutation(const Gate& g, Gate* a, std::vector<int>* sigma);
 
 // How one gate can be executed inside a pass (or not at all).
 PassRole pass_role(const LaunchStructure& ls, const PassConfig& cfg);

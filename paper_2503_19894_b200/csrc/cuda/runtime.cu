@@ -217,11 +217,6 @@ struct ProgramGate {
   std::vector<size_t> sub_mat;  // arena offset, or SIZE_MAX without a device matrix
   int batch = -1;          // >= 0: first gate of diagonal batch `batch`
   bool in_batch = false;   // applied by an earlier gate's batch launch
-  // factored gate (tilesim::factor_qubit_permutation): plan / ls / launch
-  // apply A, and this qubit permutation of post_targets (bit b -> post_sigma[b])
-  // runs first in the permutation step that follows
-  std::vector<int> post_targets, post_sigma;
-  bool post_used = false;
 };
 
 struct ProgramBatch {
@@ -260,7 +255,6 @@ struct tsg_program {
   tsg_ctx* ctx = nullptr;
   int n = 0;
   int prec = 64;
-  double zero_tol = 1e-8, one_tol = 1e-8;
   std::vector<ProgramGate> gates;
   std::vector<ProgramBatch> batches;
   std::vector<ProgramPass> passes;
@@ -1453,17 +1447,10 @@ bool split_pays(const LaunchStructure& ls, const std::vector<LaunchStructure>& p
 // the bit at t[b] to t[sigma[b]].  A permutation that is not an involution
 // is split cycle by cycle into I2 o I1 (reflections of each cycle), applied
 // as the sweep with I2, then the sweep with I1.
-ProgramPermute compose_permutation(const tsg_program* prog, const std::vector<int>& gates,
-                                   const ProgramGate* lead = nullptr) {
+ProgramPermute compose_permutation(const tsg_program* prog, const std::vector<int>& gates) {
   const int n = prog->n;
   std::vector<int> src(n);
   for (int q = 0; q < n; ++q) src[q] = q;
-  if (lead) {  // the permutation split off the gate before the run (applied first)
-    std::vector<int> next = src;
-    for (size_t b = 0; b < lead->post_sigma.size(); ++b)
-      next[lead->post_targets[lead->post_sigma[b]]] = src[lead->post_targets[b]];
-    src = std::move(next);
-  }
   for (int gi : gates) {
     const LaunchStructure& ls = prog->gates[gi].ls;
     std::vector<int> sigma;
@@ -1499,80 +1486,23 @@ ProgramPermute compose_permutation(const tsg_program* prog, const std::vector<in
   return out;
 }
 
-// A gate right before a run of qubit permutations that is itself a qubit
-// permutation times a gate on fewer qubits (tilesim::factor_qubit_permutation)
-// is split: the smaller gate A takes the gate's place (a tile pass can take
-// it), the permutation joins the run's permutation step.  QFT-30: the last H
-// fused with two swaps -- a 4-qubit DMMA sweep -- becomes a one-qubit op in
-// the last pass.  TSG_NO_PERM_FACTOR=1 keeps such gates whole.
-bool factor_before_permutations(tsg_program* prog, const PassConfig& cfg, std::vector<unsigned char>& arena) {
-  const char* off = std::getenv("TSG_NO_PERM_FACTOR");
-  if ((off && *off && *off != '0') || cfg.min_permute_run <= 0 || std::getenv("TSG_NO_PERMUTE")) return false;
-  bool any = false;
-  const int G = static_cast<int>(prog->gates.size());
-  std::vector<char> perm(G, 0);
-  for (int i = 0; i < G; ++i) perm[i] = qubit_permutation(prog->gates[i].ls, nullptr);
-  for (int i = 0; i < G; ++i) {
-    ProgramGate& pg = prog->gates[i];
-    if (perm[i] || pg.ls.klass == KernelClass::Identity || pg.plan.gate.k() > 5) continue;
-    int run = 0;  // consecutive permutations after it (identities skipped)
-    for (int j = i + 1; j < G; ++j) {
-      if (prog->gates[j].ls.klass == KernelClass::Identity) continue;
-      if (!perm[j]) break;
-      ++run;
-    }
-    if (run + 1 < cfg.min_permute_run || run == 0) continue;
-    Gate a;
-    std::vector<int> sigma;
-    if (!factor_qubit_permutation(pg.plan.gate, &a, &sigma)) continue;
-    pg.post_targets = pg.plan.gate.targets;
-    pg.post_sigma = sigma;
-    any = true;
-    pg.plan = plan_kernel(a, prog->n, 0, prog->zero_tol, prog->one_tol, false);
-    pg.ls = prog->prec == 64 ? pg.plan.launch : derive_launch(pg.plan, nullptr, prog->prec);
-    pg.launch = make_launch(pg.plan, pg.ls);
-    pg.has_mat = false;
-    if (needs_tile_matrix(pg.launch, prog->prec)) {
-      const auto bytes = tile_matrix_bytes(pg.ls, pg.launch);
-      pg.mat_offset = (arena.size() + 255) & ~size_t{255};
-      arena.resize(pg.mat_offset + bytes.size());
-      std::copy(bytes.begin(), bytes.end(), arena.begin() + pg.mat_offset);
-      pg.has_mat = true;
-    }
-  }
-  return any;
-}
-
 // Steps of a program: tile passes (tilesim/pass.hpp) when the state holds at
 // least one tile, else per-gate launches with diagonal batches.
 void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
   const PassConfig cfg = pass_config(prog->prec, prog->n);
   const bool use_pass = !std::getenv("TSG_NO_PASS") && prog->n >= cfg.tile_log2;
   if (use_pass) {
-    PassConfig pcfg = cfg;
-    // a split-off permutation is not in the planner's gate list: no gate may be
-    // hoisted across its run, so those programs keep the in-order planner
-    if (factor_before_permutations(prog, cfg, arena)) pcfg.lookahead = 0;
     std::vector<LaunchStructure> ls;
     ls.reserve(prog->gates.size());
     for (const ProgramGate& pg : prog->gates) ls.push_back(pg.ls);
-    for (const PassStep& st : plan_passes(ls, prog->n, pcfg)) {
+    for (const PassStep& st : plan_passes(ls, prog->n, cfg)) {
       ProgramStep step;
       step.gate = st.gates.front();
       step.n_gates = static_cast<int>(st.gates.size());
       if (st.is_permute) {
         step.kind = kStepPermute;
         step.index = static_cast<int>(prog->permutes.size());
-        // the gate right before the run (identities skipped) may have had a
-        // qubit permutation split off: it runs first, inside this step
-        ProgramGate* lead = nullptr;
-        for (int gi = st.gates.front() - 1; gi >= 0; --gi) {
-          if (prog->gates[gi].ls.klass == KernelClass::Identity && prog->gates[gi].post_sigma.empty()) continue;
-          if (!prog->gates[gi].post_sigma.empty()) lead = &prog->gates[gi];
-          break;
-        }
-        prog->permutes.push_back(compose_permutation(prog, st.gates, lead));
-        if (lead) lead->post_used = true;
+        prog->permutes.push_back(compose_permutation(prog, st.gates));
         for (size_t i = 1; i < st.gates.size(); ++i) prog->gates[st.gates[i]].in_batch = true;
       } else if (st.is_pass) {
         step.kind = kStepPass;
@@ -1586,8 +1516,6 @@ void plan_steps(tsg_program* prog, std::vector<unsigned char>& arena) {
       }
       prog->steps.push_back(step);
     }
-    for (const ProgramGate& pg : prog->gates)
-      if (!pg.post_sigma.empty() && !pg.post_used) throw SimError("factored gate: its permutation found no permutation step");
     // standalone 5..6-qubit sub-gates with block qubits: one launch per block
     // (2^-|B| of the state each, 2^|E|-qubit sub-gates off the FP64 roof)
     if (!std::getenv("TSG_NO_BLOCK_SPLIT"))
@@ -1757,8 +1685,6 @@ std::unique_ptr<tsg_program> plan_program(tsg_ctx* ctx, const Circuit& fused, do
   prog->ctx = ctx;
   prog->n = fused.n_qubits;
   prog->prec = precision_bits;
-  prog->zero_tol = zero_tol;
-  prog->one_tol = one_tol;
   const uint64_t amp = precision_bits == 64 ? 16 : 8;
   for (const Gate& g : fused.gates) {
     ProgramGate pg;

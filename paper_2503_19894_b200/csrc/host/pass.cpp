@@ -51,7 +51,6 @@ PassConfig pass_config(int precision_bits, int n_qubits) {
       c.perm_sweeps_smem = 0.5;
     }
   }
-  if (const char* e = std::getenv("TSG_PASS_LOOKAHEAD")) c.lookahead = std::max(0, std::atoi(e));
   // calibration experiments: TSG_PASS_COSTS="base,diag,g1,g2,g3,g4,g5,max_gen_ks"
   if (const char* e = std::getenv("TSG_PASS_COSTS")) {
     double v[8];
@@ -259,71 +258,6 @@ bool qubit_permutation(const LaunchStructure& ls, std::vector<int>* sigma) {
   return true;
 }
 
-bool factor_qubit_permutation(const Gate& g, Gate* a, std::vector<int>* sigma) {
-  const int k = g.k();
-  if (k < 2 || k > 5) return false;
-  const uint64_t D = uint64_t{1} << k;
-  std::vector<int> bits(k), best_sigma;
-  for (int b = 0; b < k; ++b) bits[b] = b;
-  uint64_t best_s = 0;
-  int best_size = k;
-  std::vector<cplx> A(D * D);
-  do {
-    bool identity = true;
-    for (int b = 0; b < k; ++b) identity = identity && bits[b] == b;
-    if (identity) continue;
-    // A[r][c] = G[pi(r)][c], pi(r) = sum_b r_b << sigma(b)
-    for (uint64_t r = 0; r < D; ++r) {
-      uint64_t pr = 0;
-      for (int b = 0; b < k; ++b) pr |= ((r >> b) & 1u) << bits[b];
-      for (uint64_t c = 0; c < D; ++c) A[r * D + c] = g.matrix.at(pr, c);
-    }
-    uint64_t s_mask = 0;  // bits where A is not the identity times the rest
-    for (int b = 0; b < k; ++b) {
-      const uint64_t B = uint64_t{1} << b;
-      bool trivial = true;
-      for (uint64_t r = 0; r < D && trivial; ++r)
-        for (uint64_t c = 0; c < D && trivial; ++c) {
-          if (((r ^ c) & B) != 0) trivial = A[r * D + c] == cplx(0.0, 0.0);
-          else if (!(r & B)) trivial = A[r * D + c] == A[(r | B) * D + (c | B)];
-        }
-      if (!trivial) s_mask |= B;
-    }
-    const int size = __builtin_popcountll(s_mask);
-    if (size >= 1 && size < best_size) {
-      best_size = size;
-      best_s = s_mask;
-      best_sigma = bits;
-    }
-  } while (std::next_permutation(bits.begin(), bits.end()));
-  if (best_sigma.empty()) return false;
-  // A on the qubits of S: its block at the other bits = 0
-  std::vector<int> sb;
-  for (int b = 0; b < k; ++b)
-    if ((best_s >> b) & 1u) sb.push_back(b);
-  const int ka = static_cast<int>(sb.size());
-  const uint64_t Da = uint64_t{1} << ka;
-  GateMatrix m(ka);
-  auto dep = [&](uint64_t x) {
-    uint64_t y = 0;
-    for (int i = 0; i < ka; ++i) y |= ((x >> i) & 1u) << sb[i];
-    return y;
-  };
-  for (uint64_t r = 0; r < Da; ++r) {
-    uint64_t pr = 0;
-    const uint64_t rr = dep(r);
-    for (int b = 0; b < k; ++b) pr |= ((rr >> b) & 1u) << best_sigma[b];
-    for (uint64_t c = 0; c < Da; ++c) m.at(r, c) = g.matrix.at(pr, dep(c));
-  }
-  a->matrix = std::move(m);
-  a->targets.clear();
-  for (int b : sb) a->targets.push_back(g.targets[b]);
-  a->name.clear();
-  a->params.clear();
-  *sigma = best_sigma;
-  return true;
-}
-
 // Qubits a gate touches and the ones it mixes (as bit masks), for the
 // commutation test of the lookahead planner: two gates commute when every
 // qubit they share is a block (non-mixed) qubit of both -- for each value of
@@ -509,7 +443,10 @@ static double plan_sweeps(const std::vector<PassStep>& steps, const std::vector<
 // passes ~3% slower (profiles/r02/planner_ab.txt).  TSG_PASS_LOOKAHEAD=<window>
 // sets the window (default 256; 0: in-order only).
 std::vector<PassStep> plan_passes(const std::vector<LaunchStructure>& gates, int n, const PassConfig& cfg) {
-  const int window = cfg.lookahead;
+  static const int window = [] {
+    const char* e = std::getenv("TSG_PASS_LOOKAHEAD");
+    return e ? std::max(0, std::atoi(e)) : 256;
+  }();
   std::vector<PassStep> in_order = plan_passes_window(gates, n, cfg, 0);
   if (window == 0 || cfg.force) return in_order;
   std::vector<PassStep> ahead = plan_passes_window(gates, n, cfg, window);

@@ -131,29 +131,3 @@ def test_qft_with_permute_step_analytic():
     y = np.arange(1 << n)
     want = np.exp(2j * np.pi * ((x * y) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
     assert np.abs(sv.amplitudes() - want).max() <= 1e-10
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("prec", [64, 32])
-def test_qft_last_block_factored(prec, monkeypatch):
-    """QFT's last fused block (H with two of the bit-reversal swaps) splits into
-    the H -- taken by the last tile pass -- and the swaps, which join the
-    permutation step (tilesim::factor_qubit_permutation): one sweep fewer,
-    the same state as the unsplit program and the closed form."""
-    n, x = 18, 0x2B5C1
-    fused, _ = ts.run_fusion(ts.gen_benchmark("qft", n), ts.FusionConfig(k_max=5))
-    pf = ts.Program(fused, PREC[prec])
-    monkeypatch.setenv("TSG_NO_PERM_FACTOR", "1")
-    p0 = ts.Program(fused, PREC[prec])
-    kf = [s["kernel"] for s in pf.steps()]
-    k0 = [s["kernel"] for s in p0.steps()]
-    assert len(kf) == len(k0) - 1, (kf, k0)
-    assert kf[-1].startswith("k_permute") and kf[-2].startswith("k_pass"), kf
-    a = ts.Statevector(n, PREC[prec]).init_basis(x)
-    b = ts.Statevector(n, PREC[prec]).init_basis(x)
-    pf.run(a)
-    p0.run(b)
-    assert ts.compare_states(a, b) <= (1e-13 if prec == 64 else 1e-6)
-    y = np.arange(1 << n)
-    want = np.exp(2j * np.pi * ((x * y) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
-    assert np.abs(a.amplitudes() - want).max() <= (1e-10 if prec == 64 else 1e-5)
