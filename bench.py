@@ -240,7 +240,10 @@ def run_sharded(args, rank, world, local, dist):
         raise SystemExit("sharding needs a power-of-two GPU count")
     g = world.bit_length() - 1
     n = args.n
-    ctx = ts.Context(local)
+    # one GPU per rank; on a box with fewer GPUs than ranks (a functional check
+    # only) ranks share devices round-robin and the line says so
+    n_dev = max(1, ts.device_count())
+    ctx = ts.Context(local % n_dev)
 
     def bcast_uid():
         obj = [ts.DistState.unique_id() if rank == 0 else None]
@@ -326,7 +329,8 @@ def run_sharded(args, rank, world, local, dist):
             "data": "synthetic (generated QFT-30 / RQC-30 circuits, basis-state input)",
             "config": config_block(n, args.kmax, f"{sq['original_gate_count']}->{sq['fused_block_count']}",
                                    f"{sr['original_gate_count']}->{sr['fused_block_count']}"),
-            "parallelism": f"{g} global qubits over {world} GPUs (one process per GPU, peer-memory exchanges)",
+            "parallelism": f"{g} global qubits over {world} GPUs (one process per GPU, peer-memory exchanges)"
+                           + ("" if n_dev >= world else f"; FUNCTIONAL CHECK ONLY: {world} ranks share {n_dev} GPU(s)"),
             "fused_stream_sha16": fused_stream_sha16([product_stream(fq), product_stream(fr)]),
             "exchange": {"exchanges_per_step": iq["exchanges"] + ir["exchanges"],
                          "pipelined_per_step": iq["pipelined_exchanges"] + ir["pipelined_exchanges"],
