@@ -10,11 +10,12 @@
 //   [Yr | Yi] (G x 2D) = [Xr | Xi] (G x 2D) . B^T,   B = | Mr  -Mi |
 //                                                         | Mi   Mr |
 //
-// (MMA M = 128 groups, N = K = 2D).  Operands are split into signed 8-bit
+// (MMA M = 128 groups, N = K = 2D).  Operands are split into 8-bit integer
 // slices (the Ozaki scheme): every group row x is scaled by a power of two
 // s with |x| / s < 1 and written as x = s (a1 2^-7 + a2 2^-14 + a3 2^-21 + r)
-// with integer slices |a_i| <= 127 (round to nearest: |r| <= 2^-22); every
-// row of B likewise with its own power of two t and slices b_j.  Slice
+// with integer slices (a1 signed, a2, a3 in [0, 127]: the digits of x's
+// 21-bit rounding, |r| <= 2^-22); every row of B likewise with its own power
+// of two t and signed slices |b_j| <= 127 (round to nearest per digit).  Slice
 // products are integers and their K-sums stay far below 2^31, so the tensor
 // core computes them EXACTLY; three INT32 accumulators collect the levels
 // i + j = 2, 3, 4:
@@ -129,19 +130,20 @@ __device__ __forceinline__ float slice_scale(float m) {
   if (!(m > 0.0f)) return 1.0f;
   return __uint_as_float((__float_as_uint(m) + 0x007fffffu) & 0xff800000u);
 }
-// Slices of u = x / s * 128 (|u| <= 127): a1, a2, a3 as the low byte of the
-// magic-number rounding (round to nearest even, two's complement)
-__device__ __forceinline__ void slice3(float u, uint32_t& b1, uint32_t& b2, uint32_t& b3) {
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-  float t = u + kMagic;
-  float a = t - kMagic;
-  b1 = __float_as_uint(t);
-  u = (u - a) * 128.0f;
-  t = u + kMagic;
-  a = t - kMagic;
-  b2 = __float_as_uint(t);
-  u = (u - a) * 128.0f;
-  b3 = __float_as_uint(u + kMagic);
+// Slices of four values u = x / s * 128 (|u| <= 127) from their 21-bit
+// roundings V = rint(u 2^14): t = u 2^14 + 1.5 2^23 (one FFMA, round to
+// nearest even) holds V in two's complement in its low 22 bits, and V's
+// digits are a1 = V >> 14 (signed, [-128, 127]), a2 = (V >> 7) & 127 and
+// a3 = V & 127 (unsigned 7-bit: valid INT8), x = s (a1 2^-7 + a2 2^-14 +
+// a3 2^-21) + r, |r| <= 2^-22 s.  Packed four per 32-bit TMEM column with
+// byte permutes and two shifts per digit word (no per-digit float work).
+__device__ __forceinline__ void digits4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t& w1,
+                                        uint32_t& w2, uint32_t& w3) {
+  const uint32_t lo01 = __byte_perm(t0, t1, 0x5410), lo23 = __byte_perm(t2, t3, 0x5410);  // bits 0-15 of each
+  const uint32_t mi01 = __byte_perm(t0, t1, 0x6521), mi23 = __byte_perm(t2, t3, 0x6521);  // bits 8-23 of each
+  w3 = __byte_perm(lo01, lo23, 0x6420) & 0x7f7f7f7fu;                                     // bits 0-6
+  w2 = __byte_perm(lo01 >> 7, lo23 >> 7, 0x6420) & 0x7f7f7f7fu;                           // bits 7-13
+  w1 = __byte_perm(mi01 >> 6, mi23 >> 6, 0x6420);                                         // bits 14-21
 }
 // int32 (|v| < 2^22) to float, exactly
 __device__ __forceinline__ float small_i2f(uint32_t v) { return __uint_as_float(v + 0x4B400000u) - 12582912.0f; }
@@ -317,7 +319,8 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
     const float sg = slice_scale(m);
-    const float inv = __uint_as_float(0x82800000u - __float_as_uint(sg));  // 128 / sg (powers of two: (134 - E) << 23)
+    // 128 / sg * 2^14 (powers of two: (148 - E) << 23)
+    const float inv = __uint_as_float(0x89800000u - __float_as_uint(sg));
     // this thread's part of the group's row of the three A slices, straight
     // into the group's TMEM lane
 #pragma unroll
@@ -326,12 +329,11 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
       uint32_t w1[8], w2[8], w3[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        uint32_t e1[4], e2[4], e3[4];
+        constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+        uint32_t t[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) slice3(v[4 * (cc + q) + e] * inv, e1[e], e2[e], e3[e]);
-        w1[q] = __byte_perm(__byte_perm(e1[0], e1[1], 0x0040), __byte_perm(e1[2], e1[3], 0x0040), 0x5410);
-        w2[q] = __byte_perm(__byte_perm(e2[0], e2[1], 0x0040), __byte_perm(e2[2], e2[3], 0x0040), 0x5410);
-        w3[q] = __byte_perm(__byte_perm(e3[0], e3[1], 0x0040), __byte_perm(e3[2], e3[3], 0x0040), 0x5410);
+        for (int e = 0; e < 4; ++e) t[e] = __float_as_uint(fmaf(v[4 * (cc + q) + e], inv, kMagic));
+        digits4(t[0], t[1], t[2], t[3], w1[q], w2[q], w3[q]);
       }
       tmem_st8(row + 3 * U::N + 0 * U::ACOLS + c, w1);
       tmem_st8(row + 3 * U::N + 1 * U::ACOLS + c, w2);
