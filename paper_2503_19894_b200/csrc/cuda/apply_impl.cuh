@@ -10,6 +10,9 @@
 #include <cstdlib>
 #include <string>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "kernels.cuh"
 #include "kernels_dmma.cuh"
 #include "kernels_stream.cuh"
@@ -305,6 +308,16 @@ bool try_stream(const GateLaunch& g, cudaStream_t s, int num_sms) {
 }
 
 // ------------------------------------------------------------ stream_dmma
+// TSG_DMMA_TMA: 0 off, 1 loads of the direct-out (FP64-bound) kernels,
+// 2 loads of every kernel, 3 loads and write-backs
+inline int dmma_tma_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("TSG_DMMA_TMA");
+    return e && *e ? std::atoi(e) : 1;
+  }();
+  return mode;
+}
+
 template <typename Real, int KS, int LOG2G_ = DShape<Real, KS>::LOG2G>
 bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, int* stages, bool simt,
                    bool few_tiles = false) {
@@ -407,14 +420,29 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   // smaller bulk copies measured slower for the HBM-bound ks <= 4 kernels
   const bool direct_out = KS >= 5 || (sizeof(Real) == 4 && KS >= 4);  // k_stream_dmma kDirectOut
   if (direct_out && !simt && L > chunk && wavefronts(chunk) < wavefronts(L)) p.chunk_log2 = chunk;
+  // TMA tile loads (dmma_tma_plan) take boxes of at most 256 elements per
+  // row: a longer padded run is cut into the chunk size with the fewest
+  // wavefronts instead
+  if (direct_out && !simt && dmma_tma_mode() >= 1 && p.chunk_log2 == L && (1u << L) + pad > 256 && n_run > 0) {
+    int best = 7;
+    for (int c = 6; c >= 5; --c)
+      if (wavefronts(c) < wavefronts(best)) best = c;
+    p.chunk_log2 = best;
+  }
   layout(p.chunk_log2, &p.chunk_stride, &p.run_stride);
   for (int j = 0; j < (1 << KS); ++j) {
     const uint32_t w = low_of[j];
     p.soff[j] = run_of[j] * p.run_stride + (w >> p.chunk_log2) * p.chunk_stride + (w & ((1u << p.chunk_log2) - 1));
   }
+  // one run, one chunk: the padding after it serves no bank spread, and
+  // without it the run is a plain (TMA-expressible) box
+  if (p.n_runs == 1 && p.chunk_log2 == L) p.chunk_stride = p.run_stride = 1u << L;
+  // stages start on 128-byte boundaries (TMA tensor-copy destinations)
+  constexpr uint32_t kAlignElems = 128 / sizeof(Real);
+  p.stage_elems = (p.run_stride * static_cast<uint32_t>(p.n_runs) + kAlignElems - 1) / kAlignElems * kAlignElems;
   // Two CTAs per SM beat deeper pipelines (measured): 3 stages when two CTAs
   // still fit in shared memory, else 2.
-  const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(Real);
+  const size_t stage = 2 * size_t{p.stage_elems} * sizeof(Real);
   size_t fixed = 128;  // (complex64 6-qubit geometries serve k_stream_umma, which sizes its own shared memory)
   if constexpr (KS <= 5) fixed += simt ? dmma_m_smem_bytes<Real, KS, true>() : dmma_m_smem_bytes<Real, KS>();
   if constexpr (KS == 6 && sizeof(Real) == 8) fixed += dmma_m_smem_bytes<Real, KS>();
@@ -422,6 +450,90 @@ bool dmma_geometry(const GateLaunch& g, DmmaParams<Real, KS>& p, size_t* smem, i
   *stages = 3 * stage + fixed <= per_cta ? 3 : 2;
   *smem = *stages * stage + fixed;
   return *smem <= 220 * 1024;
+}
+
+// TMA tensor maps for a k_stream_dmma launch (DmmaParams::tmap): the tile's
+// shared-memory layout [runs][chunks][chunk + pad] is one box of a rank-5
+// view of the state --
+//   dim 0  the chunk's amplitudes; the box is pad elements wider than the
+//          dimension, so the padding is zero-filled on loads and skipped on
+//          stores (an unchunked, unpadded run: up to 256 amplitudes, dim 1
+//          takes the rest)
+//   dim 1  chunks of a run
+//   dim 2  tile base >> L (box 1): the tile bases and the run offsets are
+//          disjoint index bits, so this dimension aliases the next two
+//   dim 3, 4  the lowest run bits, as runs of consecutive qubits
+// -- and runs beyond dims 3-4 take one copy each (tma_issues).  Needs 128-byte
+// aligned copy destinations and box widths of at most 256 elements; returns
+// false (per-chunk bulk copies) otherwise.  TSG_DMMA_TMA=0 disables.
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+template <typename Real, int KS>
+bool dmma_tma_plan(const GateLaunch& g, DmmaParams<Real, KS>& p) {
+  static_assert(sizeof(TmaDesc) == sizeof(CUtensorMap), "TmaDesc mirrors CUtensorMap");
+  p.tma_issues = p.tma_store = 0;
+  const int mode = dmma_tma_mode();
+  const bool direct_out = KS >= 5 || (sizeof(Real) == 4 && KS >= 4);  // k_stream_dmma kDirectOut
+  if (mode <= 0 || (mode == 1 && !direct_out) || !tensor_map_encoder()) return false;
+  const uint32_t e0 = 1u << p.chunk_log2, pad = p.chunk_stride - e0;
+  cuuint64_t dim[5] = {1, 1, 1, 1, 1}, stride[4] = {0, 0, 0, 0};
+  cuuint32_t box[5] = {1, 1, 1, 1, 1}, estride[5] = {1, 1, 1, 1, 1};
+  if (pad == 0) {  // one unpadded run: contiguous 2^L amplitudes
+    const uint32_t d0 = std::min<uint32_t>(1u << p.L, 256);
+    dim[0] = box[0] = d0;
+    dim[1] = box[1] = (1u << p.L) / d0;
+    stride[0] = size_t{d0} * sizeof(Real);
+  } else {
+    if (e0 + pad > 256) return false;
+    dim[0] = e0;
+    box[0] = e0 + pad;
+    dim[1] = box[1] = 1u << (p.L - p.chunk_log2);
+    stride[0] = size_t{e0} * sizeof(Real);
+  }
+  if (size_t{box[0]} * sizeof(Real) % 16 != 0) return false;
+  dim[2] = uint64_t{1} << (g.n - p.L);
+  stride[1] = (size_t{1} << p.L) * sizeof(Real);
+  // run bit b is qubit ctz(roff[1 << b]); dims 3 and 4 take the lowest two
+  // groups of consecutive qubits
+  int n_run = 0;
+  while ((1 << n_run) < p.n_runs) ++n_run;
+  int b = 0;
+  for (int d = 3; d <= 4 && b < n_run; ++d) {
+    const int q0 = __builtin_ctzll(p.roff[1 << b]);
+    int m = 1;
+    while (b + m < n_run && __builtin_ctzll(p.roff[1 << (b + m)]) == q0 + m) ++m;
+    dim[d] = box[d] = 1u << m;
+    stride[d - 1] = (size_t{1} << q0) * sizeof(Real);
+    b += m;
+  }
+  for (int d = 2; d < 4; ++d)
+    if (stride[d] == 0) stride[d] = stride[d - 1];  // unused (size 1) dimensions
+  p.tma_shift = b;
+  p.tma_issue_elems = (1u << b) * p.run_stride;
+  const int issues = p.n_runs >> b;
+  if (issues > 1 && (p.tma_issue_elems * sizeof(Real)) % 128 != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(g.re) | reinterpret_cast<uintptr_t>(g.im)) & 15u) return false;
+  const CUtensorMapDataType type = sizeof(Real) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  for (int a = 0; a < 2; ++a) {
+    void* base = a ? g.im : g.re;
+    if (tensor_map_encoder()(reinterpret_cast<CUtensorMap*>(&p.tmap[a]), type, 5, base, dim, stride, box, estride,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  p.tma_issues = issues;
+  p.tma_store = mode >= 3 && !direct_out;
+  return true;
 }
 
 template <typename Real, int KS, int STAGES, bool SP, bool SIMT>
@@ -532,10 +644,11 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   p.re = static_cast<Real*>(g.re);
   p.im = static_cast<Real*>(g.im);
   p.mat = static_cast<const double*>(g.dev_mat);
+  dmma_tma_plan<Real, KS>(g, p);
   static const bool debug = std::getenv("TSG_DMMA_DEBUG") != nullptr;
   if (debug)
-    std::fprintf(stderr, "dmma ks=%d L=%d chunk=%d runs=%d stages=%d smem=%zu tiles=%d/%d/%d of %d sparse=%d jit=%d\n", KS,
-                 p.L, p.chunk_log2, p.n_runs, st.stages, st.smem, __builtin_popcount(p.nzblk[0]),
+    std::fprintf(stderr, "dmma ks=%d L=%d chunk=%d runs=%d tma=%d stages=%d smem=%zu tiles=%d/%d/%d of %d sparse=%d jit=%d\n",
+                 KS, p.L, p.chunk_log2, p.n_runs, p.tma_issues, st.stages, st.smem, __builtin_popcount(p.nzblk[0]),
                  __builtin_popcount(p.nzblk[1]), __builtin_popcount(p.nzblk[2]), S::RB * S::KST, st.sparse ? 1 : 0,
                  g.jit ? 1 : 0);
   if constexpr (sizeof(Real) == 8 && KS <= 5) {

@@ -111,6 +111,17 @@ struct DmmaParams {
   uint32_t soff[1 << KS];  // shared offset of element j (padded runs and chunks)
   uint64_t goff[1 << KS];  // global offset of element j from the tile base
   uint32_t nzblk[3];       // bit (rb * KST + ks): block of Mr / Mi / Ms is nonzero
+  uint32_t stage_elems;    // shared elements per array and stage (a multiple of 128 bytes)
+  // TMA tensor-map tile copies (dmma_tma_plan; tma_issues = 0: one bulk copy
+  // per chunk).  The maps view re / im as [chunk + pad | chunks per run |
+  // tile (stride 2^L) | run bits | run bits]; copy i moves runs
+  // [i << tma_shift, (i + 1) << tma_shift) at tile coordinate
+  // (base + roff[i << tma_shift]) >> L, tma_issue_elems shared elements apart.
+  int tma_issues;
+  int tma_store;  // write-back through the maps too (else per-chunk bulk stores)
+  int tma_shift;
+  uint32_t tma_issue_elems;
+  TmaDesc tmap[2];
 };
 
 // A pure function of its operands (no volatile): the compiler may schedule
@@ -343,7 +354,7 @@ __device__ __forceinline__ void k_stream_dmma_body(const DmmaParams<Real, KS>& p
   constexpr bool kDirectOut =
       KS >= (sizeof(Real) == 4 ? TSG_DMMA_DIRECT_OUT_MIN_KS_F32 : TSG_DMMA_DIRECT_OUT_MIN_KS) && !kSimt;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
+  const uint32_t stage_elems = p.stage_elems;
   double* mfrag = reinterpret_cast<double*>(smem_raw);  // [3][KST][RB][32] when !MREG
   Real* buf = reinterpret_cast<Real*>(smem_raw + dmma_m_smem_bytes<Real, KS, SIMT>());  // [STAGES][2][stage_elems]
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(buf) +
@@ -397,6 +408,17 @@ __device__ __forceinline__ void k_stream_dmma_body(const DmmaParams<Real, KS>& p
       lstream.advance();
       Real* dr = buf + (2 * s) * stage_elems;
       Real* di = dr + stage_elems;
+      if (p.tma_issues > 0) {  // a few tensor copies per tile (padding included)
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], 2u * sizeof(Real) * p.run_stride * static_cast<uint32_t>(p.n_runs));
+          for (int i = 0; i < p.tma_issues; ++i) {
+            const int c2 = static_cast<int>((base + p.roff[i << p.tma_shift]) >> p.L);
+            tma_g2s(dr + i * p.tma_issue_elems, &p.tmap[0], c2, &full[s]);
+            tma_g2s(di + i * p.tma_issue_elems, &p.tmap[1], c2, &full[s]);
+          }
+        }
+        return;
+      }
       if (lane == 0) mbar_expect_tx(&full[s], 2u * chunk_bytes * static_cast<uint32_t>(n_chunks));
       __syncwarp();
       for (int c = lane; c < n_chunks; c += 32) {
@@ -423,12 +445,21 @@ __device__ __forceinline__ void k_stream_dmma_body(const DmmaParams<Real, KS>& p
         sstream.advance();
         const Real* sr = buf + (2 * s) * stage_elems;
         const Real* si = sr + stage_elems;
-        for (int c = lane; c < n_chunks; c += 32) {
-          const int r = c >> chunk_shift, q = c & ((1 << chunk_shift) - 1);
-          const uint32_t so = r * p.run_stride + q * p.chunk_stride;
-          const uint64_t go = base + p.roff[r] + (static_cast<uint64_t>(q) << p.chunk_log2);
-          bulk_s2g(p.re + go, sr + so, chunk_bytes);
-          bulk_s2g(p.im + go, si + so, chunk_bytes);
+        if (p.tma_store) {
+          if (lane == 0)
+            for (int i = 0; i < p.tma_issues; ++i) {
+              const int c2 = static_cast<int>((base + p.roff[i << p.tma_shift]) >> p.L);
+              tma_s2g(&p.tmap[0], c2, sr + i * p.tma_issue_elems);
+              tma_s2g(&p.tmap[1], c2, si + i * p.tma_issue_elems);
+            }
+        } else {
+          for (int c = lane; c < n_chunks; c += 32) {
+            const int r = c >> chunk_shift, q = c & ((1 << chunk_shift) - 1);
+            const uint32_t so = r * p.run_stride + q * p.chunk_stride;
+            const uint64_t go = base + p.roff[r] + (static_cast<uint64_t>(q) << p.chunk_log2);
+            bulk_s2g(p.re + go, sr + so, chunk_bytes);
+            bulk_s2g(p.im + go, si + so, chunk_bytes);
+          }
         }
         bulk_commit();
         if (next < p.n_tiles) {

@@ -70,6 +70,25 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// TMA tensor-map copies (cp.async.bulk.tensor, SASS UTMALDG / UTMASTG): the
+// descriptor is an opaque 128-byte CUtensorMap built on the host
+// (cuTensorMapEncodeTiled) and passed inside a __grid_constant__ parameter
+// block; every copy here is rank 5 with only coordinate 2 nonzero.
+struct alignas(64) TmaDesc {
+  unsigned long long w[16];
+};
+__device__ __forceinline__ void tma_g2s(void* dst, const TmaDesc* d, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %2, %3, %2, "
+      "%2}], [%4];" ::"r"(smem_addr(dst)),
+      "l"(d), "r"(0), "r"(c2), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_s2g(const TmaDesc* d, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%2, %2, %3, %2, %2}], [%1];" ::"l"(d),
+               "r"(smem_addr(src)), "r"(0), "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }

@@ -417,6 +417,14 @@ void choose_dmma_perm(tsg::GateLaunch& g, const LaunchStructure& ls) {
       std::copy(P, P + D, best);
     }
   } while (std::next_permutation(bits, bits + g.ks));
+  // A reordered launch pays only when the product then skips its zero tiles
+  // (dmma_setup: sparse at >= 1/4 zero tiles); otherwise the dense product
+  // runs either way and the sorted order keeps each 8-row block of outputs
+  // contiguous -- RQC-30's 5-qubit gate on qubits 0..4 with 88 of 96 tiles
+  // nonzero under its best order: 9.96 ms reordered, 7.7 ms sorted.
+  const int total = 3 * (D / 8) * (D / 4);
+  static const bool any_gain = std::getenv("TSG_DMMA_PERM_ANY") != nullptr;  // round-2 rule (A/B runs)
+  if (!any_gain && 4 * (total - best_tiles) < total) return;
   for (int j = 0; j < D; ++j) g.perm[j] = static_cast<uint8_t>(best[j]);
 }
 
