@@ -750,6 +750,7 @@ bool umma_plan(const GateLaunch& g, DmmaParams<float, KS>& p) {
     for (int j = 0; j < (1 << KS); ++j)
       p.soff[j] = run_of[j] * p.run_stride + (low_of[j] >> 6) * p.chunk_stride + (low_of[j] & 63u);
   }
+  p.stage_elems = (p.run_stride * static_cast<uint32_t>(p.n_runs) + 31u) / 32u * 32u;  // 128-byte stages
   return true;
 }
 
@@ -776,9 +777,10 @@ bool try_umma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   p.re = static_cast<float*>(g.re);
   p.im = static_cast<float*>(g.im);
   p.mat = static_cast<const double*>(g.dev_mat);
+  dmma_tma_plan<float, KS>(g, p);
   // two CTAs per SM (256 TMEM columns each), two stages each; at least 80 KB
   // so that a third CTA never lands on an SM (tcgen05.alloc would wait)
-  const size_t stage = 2 * size_t{p.run_stride} * p.n_runs * sizeof(float);
+  const size_t stage = 2 * size_t{p.stage_elems} * sizeof(float);
   const size_t fixed = umma_fixed_smem<KS>() + 256;
   if constexpr (UmmaShape<KS>::kCtasPerSm == 1) {  // one CTA per SM (all of TMEM): > 114 KB keeps it so
     if (fixed + 2 * stage > 227 * 1024) return false;

@@ -170,7 +170,7 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* b_ops = smem_raw;                                       // [b1 | b2 | b3]
   float* b_scale = reinterpret_cast<float*>(smem_raw + 3 * U::kBBytes);  // t_n 2^-28
-  const uint32_t stage_elems = p.run_stride * static_cast<uint32_t>(p.n_runs);
+  const uint32_t stage_elems = p.stage_elems;
   float* buf = reinterpret_cast<float*>(smem_raw + umma_fixed_smem<KS>());  // [STAGES][2][stage_elems]
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(buf) + sizeof(float) * 2 * STAGES * stage_elems);
   uint64_t* empty = full + STAGES;
@@ -253,6 +253,17 @@ __global__ void __maxnreg__(umma_max_regs<KS>()) k_stream_umma(const __grid_cons
       lstream.advance();
       float* dr = buf + (2 * s) * stage_elems;
       float* di = dr + stage_elems;
+      if (p.tma_issues > 0) {  // tensor-map copies (dmma_tma_plan), padding included
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], 2u * sizeof(float) * p.run_stride * static_cast<uint32_t>(p.n_runs));
+          for (int i = 0; i < p.tma_issues; ++i) {
+            const int c2 = static_cast<int>((base + p.roff[i << p.tma_shift]) >> p.L);
+            tma_g2s(dr + i * p.tma_issue_elems, &p.tmap[0], c2, &full[s]);
+            tma_g2s(di + i * p.tma_issue_elems, &p.tmap[1], c2, &full[s]);
+          }
+        }
+        return;
+      }
       if (lane == 0) mbar_expect_tx(&full[s], 2u * chunk_bytes * static_cast<uint32_t>(n_chunks));
       __syncwarp();
       for (int c = lane; c < n_chunks; c += 32) {
