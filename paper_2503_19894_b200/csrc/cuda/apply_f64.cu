@@ -18,7 +18,7 @@ bool dmma_jit_spec_ks(const GateLaunch& g, std::string* source, std::string* nam
   const char* mode = std::getenv("TSG_DMMA_JIT");  // "2": every launch with a zero tile (experiments)
   const bool every = mode && mode[0] == '2';
   if (st.nonzero == all || (!every && (3 * st.nonzero < all || 3 * st.nonzero > 2 * all))) return false;
-  *source = dmma_jit_source(KS, st.stages, st.p.nzblk, name);
+  *source = dmma_jit_source(KS, st.stages, st.p.nzblk, st.tpose, name);
   return true;
 }
 }  // namespace

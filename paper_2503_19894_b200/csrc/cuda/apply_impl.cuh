@@ -536,9 +536,9 @@ bool dmma_tma_plan(const GateLaunch& g, DmmaParams<Real, KS>& p) {
   return true;
 }
 
-template <typename Real, int KS, int STAGES, bool SP, bool SIMT>
+template <typename Real, int KS, int STAGES, bool SP, bool SIMT, bool TPOSE = false>
 void launch_dmma(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int num_sms) {
-  auto kern = k_stream_dmma<Real, KS, STAGES, SP, SIMT>;
+  auto kern = k_stream_dmma<Real, KS, STAGES, SP, SIMT, TPOSE>;
   static size_t configured_smem = 0;
   if (configured_smem < smem) {
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "dmma smem");
@@ -553,9 +553,12 @@ void launch_dmma(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int
 }
 
 template <typename Real, int KS, int STAGES, bool SP>
-void launch_dmma_pick(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int num_sms, bool simt) {
+void launch_dmma_pick(const DmmaParams<Real, KS>& p, size_t smem, cudaStream_t s, int num_sms, bool simt, bool tpose) {
   if constexpr (sizeof(Real) == 4 && KS <= 3) {
     if (simt) return launch_dmma<Real, KS, STAGES, false, true>(p, smem, s, num_sms);  // SIMT evaluates densely
+  }
+  if constexpr (KS == 5 || (sizeof(Real) == 4 && KS == 4)) {
+    if (tpose) return launch_dmma<Real, KS, STAGES, SP, false, true>(p, smem, s, num_sms);
   }
   if constexpr (KS >= 6) launch_dmma<Real, KS, STAGES, false, false>(p, smem, s, num_sms);
   else launch_dmma<Real, KS, STAGES, SP, false>(p, smem, s, num_sms);
@@ -569,7 +572,8 @@ struct DmmaSetup {
   size_t smem = 0;
   int stages = 3;
   bool simt = false, sparse = false;
-  int nonzero = 0;  // nonzero 8 x 4 tiles of [Mr | Mi | Ms]
+  bool tpose = false;  // transposed product (k_stream_dmma TPOSE): qubit 0 is the first element bit
+  int nonzero = 0;     // nonzero 8 x 4 tiles of [Mr | Mi | Ms]
 };
 
 template <typename Real, int KS>
@@ -584,6 +588,15 @@ bool dmma_setup(const GateLaunch& g, DmmaSetup<Real, KS>& st) {
   for (int b = 0; b < g.ks; ++b) lowest = std::min(lowest, g.sub_targets[b]);
   for (int c = 0; c < g.n_ctrl; ++c) lowest = std::min(lowest, g.ctrl[c]);
   st.simt = sizeof(Real) == 4 && KS <= 3 && lowest >= 5;
+  // direct-out products whose first element bit is qubit 0: two groups are
+  // never adjacent there, two elements are -- the transposed product stores
+  // 2-element vectors (TSG_DMMA_TPOSE=0 disables)
+  static const bool tpose_on = [] {
+    const char* e = std::getenv("TSG_DMMA_TPOSE");
+    return !(e && e[0] == '0');
+  }();
+  const bool direct_out = KS >= 5 || (sizeof(Real) == 4 && KS >= 4);  // k_stream_dmma kDirectOut
+  st.tpose = tpose_on && direct_out && KS <= 5 && !st.simt && g.sub_targets[__builtin_ctz(static_cast<unsigned>(g.perm[1]))] == 0;
   constexpr int D = S::D;
   for (int rb = 0; rb < S::RB; ++rb)
     for (int k = 0; k < S::KST && KS <= 5; ++k) {  // (ks = 6: dense only)
@@ -647,8 +660,8 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   dmma_tma_plan<Real, KS>(g, p);
   static const bool debug = std::getenv("TSG_DMMA_DEBUG") != nullptr;
   if (debug)
-    std::fprintf(stderr, "dmma ks=%d L=%d chunk=%d runs=%d tma=%d stages=%d smem=%zu tiles=%d/%d/%d of %d sparse=%d jit=%d\n",
-                 KS, p.L, p.chunk_log2, p.n_runs, p.tma_issues, st.stages, st.smem, __builtin_popcount(p.nzblk[0]),
+    std::fprintf(stderr, "dmma ks=%d L=%d chunk=%d runs=%d tma=%d tpose=%d stages=%d smem=%zu tiles=%d/%d/%d of %d sparse=%d jit=%d\n",
+                 KS, p.L, p.chunk_log2, p.n_runs, p.tma_issues, st.tpose ? 1 : 0, st.stages, st.smem, __builtin_popcount(p.nzblk[0]),
                  __builtin_popcount(p.nzblk[1]), __builtin_popcount(p.nzblk[2]), S::RB * S::KST, st.sparse ? 1 : 0,
                  g.jit ? 1 : 0);
   if constexpr (sizeof(Real) == 8 && KS <= 5) {
@@ -659,12 +672,12 @@ bool try_dmma(const GateLaunch& g, cudaStream_t s, int num_sms) {
   }
   switch (st.stages) {
     case 3:
-      st.sparse ? launch_dmma_pick<Real, KS, 3, true>(p, st.smem, s, num_sms, st.simt)
-                : launch_dmma_pick<Real, KS, 3, false>(p, st.smem, s, num_sms, st.simt);
+      st.sparse ? launch_dmma_pick<Real, KS, 3, true>(p, st.smem, s, num_sms, st.simt, st.tpose)
+                : launch_dmma_pick<Real, KS, 3, false>(p, st.smem, s, num_sms, st.simt, st.tpose);
       break;
     default:
-      st.sparse ? launch_dmma_pick<Real, KS, 2, true>(p, st.smem, s, num_sms, st.simt)
-                : launch_dmma_pick<Real, KS, 2, false>(p, st.smem, s, num_sms, st.simt);
+      st.sparse ? launch_dmma_pick<Real, KS, 2, true>(p, st.smem, s, num_sms, st.simt, st.tpose)
+                : launch_dmma_pick<Real, KS, 2, false>(p, st.smem, s, num_sms, st.simt, st.tpose);
       break;
   }
   return true;

@@ -210,7 +210,12 @@ struct DmmaStaticNz {
 
 // Consumer warps of k_stream_dmma: Y = M X on the DMMA pipe for row block RB
 // (RBC >= 0: a compile-time row block, RBC < 0: rb at run time).
-template <typename Real, int KS, int STAGES, typename NZ, bool MREG, bool kDirectOut, int RBC>
+// TPOSE (direct-out only): the product is computed transposed, Y^T = X^T M^T
+// -- the same fragment registers with the mma operands swapped -- so that a
+// lane holds two ADJACENT elements of one group instead of one element of
+// two groups: with qubit 0 as the first element bit (targets on qubit 0,
+// where two groups are never adjacent) every store is a 2-element vector.
+template <typename Real, int KS, int STAGES, typename NZ, bool MREG, bool kDirectOut, int RBC, bool TPOSE = false>
 __device__ __forceinline__ void dmma_consumer(const DmmaParams<Real, KS>& p, Real* buf, uint64_t* full, uint64_t* empty,
                                               uint32_t stage_elems, const double* mfrag,
                                               const DmmaTileStream& stream0, int warp_rb, int wg, int lane) {
@@ -251,6 +256,13 @@ __device__ __forceinline__ void dmma_consumer(const DmmaParams<Real, KS>& p, Rea
   }
   // no target on bit 0: groups 2c, 2c+1 are adjacent, even-aligned amplitudes
   const bool pair_store = gbc[0][1] == gbc[0][0] + 1 && (gbc[0][0] & 1u) == 0 && (goffc & 1u) == 0;
+  // transposed: this lane's elements 8 rb + 2 lc (+1) of group 8 nb + lr
+  static_assert(!TPOSE || kDirectOut, "transposed products store from registers");
+  const uint64_t goffe = p.goff[8 * rb + 2 * lc];
+  const bool pair_store_t = p.goff[8 * rb + 2 * lc + 1] == goffe + 1 && (goffe & 1u) == 0;
+  uint32_t gbt[S::NR];
+#pragma unroll
+  for (int nb = 0; nb < S::NR; ++nb) gbt[nb] = dmma_group_pos(p, wg * S::GW + nb * 8 + lr);
 
   DmmaTileStream cstream = stream0;  // output addresses (ks = 5)
   uint32_t j = 0;
@@ -287,9 +299,15 @@ __device__ __forceinline__ void dmma_consumer(const DmmaParams<Real, KS>& p, Rea
       for (int nb = 0; nb < S::NR; ++nb) {
         const double br = (!kDrop || use_r || use_s) ? static_cast<double>(xr[lbb[nb] + offb[k]]) : 0.0;
         const double bi = (!kDrop || use_i || use_s) ? static_cast<double>(xi[lbb[nb] + offb[k]]) : 0.0;
-        if (use_r) dmma(t1[nb], fr, br);
-        if (use_i) dmma(t2[nb], fi, bi);
-        if (use_s) dmma(t3[nb], fs, br + bi);
+        if constexpr (TPOSE) {  // C^T = B^T A^T: the B fragment serves as A and vice versa
+          if (use_r) dmma(t1[nb], br, fr);
+          if (use_i) dmma(t2[nb], bi, fi);
+          if (use_s) dmma(t3[nb], br + bi, fs);
+        } else {
+          if (use_r) dmma(t1[nb], fr, br);
+          if (use_i) dmma(t2[nb], fi, bi);
+          if (use_s) dmma(t3[nb], fs, br + bi);
+        }
       }
     }
     if constexpr (!kDirectOut) {
@@ -312,6 +330,29 @@ __device__ __forceinline__ void dmma_consumer(const DmmaParams<Real, KS>& p, Rea
     // the results from registers (the stage is not written back)
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+    if constexpr (TPOSE) {
+      const uint64_t tbe = cstream.base() + goffe;
+      cstream.advance();
+      using V2 = std::conditional_t<sizeof(Real) == 8, double2, float2>;
+#pragma unroll
+      for (int nb = 0; nb < S::NR; ++nb) {
+        const uint64_t a = tbe + gbt[nb];
+        const Real r0 = static_cast<Real>(t1[nb][0] - t2[nb][0]), r1 = static_cast<Real>(t1[nb][1] - t2[nb][1]);
+        const Real i0 = static_cast<Real>(t3[nb][0] - t1[nb][0] - t2[nb][0]);
+        const Real i1 = static_cast<Real>(t3[nb][1] - t1[nb][1] - t2[nb][1]);
+        if (pair_store_t) {
+          *reinterpret_cast<V2*>(p.re + a) = V2{r0, r1};
+          *reinterpret_cast<V2*>(p.im + a) = V2{i0, i1};
+        } else {
+          p.re[a] = r0;
+          p.im[a] = i0;
+          const uint64_t b = a - goffe + p.goff[8 * rb + 2 * lc + 1];
+          p.re[b] = r1;
+          p.im[b] = i1;
+        }
+      }
+      continue;
+    }
     const uint64_t tb = cstream.base() + goffc;
     cstream.advance();
     if (pair_store) {  // the lane's two groups are adjacent amplitudes: one 2-element store per array
@@ -336,7 +377,7 @@ __device__ __forceinline__ void dmma_consumer(const DmmaParams<Real, KS>& p, Rea
   }
 }
 
-template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT, typename NZ>
+template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT, typename NZ, bool TPOSE = false>
 __device__ __forceinline__ void k_stream_dmma_body(const DmmaParams<Real, KS>& p) {
   using S = DShape<Real, KS>;
   constexpr bool MREG = dmma_m_in_regs<KS>();
@@ -540,21 +581,21 @@ __device__ __forceinline__ void k_stream_dmma_body(const DmmaParams<Real, KS>& p
     static_assert(S::RB <= 8, "row blocks");
 #define TSG_DMMA_RB(R)                                                                                          \
   if constexpr (S::RB > R)                                                                                      \
-    if (rb == R) return dmma_consumer<Real, KS, STAGES, NZ, MREG, kDirectOut, R>(p, buf, full, empty, stage_elems, \
+    if (rb == R) return dmma_consumer<Real, KS, STAGES, NZ, MREG, kDirectOut, R, TPOSE>(p, buf, full, empty, stage_elems, \
                                                                                 mfrag, stream0, rb, wg, lane);
     TSG_DMMA_RB(0) TSG_DMMA_RB(1) TSG_DMMA_RB(2) TSG_DMMA_RB(3) TSG_DMMA_RB(4) TSG_DMMA_RB(5) TSG_DMMA_RB(6)
     TSG_DMMA_RB(7)
 #undef TSG_DMMA_RB
   } else {
-    dmma_consumer<Real, KS, STAGES, std::conditional_t<SPARSE, DmmaRuntimeNz, DmmaDenseNz>, MREG, kDirectOut, -1>(
+    dmma_consumer<Real, KS, STAGES, std::conditional_t<SPARSE, DmmaRuntimeNz, DmmaDenseNz>, MREG, kDirectOut, -1, TPOSE>(
         p, buf, full, empty, stage_elems, mfrag, stream0, rb, wg, lane);
   }
 }
 
-template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT = false>
+template <typename Real, int KS, int STAGES, bool SPARSE, bool SIMT = false, bool TPOSE = false>
 __global__ void __launch_bounds__(DShape<Real, KS>::kThreads + 32, DShape<Real, KS>::W >= 16 ? 1 : 2)
     k_stream_dmma(const __grid_constant__ DmmaParams<Real, KS> p) {
-  k_stream_dmma_body<Real, KS, STAGES, SPARSE, SIMT, std::conditional_t<SPARSE, DmmaRuntimeNz, DmmaDenseNz>>(p);
+  k_stream_dmma_body<Real, KS, STAGES, SPARSE, SIMT, std::conditional_t<SPARSE, DmmaRuntimeNz, DmmaDenseNz>, TPOSE>(p);
 }
 
 // --------------------------------------------------------------------------

@@ -262,9 +262,10 @@ std::string pass_jit_source(int precision_bits, const PassOp* ops, int n_ops, st
   return k.str();
 }
 
-std::string dmma_jit_source(int ks, int stages, const uint32_t nz[3], std::string* name) {
+std::string dmma_jit_source(int ks, int stages, const uint32_t nz[3], bool tpose, std::string* name) {
   std::ostringstream body;
-  body << "complex128 ks=" << ks << " stages=" << stages << " nz=" << nz[0] << "," << nz[1] << "," << nz[2];
+  body << "complex128 ks=" << ks << " stages=" << stages << " nz=" << nz[0] << "," << nz[1] << "," << nz[2]
+       << (tpose ? " tpose" : "");
   const std::string key = hex16(fnv1a(body.str(), fnv1a(std::string(kJitHeaderHash) + "dmma")));
   *name = "tsg_dmma_jit_" + key;
   std::ostringstream k;
@@ -273,7 +274,7 @@ std::string dmma_jit_source(int ks, int stages, const uint32_t nz[3], std::strin
     << "tsg::DShape<double, " << ks << ">::W >= 16 ? 1 : 2) " << *name
     << "(const __grid_constant__ tsg::DmmaParams<double, " << ks << "> p) {\n"
     << "  tsg::k_stream_dmma_body<double, " << ks << ", " << stages << ", true, false, tsg::DmmaStaticNz<" << nz[0]
-    << "u, " << nz[1] << "u, " << nz[2] << "u>>(p);\n}\n";
+    << "u, " << nz[1] << "u, " << nz[2] << "u>, " << (tpose ? "true" : "false") << ">(p);\n}\n";
   return k.str();
 }
 

@@ -18,7 +18,7 @@ const void* pass_jit_kernel(const std::string& source, const std::string& name);
 
 // CUDA source of a complex128 k_stream_dmma product with its nonzero 8 x 4
 // tiles of [Mr | Mi | Mr + Mi] compiled in (DmmaStaticNz); *name = its kernel name
-std::string dmma_jit_source(int ks, int stages, const uint32_t nz[3], std::string* name);
+std::string dmma_jit_source(int ks, int stages, const uint32_t nz[3], bool tpose, std::string* name);
 // The JIT source of a full-range complex128 launch that takes the DMMA
 // stream kernel and has at least one zero tile; false otherwise (apply_f64.cu)
 bool dmma_jit_spec(const GateLaunch& g, std::string* source, std::string* name);

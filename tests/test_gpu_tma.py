@@ -59,15 +59,16 @@ def _run(mode):
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     res = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("RESULT ")][-1][7:])
-    tma = [int(tok.split("=")[1]) for ln in r.stderr.splitlines() if ln.startswith("dmma ")
-           for tok in ln.split() if tok.startswith("tma=")]
-    return res, tma
+    dbg = [ln for ln in r.stderr.splitlines() if ln.startswith("dmma ")]
+    tma = [int(tok.split("=")[1]) for ln in dbg for tok in ln.split() if tok.startswith("tma=")]
+    tpose = [int(tok.split("=")[1]) for ln in dbg for tok in ln.split() if tok.startswith("tpose=")]
+    return res, tma, tpose
 
 
 def test_dmma_tma_modes_match_oracle():
     counts = {}
     for mode in (0, 1, 3):
-        res, tma = _run(mode)
+        res, tma, tpose = _run(mode)
         for prec, targets, kind, d in res:
             assert d <= (1e-12 if prec == "f64" else 1e-5), (mode, prec, targets, kind, d)
         assert len(tma) >= 8, tma  # (controlled and permutation cases may take other kernels)
@@ -75,5 +76,7 @@ def test_dmma_tma_modes_match_oracle():
         if mode == 1:
             assert counts[1] >= 8, str(tma)  # the 5-qubit complex128 and 4-5 qubit complex64 products
             assert max(tma) > 1, tma  # scattered high targets: several tensor copies per tile
+            # targets on qubit 0 (complex128 0..4, complex64 0..4): the transposed product
+            assert sum(tpose) >= 2, tpose
     assert counts[0] == 0
     assert counts[3] >= counts[1] + 2, counts  # write-back (ks 3-4 complex128) kernels through the maps too
